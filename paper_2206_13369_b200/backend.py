@@ -1,0 +1,209 @@
+"""CUDA backends: thin objects owning a plan + its torch-allocated buffers and
+exposing the per-iteration steps of the C ABI (include/mlr_b200.h).
+
+PyTorch is used only to allocate device memory and to hand out the current
+stream; all arithmetic runs in libmlr_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class CudaPcp:
+    """Device plan for ML-PCP over one row block of the iterate."""
+
+    def __init__(self, chain, m_local, m_global, f32, max_iters, device):
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.f32 = bool(f32)
+        self.n = chain.n_fine
+        self.m_local = int(m_local)
+        self.max_iters = int(max_iters)
+        self.chain_h = chain.device_handle(self.device.index)
+        lib = self.lib
+        nbytes = lib.mlr_pcp_workspace_bytes(self.chain_h, self.m_local, int(self.f32), self.max_iters)
+        if nbytes < 0:
+            raise _lib.MlrError("mlr_pcp_workspace_bytes failed")
+        self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p()
+        _lib.check(lib.mlr_pcp_create(self.chain_h, self.m_local, int(m_global), int(self.f32), self.max_iters,
+                                      _ptr(self.ws), ctypes.byref(h)))
+        self.h = h
+        self.red = torch.zeros(int(lib.mlr_pcp_red_doubles(h)), dtype=torch.float64, device=self.device)
+        self.np_ = int(lib.mlr_chain_padded_width(self.chain_h))
+        self.stats = torch.zeros(4, dtype=torch.float64, device=self.device)
+        self.lz_w = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+
+    def close(self):
+        if self.h is not None:
+            self.lib.mlr_pcp_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def input_stats(self, D):
+        _lib.check(self.lib.mlr_pcp_input_stats(self.h, _ptr(D), D.stride(0), _ptr(self.stats), _stream()))
+        return self.stats
+
+    def lanczos_init(self):
+        _lib.check(self.lib.mlr_pcp_lanczos_init(self.h, _stream()))
+
+    def lanczos_matvec(self, D):
+        _lib.check(self.lib.mlr_pcp_lanczos_matvec(self.h, _ptr(D), D.stride(0), _ptr(self.lz_w), _stream()))
+        return self.lz_w
+
+    def lanczos_update(self, w, tol):
+        _lib.check(self.lib.mlr_pcp_lanczos_update(self.h, _ptr(w), float(tol), _stream()))
+
+    def lanczos_state(self):
+        out = np.zeros(4)
+        _lib.check(self.lib.mlr_pcp_lanczos_state(self.h, out.ctypes.data, _stream()))
+        return {"k": int(out[0]), "done": int(out[1]), "sigma1": float(out[2]), "theta": float(out[3])}
+
+    def start(self, D, Y0, lam, mu0, rho, tol, max_iters, time_budget, jac_tol, jac_max_sweeps):
+        _lib.check(self.lib.mlr_pcp_start(
+            self.h, _ptr(D), D.stride(0), _ptr(Y0), Y0.stride(0), _ptr(self.stats), float(lam),
+            float(mu0 or 0.0), float(rho), float(tol), int(max_iters), float(time_budget or 0.0),
+            float(jac_tol), int(jac_max_sweeps), _stream()))
+
+    def gram(self, with_stats):
+        _lib.check(self.lib.mlr_pcp_gram(self.h, _ptr(self.red), int(with_stats), _stream()))
+
+    def stats_slice(self):
+        nn = self.np_ * self.np_
+        return nn, nn + 3
+
+    def finalize(self):
+        _lib.check(self.lib.mlr_pcp_finalize(self.h, _ptr(self.red), _stream()))
+
+    def svt(self):
+        _lib.check(self.lib.mlr_pcp_svt(self.h, _ptr(self.red), _stream()))
+
+    def update(self, D, Yin, Yout):
+        _lib.check(self.lib.mlr_pcp_update(self.h, _ptr(D), D.stride(0), _ptr(Yin), _ptr(Yout), Yout.stride(0),
+                                           _stream()))
+
+    def outputs(self, D, Yprev, L, S):
+        _lib.check(self.lib.mlr_pcp_outputs(self.h, _ptr(D), D.stride(0), _ptr(Yprev), Yprev.stride(0), _ptr(L),
+                                            _ptr(S), L.stride(0), _stream()))
+
+    def state(self):
+        out = np.zeros(16)
+        _lib.check(self.lib.mlr_pcp_state(self.h, out.ctypes.data, _stream()))
+        keys = ("k", "done", "status", "rank", "mu", "mu_final", "mu_last", "nuclear", "sigma1", "d_norm",
+                "jac_sweeps", "tau", "scale", "lam")
+        d = dict(zip(keys, out[:len(keys)].tolist()))
+        for k in ("k", "done", "status", "rank", "jac_sweeps"):
+            d[k] = int(d[k])
+        return d
+
+    def history(self, count):
+        out = np.zeros((max(count, 1), 8))
+        _lib.check(self.lib.mlr_pcp_history(self.h, int(count), out.ctypes.data, _stream()))
+        return out[:count]
+
+    def empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+
+class CudaCpcp:
+    """Device plan for ML-CPCP over one row block."""
+
+    def __init__(self, chain, m_local, m_global, row0, f32, max_iters, world, device):
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.f32 = bool(f32)
+        self.n = chain.n_fine
+        self.m_local = int(m_local)
+        self.max_iters = int(max_iters)
+        self.chain_h = chain.device_handle(self.device.index)
+        lib = self.lib
+        nbytes = lib.mlr_cpcp_workspace_bytes(self.chain_h, self.m_local, int(self.f32), self.max_iters)
+        self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p()
+        _lib.check(lib.mlr_cpcp_create(self.chain_h, self.m_local, int(m_global), int(row0), int(self.f32),
+                                       self.max_iters, int(world), _ptr(self.ws), ctypes.byref(h)))
+        self.h = h
+        self.np_ = int(lib.mlr_chain_padded_width(self.chain_h))
+        self.red = torch.zeros(int(lib.mlr_cpcp_red_doubles(h)), dtype=torch.float64, device=self.device)
+        self.amax = torch.zeros(4, dtype=torch.float64, device=self.device)
+        self.amax_all = torch.zeros(4 * int(world), dtype=torch.float64, device=self.device)
+        self.dots = torch.zeros(3, dtype=torch.float64, device=self.device)
+        self.mstats = torch.zeros(4, dtype=torch.float64, device=self.device)
+        self.mwork = torch.zeros(int(lib.mlr_matrix_stats_work_doubles()), dtype=torch.float64, device=self.device)
+
+    def close(self):
+        if self.h is not None:
+            self.lib.mlr_cpcp_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def input_stats(self, D):
+        _lib.check(self.lib.mlr_matrix_stats(D.shape[0], D.shape[1], int(self.f32), _ptr(D), D.stride(0),
+                                             _ptr(self.mstats), _ptr(self.mwork), _stream()))
+        return self.mstats
+
+    def start(self, D, mask, S, lam_l, lam_s, tol, radius, max_iters, time_budget):
+        ldm = mask.shape[1] if mask is not None else 0
+        _lib.check(self.lib.mlr_cpcp_start(self.h, _ptr(D), D.stride(0), _ptr(mask), ldm, _ptr(S), S.stride(0),
+                                           float(lam_l), float(lam_s), float(tol), float(radius), int(max_iters),
+                                           float(time_budget or 0.0), _stream()))
+
+    def gram(self):
+        _lib.check(self.lib.mlr_cpcp_gram(self.h, _ptr(self.red), _ptr(self.amax), _stream()))
+
+    def stats_slice(self):
+        nn = self.np_ * self.np_
+        return nn, nn + 5
+
+    def begin(self):
+        _lib.check(self.lib.mlr_cpcp_begin(self.h, _ptr(self.red), _ptr(self.amax_all), _stream()))
+
+    def lmo(self):
+        _lib.check(self.lib.mlr_cpcp_lmo(self.h, _ptr(self.red), _ptr(self.amax_all), _ptr(self.dots), _stream()))
+
+    def update(self, D, mask, S):
+        ldm = mask.shape[1] if mask is not None else 0
+        _lib.check(self.lib.mlr_cpcp_update(self.h, _ptr(D), D.stride(0), _ptr(mask), ldm, _ptr(S), S.stride(0),
+                                            _ptr(self.dots), _stream()))
+
+    def finalize(self):
+        _lib.check(self.lib.mlr_cpcp_finalize(self.h, _ptr(self.red), _stream()))
+
+    def outputs(self, L):
+        _lib.check(self.lib.mlr_cpcp_outputs(self.h, _ptr(L), L.stride(0), _stream()))
+
+    def state(self):
+        out = np.zeros(32)
+        _lib.check(self.lib.mlr_cpcp_state(self.h, out.ctypes.data, _stream()))
+        keys = ("k", "done", "status", "t_l", "t_s", "u_l", "u_s", "sigma", "passes", "ga", "gb", "corner_l",
+                "corner_s", "i_s", "j_s", "s2", "pd_norm", "sq", "l1", "nnz", "ss", "sr", "r_is", "s_is", "spike",
+                "none", "coef")
+        d = dict(zip(keys, out[:len(keys)].tolist()))
+        for k in ("k", "done", "status", "passes", "corner_l", "corner_s", "i_s", "j_s", "none"):
+            d[k] = int(d[k])
+        return d
+
+    def history(self, count):
+        out = np.zeros((max(count, 1), 8))
+        objs = np.zeros(max(count, 1))
+        _lib.check(self.lib.mlr_cpcp_history(self.h, int(count), out.ctypes.data, objs.ctypes.data, _stream()))
+        return out[:count], objs[:count]
+
+    def empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)

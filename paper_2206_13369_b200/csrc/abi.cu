@@ -1,0 +1,522 @@
+// extern "C" boundary (include/mlr_b200.h): chain upload, plan creation over
+// caller workspace, and thin wrappers over the pcp.cu / cpcp.cu drivers.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mlr_b200.h"
+#include "common.cuh"
+#include "cpcp.h"
+#include "kernels.h"
+#include "pcp.h"
+
+namespace mlr {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+  return kErrCuda;
+}
+
+struct Chain {
+  ChainDev d;
+  std::vector<void*> allocs;
+};
+
+static int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// ------------------------------------------------------------ restrict / prolong
+template <typename T>
+__global__ void restrict_kernel(ChainDev ch, int64_t m, const T* __restrict__ X, int64_t ldx, T* __restrict__ out) {
+  const T* w0 = nullptr;
+  const T* w1 = nullptr;
+  if constexpr (std::is_same<T, float>::value) { w0 = ch.w0f; w1 = ch.w1f; } else { w0 = ch.w0; w1 = ch.w1; }
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    const T* row = X + i * ldx;
+    for (int k = threadIdx.x; k < ch.np; k += blockDim.x) {
+      T a = T(0);
+      if (k < ch.nh)
+        for (int j = ch.lo[k]; j < ch.hi[k]; ++j) a += row[j] * (ch.c0[j] == k ? w0[j] : w1[j]);
+      out[i * ch.np + k] = a;
+    }
+  }
+}
+
+template <typename T>
+__global__ void prolong_kernel(ChainDev ch, int64_t m, const T* __restrict__ XH, T* __restrict__ out, int64_t ldo) {
+  const T* w0 = nullptr;
+  const T* w1 = nullptr;
+  if constexpr (std::is_same<T, float>::value) { w0 = ch.w0f; w1 = ch.w1f; } else { w0 = ch.w0; w1 = ch.w1; }
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    const T* row = XH + i * ch.np;
+    for (int j = threadIdx.x; j < ch.n; j += blockDim.x) {
+      const int c = ch.c0[j];
+      T v = w0[j] * row[c];
+      if (c + 1 < ch.np) v += w1[j] * row[c + 1];
+      out[i * ldo + j] = v;
+    }
+  }
+}
+
+__global__ void eye_kernel(double* V, int np) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)np * np;
+       e += (int64_t)gridDim.x * blockDim.x)
+    V[e] = (e / np == e % np) ? 1.0 : 0.0;
+}
+
+__global__ void eig_values_kernel(int np, const double* __restrict__ X, const double* __restrict__ V,
+                                  double* __restrict__ lam) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  double s = 0.0;
+  for (int r = 0; r < np; ++r) s = fma(V[(int64_t)r * np + i], X[(int64_t)r * np + i], s);
+  lam[i] = s;
+}
+
+// ------------------------------------------------------------ workspace carving
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((char*)b) {}
+  template <typename P>
+  P* take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    P* p = base ? reinterpret_cast<P*>(base + off) : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+static void carve_pcp(PcpPlan& p, Carver& c) {
+  const int np = p.ch.np, n = p.ch.n;
+  const size_t tb = p.f32 ? 4 : 8;
+  const size_t nn = (size_t)np * np;
+  p.dev = c.take<PcpDev>(sizeof(PcpDev));
+  p.lz = c.take<LanczosDev>(sizeof(LanczosDev));
+  p.hist = c.take<double>(sizeof(double) * kHistCols * p.max_iters);
+  p.A = c.take<void>(tb * (size_t)p.m_local * np);
+  p.Z = c.take<void>(tb * (size_t)p.m_local * np);
+  p.gram_part = c.take<double>(sizeof(double) * nn * p.gram_splits);
+  p.row_part = c.take<double>(sizeof(double) * 4 * p.row_blocks);
+  p.T1 = c.take<double>(8 * nn);
+  p.Bm = c.take<double>(8 * nn);
+  p.Xm = c.take<double>(8 * nn);
+  p.Vm = c.take<double>(8 * nn);
+  p.Wm = c.take<double>(8 * nn);
+  p.sig = c.take<double>(8 * np);
+  p.fw = c.take<double>(8 * np);
+  p.jac_partials = c.take<double>(8 * (size_t)jacobi_partials_doubles(np));
+  p.jac_off = c.take<double>(8 * 2);
+  p.jac_result = c.take<int>(4 * 4);
+  p.lzQ = c.take<double>(8 * (size_t)n * (p.lz_kmax + 1));
+  p.lzT = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
+  p.lzW = c.take<double>(8 * (size_t)n * p.lz_splits);
+  p.lzWork = c.take<double>(8 * (size_t)n);
+}
+
+static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t m_global, int f32, int max_iters) {
+  p = PcpPlan{};
+  p.ch = ch;
+  p.f32 = f32 != 0;
+  p.m_local = m_local;
+  p.m_global = m_global;
+  p.max_iters = max_iters;
+  const int sms = sm_count();
+  p.row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m_local, (int64_t)sms * 8));
+  const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64);
+  int64_t splits = ceil_div(2 * sms, tiles);
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
+  p.gram_splits = (int)std::max<int64_t>(1, splits);
+  const int64_t col_blocks = ceil_div(ch.n, 128);
+  int64_t ls = ceil_div(2 * sms, col_blocks);
+  ls = std::min<int64_t>(ls, std::max<int64_t>(1, m_local / 32));
+  p.lz_splits = (int)std::max<int64_t>(1, ls);
+  p.lz_kmax = std::min(500, std::max(8, ch.n));
+  p.jac_tol_host = 1e-14;
+  p.jac_max_sweeps = 60;
+}
+
+static void carve_cpcp(CpcpPlan& p, Carver& c) {
+  const int np = p.ch.np;
+  const size_t tb = p.f32 ? 4 : 8;
+  const size_t nn = (size_t)np * np;
+  p.dev = c.take<CpcpDev>(sizeof(CpcpDev));
+  p.hist = c.take<double>(sizeof(double) * kCpHistCols * p.max_iters);
+  p.obj = c.take<double>(sizeof(double) * p.max_iters);
+  p.LH = c.take<void>(tb * (size_t)p.m_local * np);
+  p.GH = c.take<void>(tb * (size_t)p.m_local * np);
+  p.SH = c.take<void>(tb * (size_t)p.m_local * np);
+  p.u = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
+  p.v = c.take<double>(8 * np);
+  p.vin = c.take<double>(8 * np);
+  p.gram_part = c.take<double>(8 * nn * p.gram_splits);
+  p.row_part = c.take<double>(8 * 9 * (size_t)p.row_blocks);
+  p.dots_part = c.take<double>(8 * 3 * (size_t)p.row_blocks);
+}
+
+static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t m_global, int64_t row0, int f32,
+                        int max_iters, int world) {
+  p = CpcpPlan{};
+  p.ch = ch;
+  p.f32 = f32 != 0;
+  p.m_local = m_local;
+  p.m_global = m_global;
+  p.row0 = row0;
+  p.max_iters = max_iters;
+  p.world = world;
+  const int sms = sm_count();
+  p.row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m_local, (int64_t)sms * 8));
+  const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64);
+  int64_t splits = ceil_div(2 * sms, tiles);
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
+  p.gram_splits = (int)std::max<int64_t>(1, splits);
+  p.cluster = ch.np >= 256 ? 16 : 8;
+}
+
+}  // namespace mlr
+
+using namespace mlr;
+
+extern "C" {
+
+int mlr_version(void) { return 1; }
+const char* mlr_last_error(void) { return g_err.c_str(); }
+int mlr_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int mlr_chain_create(int n, int nh, const int32_t* c0, const double* w0, const double* w1, const double* g_diag,
+                     const double* g_off, void** chain_out) {
+  if (n < 1 || nh < 1 || nh > n || !c0 || !w0 || !w1 || !g_diag || !chain_out) {
+    set_error("mlr_chain_create: invalid arguments");
+    return kErrArg;
+  }
+  const int np = (int)round_up(nh, 64);
+  std::vector<int> lo(nh, n), hi(nh, 0);
+  for (int j = 0; j < n; ++j) {
+    const int c = c0[j];
+    if (c < 0 || c >= nh || (w1[j] != 0.0 && c + 1 >= nh)) {
+      set_error("mlr_chain_create: stencil index out of range");
+      return kErrArg;
+    }
+    if (j > 0 && c < c0[j - 1]) {
+      set_error("mlr_chain_create: stencil columns must be non-decreasing");
+      return kErrArg;
+    }
+    lo[c] = std::min(lo[c], j);
+    hi[c] = std::max(hi[c], j + 1);
+    if (w1[j] != 0.0) {
+      lo[c + 1] = std::min(lo[c + 1], j);
+      hi[c + 1] = std::max(hi[c + 1], j + 1);
+    }
+  }
+  int span = 0;
+  for (int k = 0; k < nh; ++k) {
+    if (hi[k] <= lo[k]) {
+      lo[k] = 0;
+      hi[k] = 0;
+    }
+    span = std::max(span, hi[k] - lo[k]);
+  }
+  // LDL^T of the SPD tridiagonal G_R
+  std::vector<double> gl(std::max(nh - 1, 1), 0.0), gd(nh);
+  gd[0] = g_diag[0];
+  for (int k = 1; k < nh; ++k) {
+    gl[k - 1] = g_off[k - 1] / gd[k - 1];
+    gd[k] = g_diag[k] - gl[k - 1] * g_off[k - 1];
+  }
+  for (int k = 0; k < nh; ++k)
+    if (!(gd[k] > 0.0)) {
+      set_error("mlr_chain_create: R^T R is not positive definite");
+      return kErrArg;
+    }
+  std::vector<float> w0f(n), w1f(n);
+  for (int j = 0; j < n; ++j) {
+    w0f[j] = (float)w0[j];
+    w1f[j] = (float)w1[j];
+  }
+  Chain* ch = new Chain();
+  ChainDev& d = ch->d;
+  d.n = n;
+  d.nh = nh;
+  d.np = np;
+  d.max_span = span;
+  auto up = [&](void** dst, const void* src, size_t bytes) -> int {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 8));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(chain)");
+    ch->allocs.push_back(p);
+    e = cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(chain)");
+    *dst = p;
+    return kOk;
+  };
+  int rc = 0;
+  std::vector<int> c0v(c0, c0 + n);
+  rc |= up((void**)&d.c0, c0v.data(), sizeof(int) * n);
+  rc |= up((void**)&d.w0, w0, sizeof(double) * n);
+  rc |= up((void**)&d.w1, w1, sizeof(double) * n);
+  rc |= up((void**)&d.w0f, w0f.data(), sizeof(float) * n);
+  rc |= up((void**)&d.w1f, w1f.data(), sizeof(float) * n);
+  rc |= up((void**)&d.lo, lo.data(), sizeof(int) * nh);
+  rc |= up((void**)&d.hi, hi.data(), sizeof(int) * nh);
+  rc |= up((void**)&d.gl, gl.data(), sizeof(double) * gl.size());
+  rc |= up((void**)&d.gd, gd.data(), sizeof(double) * nh);
+  if (rc) {
+    for (void* p : ch->allocs) cudaFree(p);
+    delete ch;
+    return kErrCuda;
+  }
+  *chain_out = ch;
+  return kOk;
+}
+
+int mlr_chain_destroy(void* chain) {
+  if (!chain) return kOk;
+  Chain* ch = (Chain*)chain;
+  for (void* p : ch->allocs) cudaFree(p);
+  delete ch;
+  return kOk;
+}
+
+int mlr_chain_padded_width(void* chain) { return chain ? ((Chain*)chain)->d.np : 0; }
+
+int mlr_restrict(void* chain, int64_t m, int f32, const void* X, int64_t ldx, void* out, void* stream) {
+  if (!chain || m < 0) { set_error("mlr_restrict: invalid arguments"); return kErrArg; }
+  if (m == 0) return kOk;
+  const ChainDev& ch = ((Chain*)chain)->d;
+  int blocks = (int)std::min<int64_t>(m, sm_count() * 8);
+  if (f32) restrict_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(ch, m, (const float*)X, ldx, (float*)out);
+  else restrict_kernel<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(ch, m, (const double*)X, ldx, (double*)out);
+  MLR_LAUNCH_CHECK("restrict_kernel");
+  return kOk;
+}
+
+int mlr_prolong(void* chain, int64_t m, int f32, const void* XH, void* out, int64_t ldo, void* stream) {
+  if (!chain || m < 0) { set_error("mlr_prolong: invalid arguments"); return kErrArg; }
+  if (m == 0) return kOk;
+  const ChainDev& ch = ((Chain*)chain)->d;
+  int blocks = (int)std::min<int64_t>(m, sm_count() * 8);
+  if (f32) prolong_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(ch, m, (const float*)XH, (float*)out, ldo);
+  else prolong_kernel<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(ch, m, (const double*)XH, (double*)out, ldo);
+  MLR_LAUNCH_CHECK("prolong_kernel");
+  return kOk;
+}
+
+int64_t mlr_matrix_stats_work_doubles(void) { return 3 * 148 * 8 + 64; }
+
+int mlr_matrix_stats(int64_t m, int n, int f32, const void* D, int64_t ldd, double* out3, double* work,
+                     void* stream) {
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m, 148 * 8));
+  return matrix_stats(m, n, f32 != 0, D, ldd, work, blocks, out3, (cudaStream_t)stream);
+}
+
+int64_t mlr_eigh_work_doubles(int np) { return (int64_t)np * np + jacobi_partials_doubles(np) + 64; }
+
+int mlr_eigh_psd(int np, const double* B, double* V, double* lam, double tol, int max_sweeps, double* work,
+                 int* info, void* stream) {
+  if (np <= 0 || np % 64) { set_error("mlr_eigh_psd: np must be a positive multiple of 64"); return kErrArg; }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* X = work;
+  double* part = work + (int64_t)np * np;
+  double* off = part + jacobi_partials_doubles(np);
+  int* res = (int*)(off + 4);
+  MLR_CUDA(cudaMemcpyAsync(X, B, sizeof(double) * np * np, cudaMemcpyDeviceToDevice, st));
+  eye_kernel<<<256, 256, 0, st>>>(V, np);
+  MLR_LAUNCH_CHECK("eye_kernel");
+  int rc = jacobi_eig(X, V, np, tol, max_sweeps, part, off, res, nullptr, st);
+  if (rc) return rc;
+  eig_values_kernel<<<(np + 127) / 128, 128, 0, st>>>(np, X, V, lam);
+  MLR_LAUNCH_CHECK("eig_values_kernel");
+  MLR_CUDA(cudaMemcpyAsync(info, res, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MLR_CUDA(cudaStreamSynchronize(st));
+  return kOk;
+}
+
+// ---------------------------------------------------------------- PCP
+int64_t mlr_pcp_workspace_bytes(void* chain, int64_t m_local, int f32, int max_iters) {
+  if (!chain) return -1;
+  PcpPlan p;
+  pcp_params(p, ((Chain*)chain)->d, m_local, m_local, f32, max_iters);
+  Carver c(nullptr);
+  carve_pcp(p, c);
+  return (int64_t)c.off + 256;
+}
+
+int mlr_pcp_create(void* chain, int64_t m_local, int64_t m_global, int f32, int max_iters, void* workspace,
+                   void** plan_out) {
+  if (!chain || !workspace || !plan_out || m_local < 0 || m_global < 1 || max_iters < 1) {
+    set_error("mlr_pcp_create: invalid arguments");
+    return kErrArg;
+  }
+  PcpPlan* p = new PcpPlan();
+  pcp_params(*p, ((Chain*)chain)->d, m_local, m_global, f32, max_iters);
+  Carver c(workspace);
+  carve_pcp(*p, c);
+  eye_kernel<<<256, 256>>>(p->Vm, p->ch.np);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "mlr_pcp_create");
+  }
+  *plan_out = p;
+  return kOk;
+}
+
+int mlr_pcp_destroy(void* plan) {
+  delete (PcpPlan*)plan;
+  return kOk;
+}
+
+int64_t mlr_pcp_red_doubles(void* plan) {
+  PcpPlan* p = (PcpPlan*)plan;
+  return std::max<int64_t>((int64_t)p->ch.np * p->ch.np + 8, p->ch.n + 8);
+}
+
+#define PLAN ((PcpPlan*)plan)
+#define STREAM ((cudaStream_t)stream)
+
+int mlr_pcp_input_stats(void* plan, const void* D, int64_t ldd, double* out2, void* stream) {
+  return pcp_input_stats(PLAN, D, ldd, out2, STREAM);
+}
+int mlr_pcp_lanczos_init(void* plan, void* stream) { return pcp_lanczos_init(PLAN, STREAM); }
+int mlr_pcp_lanczos_matvec(void* plan, const void* D, int64_t ldd, double* w_part, void* stream) {
+  return pcp_lanczos_matvec(PLAN, D, ldd, w_part, STREAM);
+}
+int mlr_pcp_lanczos_update(void* plan, const double* w, double tol, void* stream) {
+  return pcp_lanczos_update(PLAN, w, tol, STREAM);
+}
+int mlr_pcp_lanczos_state(void* plan, double* out4, void* stream) {
+  LanczosDev h;
+  MLR_CUDA(cudaMemcpyAsync(&h, PLAN->lz, sizeof(LanczosDev), cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaStreamSynchronize(STREAM));
+  out4[0] = h.k;
+  out4[1] = h.done;
+  out4[2] = h.sigma1;
+  out4[3] = h.theta;
+  return kOk;
+}
+int mlr_pcp_start(void* plan, const void* D, int64_t ldd, void* Y0, int64_t ldy, const double* in_stats, double lam,
+                  double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
+                  int jac_max_sweeps, void* stream) {
+  if (max_iters > PLAN->max_iters) {
+    set_error("mlr_pcp_start: max_iters exceeds the plan's history capacity");
+    return kErrArg;
+  }
+  PLAN->jac_max_sweeps = jac_max_sweeps;
+  return pcp_start(PLAN, D, ldd, Y0, ldy, in_stats, lam, mu0, rho, tol, max_iters, time_budget, jac_tol, STREAM);
+}
+int mlr_pcp_gram(void* plan, double* red, int with_stats, void* stream) {
+  return pcp_gram(PLAN, red, with_stats, STREAM);
+}
+int mlr_pcp_finalize(void* plan, const double* red, void* stream) { return pcp_finalize(PLAN, red, STREAM); }
+int mlr_pcp_svt(void* plan, const double* red, void* stream) { return pcp_svt(PLAN, red, STREAM); }
+int mlr_pcp_update(void* plan, const void* D, int64_t ldd, const void* Y_in, void* Y_out, int64_t ldy, void* stream) {
+  return pcp_update(PLAN, D, ldd, Y_in, Y_out, ldy, STREAM);
+}
+int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, int64_t ldy, void* L, void* S,
+                    int64_t ldo, void* stream) {
+  return pcp_outputs(PLAN, D, ldd, Y_prev, ldy, L, S, ldo, STREAM);
+}
+int mlr_pcp_state(void* plan, double* out16, void* stream) {
+  PcpDev h;
+  MLR_CUDA(cudaMemcpyAsync(&h, PLAN->dev, sizeof(PcpDev), cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaStreamSynchronize(STREAM));
+  double v[16] = {(double)h.k, (double)h.done, (double)h.status, (double)h.rank, h.mu, h.mu_final, h.mu_last,
+                  h.nuclear, h.sigma1, h.d_norm, (double)h.jac_sweeps, h.tau, h.scale, h.lam, 0.0, 0.0};
+  std::memcpy(out16, v, sizeof(v));
+  return kOk;
+}
+int mlr_pcp_history(void* plan, int count, double* out, void* stream) {
+  if (count < 0 || count > PLAN->max_iters) { set_error("mlr_pcp_history: bad count"); return kErrArg; }
+  MLR_CUDA(cudaMemcpyAsync(out, PLAN->hist, sizeof(double) * kHistCols * count, cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaStreamSynchronize(STREAM));
+  return kOk;
+}
+#undef PLAN
+
+// ---------------------------------------------------------------- CPCP
+#define PLAN ((CpcpPlan*)plan)
+int64_t mlr_cpcp_workspace_bytes(void* chain, int64_t m_local, int f32, int max_iters) {
+  if (!chain) return -1;
+  CpcpPlan p;
+  cpcp_params(p, ((Chain*)chain)->d, m_local, m_local, 0, f32, max_iters, 1);
+  Carver c(nullptr);
+  carve_cpcp(p, c);
+  return (int64_t)c.off + 256;
+}
+int mlr_cpcp_create(void* chain, int64_t m_local, int64_t m_global, int64_t row0, int f32, int max_iters, int world,
+                    void* workspace, void** plan_out) {
+  if (!chain || !workspace || !plan_out || m_local < 0 || m_global < 1 || max_iters < 1 || world < 1) {
+    set_error("mlr_cpcp_create: invalid arguments");
+    return kErrArg;
+  }
+  CpcpPlan* p = new CpcpPlan();
+  cpcp_params(*p, ((Chain*)chain)->d, m_local, m_global, row0, f32, max_iters, world);
+  if (p->ch.np % p->cluster) {
+    delete p;
+    set_error("mlr_cpcp_create: coarse width not divisible by the cluster size");
+    return kErrArg;
+  }
+  Carver c(workspace);
+  carve_cpcp(*p, c);
+  *plan_out = p;
+  return kOk;
+}
+int mlr_cpcp_destroy(void* plan) {
+  delete (CpcpPlan*)plan;
+  return kOk;
+}
+int64_t mlr_cpcp_red_doubles(void* plan) { return (int64_t)PLAN->ch.np * PLAN->ch.np + 8; }
+int mlr_cpcp_start(void* plan, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
+                   double lambda_l, double lambda_s, double tol, double radius, int max_iters, double time_budget,
+                   void* stream) {
+  if (max_iters > PLAN->max_iters) {
+    set_error("mlr_cpcp_start: max_iters exceeds the plan's history capacity");
+    return kErrArg;
+  }
+  return cpcp_start(PLAN, D, ldd, mask, ldm, S, lds, lambda_l, lambda_s, tol, radius, max_iters, time_budget,
+                    STREAM);
+}
+int mlr_cpcp_gram(void* plan, double* red, double* amax, void* stream) { return cpcp_gram(PLAN, red, amax, STREAM); }
+int mlr_cpcp_begin(void* plan, const double* red, const double* amax_all, void* stream) {
+  return cpcp_begin(PLAN, red, amax_all, STREAM);
+}
+int mlr_cpcp_lmo(void* plan, const double* red, const double* amax_all, double* dots, void* stream) {
+  return cpcp_lmo(PLAN, red, amax_all, dots, STREAM);
+}
+int mlr_cpcp_update(void* plan, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
+                    const double* dots, void* stream) {
+  return cpcp_update(PLAN, D, ldd, mask, ldm, S, lds, dots, STREAM);
+}
+int mlr_cpcp_finalize(void* plan, const double* red, void* stream) { return cpcp_finalize(PLAN, red, STREAM); }
+int mlr_cpcp_outputs(void* plan, void* L, int64_t ldl, void* stream) { return cpcp_outputs(PLAN, L, ldl, STREAM); }
+int mlr_cpcp_state(void* plan, double* out32, void* stream) {
+  CpcpDev h;
+  MLR_CUDA(cudaMemcpyAsync(&h, PLAN->dev, sizeof(CpcpDev), cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaStreamSynchronize(STREAM));
+  double v[32] = {(double)h.k, (double)h.done, (double)h.status, h.t_l, h.t_s, h.u_l, h.u_s, h.sigma,
+                  (double)h.passes, h.ga, h.gb, (double)h.corner_l, (double)h.corner_s, (double)h.i_s,
+                  (double)h.j_s, h.s2, h.pd_norm, h.sq, h.l1, h.nnz, h.ss, h.sr, h.r_is, h.s_is, h.spike,
+                  (double)h.none, h.coef, 0, 0, 0, 0, 0};
+  std::memcpy(out32, v, sizeof(v));
+  return kOk;
+}
+int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, void* stream) {
+  if (count < 0 || count > PLAN->max_iters) { set_error("mlr_cpcp_history: bad count"); return kErrArg; }
+  MLR_CUDA(cudaMemcpyAsync(out, PLAN->hist, sizeof(double) * kCpHistCols * count, cudaMemcpyDeviceToHost, STREAM));
+  if (objectives)
+    MLR_CUDA(cudaMemcpyAsync(objectives, PLAN->obj, sizeof(double) * count, cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaStreamSynchronize(STREAM));
+  return kOk;
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// Device state and plan for ML-CPCP (multilevel Frank-Wolfe thresholding).
+#pragma once
+#include "kernels.h"
+
+namespace mlr {
+
+constexpr int kCpHistCols = 8;  // gap, objective, rank, sparsity, wall, gamma_l, gamma_s, power passes
+constexpr int kCpStats = 5;     // sum r^2, sum |S|, nnz(S), sum S^2, sum S*r
+
+struct CpcpDev {
+  double lam_l, lam_s, tol, radius, time_budget, t0_ns, m_global, n, rtol;
+  double u_l, u_s, t_l, t_s, pd_norm;
+  // stats of the latest fine pass (after reduction)
+  double sq, l1, nnz, ss, sr;
+  // LMO of the current iteration
+  double s2, sigma, coef;   // coef = -radius * u_l if corner_l else 0
+  int corner_l, corner_s, none, passes;
+  double spike, r_is, s_is, v_tl, v_ts;
+  long long idx_is;         // column-major global index of the arg-max (-1: none)
+  long long i_s;            // global row of the arg-max
+  int j_s;
+  double ga, gb;
+  int k, done, status, max_iters, max_passes;
+};
+
+struct CpcpPlan {
+  ChainDev ch;
+  bool f32;
+  int64_t m_local, m_global, row0;
+  int max_iters, row_blocks, gram_splits, world, cluster;
+  CpcpDev* dev;
+  double* hist;      // [max_iters][kCpHistCols]
+  double* obj;       // [max_iters]
+  void* LH;          // m_local x np (T)
+  void* GH;          // m_local x np (T): r R
+  void* SH;          // m_local x np (T): S R
+  double* u;         // m_local
+  double* v;         // np (warm start)
+  double* vin;       // np
+  double* gram_part; // gram_splits x np x np
+  double* row_part;  // row_blocks x 8 (stats) + row_blocks x 4 (argmax)
+  double* dots_part; // row_blocks x 3
+  const uint32_t* mask_dev;  // bound at start (may be null: fully observed)
+  int64_t ldm_dev;
+};
+
+int cpcp_start(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
+               double lam_l, double lam_s, double tol, double radius, int max_iters, double time_budget,
+               cudaStream_t st);
+int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st);
+int cpcp_begin(CpcpPlan* p, const double* red, const double* amax_all, cudaStream_t st);
+int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dots, cudaStream_t st);
+int cpcp_update(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
+                const double* dots, cudaStream_t st);
+int cpcp_finalize(CpcpPlan* p, const double* red, cudaStream_t st);
+int cpcp_outputs(CpcpPlan* p, void* L, int64_t ldl, cudaStream_t st);
+
+}  // namespace mlr

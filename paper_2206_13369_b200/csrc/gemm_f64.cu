@@ -1,0 +1,182 @@
+// FP64-accumulating GEMMs for the coarse level (Gram, reconstruction, small
+// n_H x n_H products) on the DMMA tensor path (mma.sync m8n8k4 .f64).
+//
+// C[M x N] = op(A)[M x K] * op(B)[K x N], row-major storage, inputs float or
+// double (converted to double when staged into shared memory), output float
+// or double.  gridDim.z > 1 splits K; slice z writes C + z * c_slice and a
+// separate deterministic reduction sums the slices.
+//
+// Replaces the reference's numpy GEMMs / LAPACK calls:
+//   Gram K = A^T A          (stands in for gesdd inside svd_full, linalg.py:86-99)
+//   Z = A * W               (reconstruction, pcp.py:259-266)
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mlr {
+
+constexpr int GBM = 64, GBN = 64, GBK = 16, GPAD = 8;
+constexpr int GTHREADS = 128;  // 4 warps, 2x2, each 32x32
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+template <typename TA, typename TB, typename TC, bool TRANS_A, bool TRANS_B>
+__global__ void __launch_bounds__(GTHREADS)
+gemm_f64_kernel(int M, int N, int K, const TA* __restrict__ A, int64_t lda,
+                const TB* __restrict__ B, int64_t ldb, TC* __restrict__ C, int64_t ldc,
+                int64_t c_slice, int k_chunk, double alpha, const double* __restrict__ kscale,
+                const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double As[2][GBK][GBM + GPAD];
+  __shared__ double Bs[2][GBK][GBN + GPAD];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  const int kb = blockIdx.z * k_chunk;
+  const int ke = min(K, kb + k_chunk);
+  C += (int64_t)blockIdx.z * c_slice;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Each thread stages 8 elements of A and 8 of B per K-tile (64x16 = 1024).
+  double ra[8], rb[8];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int idx = tid + e * GTHREADS;  // 0..1023
+      int kk, mm;
+      if (TRANS_A) {  // A stored K x M: coalesce along m
+        kk = idx >> 6; mm = idx & 63;
+      } else {        // A stored M x K: coalesce along k
+        mm = idx >> 4; kk = idx & 15;
+      }
+      int gk = k0 + kk, gm = m0 + mm;
+      double v = 0.0;
+      if (gk < ke && gm < M) {
+        v = TRANS_A ? (double)A[(int64_t)gk * lda + gm] : (double)A[(int64_t)gm * lda + gk];
+        if (kscale) v *= kscale[gk];
+      }
+      ra[e] = v;
+      int nn;
+      if (TRANS_B) { nn = idx >> 4; kk = idx & 15; }   // B stored N x K
+      else { kk = idx >> 6; nn = idx & 63; }           // B stored K x N
+      gk = k0 + kk;
+      int gn = n0 + nn;
+      double w = 0.0;
+      if (gk < ke && gn < N) w = TRANS_B ? (double)B[(int64_t)gn * ldb + gk] : (double)B[(int64_t)gk * ldb + gn];
+      rb[e] = w;
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int idx = tid + e * GTHREADS;
+      int kk, mm, nn;
+      if (TRANS_A) { kk = idx >> 6; mm = idx & 63; } else { mm = idx >> 4; kk = idx & 15; }
+      As[buf][kk][mm] = ra[e];
+      if (TRANS_B) { nn = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; nn = idx & 63; }
+      Bs[buf][kk][nn] = rb[e];
+    }
+  };
+
+  int ntiles = (ke - kb + GBK - 1) / GBK;
+  if (ntiles <= 0) ntiles = 0;
+  if (ntiles > 0) {
+    load_tile(kb);
+    store_tile(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < ntiles) load_tile(kb + (t + 1) * GBK);
+#pragma unroll
+    for (int k4 = 0; k4 < GBK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][k4 + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][k4 + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (t + 1 < ntiles) store_tile(buf ^ 1);
+    __syncthreads();
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gm = m0 + wm + i * 8 + (lane >> 2);
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gn = n0 + wn + j * 8 + (lane & 3) * 2;
+      if (gn < N) C[(int64_t)gm * ldc + gn] = (TC)(alpha * acc[i][j][0]);
+      if (gn + 1 < N) C[(int64_t)gm * ldc + gn + 1] = (TC)(alpha * acc[i][j][1]);
+    }
+  }
+}
+
+// Deterministic sum of `slices` partial matrices (contiguous, stride `slice`).
+__global__ void sum_slices_kernel(const double* __restrict__ P, int64_t count, int64_t slice,
+                                  int slices, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < slices; ++z) s += P[z * slice + i];
+    out[i] = s;
+  }
+}
+
+template <typename TA, typename TB, typename TC, bool TA_, bool TB_>
+static int launch(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  void* C, int64_t ldc, int64_t c_slice, int splits, double alpha, const double* kscale,
+                  const int* skip, cudaStream_t st) {
+  dim3 grid((N + GBN - 1) / GBN, (M + GBM - 1) / GBM, splits);
+  int chunk = (int)round_up(ceil_div(K, splits), GBK);
+  gemm_f64_kernel<TA, TB, TC, TA_, TB_><<<grid, GTHREADS, 0, st>>>(
+      M, N, K, (const TA*)A, lda, (const TB*)B, ldb, (TC*)C, ldc, c_slice, chunk, alpha, kscale, skip);
+  MLR_LAUNCH_CHECK("gemm_f64_kernel");
+  return kOk;
+}
+
+int gemm_f64(GemmSpec g, cudaStream_t st) {
+  // dispatch on (A type, B type, C type, transA, transB)
+#define MLR_G(TA, TB, TC, XA, XB)                                                              \
+  if (g.a_f32 == std::is_same<TA, float>::value && g.b_f32 == std::is_same<TB, float>::value && \
+      g.c_f32 == std::is_same<TC, float>::value && g.trans_a == XA && g.trans_b == XB)            \
+    return launch<TA, TB, TC, XA, XB>(g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.C, g.ldc,         \
+                                      g.c_slice, g.splits, g.alpha, g.kscale, g.skip, st);
+  // Gram: A^T A with A float or double, C double
+  MLR_G(float, float, double, true, false)
+  MLR_G(double, double, double, true, false)
+  // reconstruction Z = A W: A float/double, W double, C float/double
+  MLR_G(float, double, float, false, false)
+  MLR_G(double, double, double, false, false)
+  // coarse products (double only): NN, NT
+  MLR_G(double, double, double, false, true)
+#undef MLR_G
+  set_error("gemm_f64: unsupported type/transpose combination");
+  return kErrArg;
+}
+
+int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out,
+               cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 8);
+  if (blocks < 1) blocks = 1;
+  sum_slices_kernel<<<blocks, 256, 0, st>>>(P, count, slice, slices, out);
+  MLR_LAUNCH_CHECK("sum_slices_kernel");
+  return kOk;
+}
+
+}  // namespace mlr

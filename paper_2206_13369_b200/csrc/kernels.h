@@ -1,0 +1,55 @@
+// Internal (C++) interfaces between the ABI layer and the kernel files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <type_traits>
+
+namespace mlr {
+
+void set_error(const std::string& msg);
+
+// ---------------------------------------------------------------- gemm
+struct GemmSpec {
+  int M, N, K;
+  const void* A; int64_t lda; bool a_f32; bool trans_a;
+  const void* B; int64_t ldb; bool b_f32; bool trans_b;
+  void* C; int64_t ldc; bool c_f32;
+  int64_t c_slice;  // elements between split-K slices of C
+  int splits;
+  double alpha;
+  const double* kscale;  // optional: op(A)[:, k] *= kscale[k]
+  const int* skip;       // optional device flag: kernel is a no-op when *skip != 0
+};
+int gemm_f64(GemmSpec g, cudaStream_t st);
+int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- jacobi
+int jacobi_block_width(int np);
+int64_t jacobi_partials_doubles(int np);
+int jacobi_eig(double* X, double* V, int np, double tol, int max_sweeps, double* partials,
+               double* off_slots, int* result, const int* skip, cudaStream_t st);
+
+// ---------------------------------------------------------------- chain
+// Composite restriction R (n x n_h) in stencil form.  Fine column j has
+// weight w0[j] on coarse column c0[j] and w1[j] on c0[j]+1 (w1 may be 0);
+// coarse column k gathers fine columns [lo[k], hi[k]).
+struct ChainDev {
+  int n, nh, np;        // np = n_h rounded up to 64
+  int* c0;              // [n]
+  double* w0; double* w1;
+  float* w0f; float* w1f;
+  int* lo; int* hi;     // [nh]
+  double* gl;           // LDL^T of G_R = R^T R: multipliers l[k], k < nh-1
+  double* gd;           // pivots d[k]
+  int max_span;         // max hi-lo
+};
+
+int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out, int trans_in,
+              cudaStream_t st);
+int svt_weights(const int* skip, int np, int nh, const double* X, const double* V, const double* tau,
+                double* sig_out, double* f_out, int* rank_out, double* nuclear_out, cudaStream_t st);
+
+}  // namespace mlr

@@ -1,0 +1,640 @@
+// ML-PCP (multilevel inexact ALM, reference pcp.py:213-309) on the device.
+//
+// Fine planes are row-major m_local x n (T = float or double).  Coarse
+// matrices A (= W R) and Z (= A W~) are m_local x np (np = n_H rounded up to
+// 64, zero padded).  The fused row kernel does, for one fine row at a time:
+//     L   = Z_i R^T                     (prolongation stencil, pcp.py:266)
+//     S   = shrink(D - L + Y/mu, lam/mu) (pcp.py:272-275)
+//     res = D - L - S; Y' = Y + mu res   (pcp.py:277-281) + reductions
+//     A'  = (D - S + Y'/(rho mu)) R      (next iteration's restriction,
+//                                        pcp.py:252-255) via a gather stencil
+// so each iteration reads D and Y once and writes Y once (plus m x n_H for
+// Z and A').  S is never stored: it is recomputed at exit from the previous
+// Y (double-buffered by the host).
+#include "common.cuh"
+#include "kernels.h"
+#include "pcp.h"
+
+namespace mlr {
+
+__device__ __forceinline__ double global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (double)t;
+}
+
+// ------------------------------------------------------------ input stats
+template <typename T>
+__global__ void input_stats_kernel(const T* __restrict__ D, int64_t ldd, int64_t m, int n,
+                                   double* __restrict__ part) {
+  // ||D||_F^2, max|D| and the count of non-finite entries (as_matrix's
+  // finiteness check, linalg.py:55-56)
+  __shared__ double scratch[2 * 32];
+  double s = 0.0, mx = 0.0, bad = 0.0;
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    const T* row = D + i * ldd;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double v = (double)row[j];
+      if (!isfinite(v)) {
+        bad += 1.0;
+        continue;
+      }
+      s = fma(v, v, s);
+      mx = fmax(mx, fabs(v));
+    }
+  }
+  mx = warp_max(mx);
+  __shared__ double smx[32];
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+  double v[2] = {s, bad};
+  block_sum<2>(v, scratch);
+  if (threadIdx.x == 0) {
+    double m2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m2 = fmax(m2, smx[w]);
+    part[3 * blockIdx.x] = v[0];
+    part[3 * blockIdx.x + 1] = m2;
+    part[3 * blockIdx.x + 2] = v[1];
+  }
+}
+
+__global__ void input_stats_finish(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0, mx = 0.0, bad = 0.0;
+    for (int b = 0; b < nparts; ++b) {
+      s += part[3 * b];
+      mx = fmax(mx, part[3 * b + 1]);
+      bad += part[3 * b + 2];
+    }
+    out[0] = s;
+    out[1] = mx;
+    out[2] = bad;
+  }
+}
+
+// ------------------------------------------------------------ Lanczos on D^T D
+// sigma_1(D) (pcp.py:100 and :114 call np.linalg.norm(d, 2), a full SVD;
+// Lanczos with full reorthogonalisation reaches ~1e-15 relative).
+__global__ void lz_init_kernel(LanczosDev* lz, double* Q, int n, int kmax) {
+  const double v = 1.0 / sqrt((double)n);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) Q[j] = v;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    lz->k = 0;
+    lz->done = 0;
+    lz->kmax = kmax;
+    lz->theta = 0.0;
+    lz->theta_prev = 0.0;
+    lz->stable = 0;
+    lz->sigma1 = 0.0;
+  }
+}
+
+template <typename T>
+__global__ void lz_dv_kernel(const LanczosDev* __restrict__ lz, const T* __restrict__ D, int64_t ldd,
+                             int64_t m, int n, const double* __restrict__ Q, double* __restrict__ t) {
+  if (lz->done) return;
+  __shared__ double scratch[32];
+  const double* q = Q + (int64_t)lz->k * n;
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    const T* row = D + i * ldd;
+    double s = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) s = fma((double)row[j], q[j], s);
+    double v[1] = {s};
+    block_sum<1>(v, scratch);
+    if (threadIdx.x == 0) t[i] = v[0];
+  }
+}
+
+template <typename T>
+__global__ void lz_dtv_kernel(const LanczosDev* __restrict__ lz, const T* __restrict__ D, int64_t ldd,
+                              int64_t m, int n, const double* __restrict__ t, double* __restrict__ wpart,
+                              int64_t rows_per_split) {
+  if (lz->done) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = blockIdx.y * rows_per_split;
+  const int64_t r1 = min(m, r0 + rows_per_split);
+  if (j >= n) return;
+  double s = 0.0;
+  for (int64_t i = r0; i < r1; ++i) s = fma((double)D[i * ldd + j], t[i], s);
+  wpart[(int64_t)blockIdx.y * n + j] = s;
+}
+
+// True if the symmetric tridiagonal (a[0..k1), b[0..k1-1)) has an eigenvalue
+// above x (Sturm count via the LDL^T pivots of T - x I).
+__device__ __forceinline__ bool tridiag_has_above(const double* a, const double* b, int k1, double x) {
+  double d = 1.0;
+  for (int i = 0; i < k1; ++i) {
+    d = (a[i] - x) - (i > 0 ? b[i - 1] * b[i - 1] / d : 0.0);
+    if (d == 0.0) d = -1e-300;
+    if (d > 0.0) return true;
+  }
+  return false;
+}
+
+// Largest eigenvalue by block-parallel multisection (all threads of the CTA
+// take part; each round shrinks the bracket ~blockDim-fold).
+__device__ double tridiag_max_eig_block(const double* a, const double* b, int k1) {
+  __shared__ double br[2];
+  __shared__ int best;
+  if (threadIdx.x == 0) {
+    double lo = 1e300, hi = -1e300;
+    for (int i = 0; i < k1; ++i) {
+      double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k1 ? fabs(b[i]) : 0.0);
+      lo = fmin(lo, a[i] - r);
+      hi = fmax(hi, a[i] + r);
+    }
+    br[0] = lo;
+    br[1] = hi;
+  }
+  __syncthreads();
+  const int nt = blockDim.x;
+  for (int round = 0; round < 12; ++round) {
+    const double lo = br[0], hi = br[1];
+    if (threadIdx.x == 0) best = -1;
+    __syncthreads();
+    const double x = lo + (hi - lo) * (double)(threadIdx.x + 1) / (double)(nt + 1);
+    if (x > lo && x < hi && tridiag_has_above(a, b, k1, x)) atomicMax(&best, (int)threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t = best;
+      const double nlo = t < 0 ? lo : lo + (hi - lo) * (double)(t + 1) / (double)(nt + 1);
+      const double nhi = t + 1 >= nt ? hi : lo + (hi - lo) * (double)(t + 2) / (double)(nt + 1);
+      br[0] = nlo;
+      br[1] = nhi;
+    }
+    __syncthreads();
+    if (!(br[1] - br[0] > 1e-17 * fabs(br[1]))) break;
+  }
+  return 0.5 * (br[0] + br[1]);
+}
+
+__global__ void __launch_bounds__(1024) lz_update_kernel(LanczosDev* lz, double* __restrict__ Q,
+                                                          const double* __restrict__ w_in,
+                                                          double* __restrict__ w, int n, double tol) {
+  if (lz->done) return;
+  __shared__ double scratch[4 * 32];
+  __shared__ double h[512];
+  const int k = lz->k;
+  double* qk = Q + (int64_t)k * n;
+  // alpha = q_k . w
+  double s = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double v = w_in[j];
+    w[j] = v;
+    s = fma(v, qk[j], s);
+  }
+  double v1[1] = {s};
+  block_sum<1>(v1, scratch);
+  __shared__ double alpha_s;
+  if (threadIdx.x == 0) alpha_s = v1[0];
+  __syncthreads();
+  const double alpha = alpha_s;
+  const double bprev = k > 0 ? lz->beta[k - 1] : 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double v = w[j] - alpha * qk[j];
+    if (k > 0) v -= bprev * Q[(int64_t)(k - 1) * n + j];
+    w[j] = v;
+  }
+  __syncthreads();
+  // full reorthogonalisation, twice (classical Gram-Schmidt)
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int c = 0; c <= k; ++c) {
+      const double* qc = Q + (int64_t)c * n;
+      double d = 0.0;
+      for (int j = threadIdx.x; j < n; j += blockDim.x) d = fma(qc[j], w[j], d);
+      double vv[1] = {d};
+      block_sum<1>(vv, scratch);
+      if (threadIdx.x == 0) h[c] = vv[0];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double v = w[j];
+      for (int c = 0; c <= k; ++c) v -= h[c] * Q[(int64_t)c * n + j];
+      w[j] = v;
+    }
+    __syncthreads();
+  }
+  double nn = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) nn = fma(w[j], w[j], nn);
+  double v2[1] = {nn};
+  block_sum<1>(v2, scratch);
+  __shared__ double beta_s;
+  __shared__ int stop_s;
+  if (threadIdx.x == 0) {
+    lz->alpha[k] = alpha;
+    lz->beta[k] = sqrt(v2[0]);
+  }
+  __syncthreads();
+  const double th_all = tridiag_max_eig_block(lz->alpha, lz->beta, k + 1);
+  if (threadIdx.x == 0) {
+    const double beta = lz->beta[k];
+    const double th = th_all;
+    const double rel = lz->theta > 0.0 ? fabs(th - lz->theta) / th : 1.0;
+    lz->theta_prev = lz->theta;
+    lz->theta = th;
+    lz->stable = (rel <= tol) ? lz->stable + 1 : 0;
+    int stop = (lz->stable >= 2 && k >= 3) || beta <= 1e-300 * fmax(th, 1e-300) || k + 1 >= lz->kmax;
+    if (stop) {
+      lz->done = 1;
+      lz->sigma1 = sqrt(fmax(th, 0.0));
+    }
+    beta_s = beta;
+    stop_s = stop;
+    lz->k = stop ? k : k + 1;
+  }
+  __syncthreads();
+  if (!stop_s) {
+    double* qn = Q + (int64_t)(k + 1) * n;
+    const double inv = 1.0 / beta_s;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) qn[j] = w[j] * inv;
+  }
+}
+
+// ------------------------------------------------------------ scalars
+__global__ void pcp_start_scalars(PcpDev* st, const LanczosDev* lz, const double* __restrict__ in_stats,
+                                  double lam, double mu0, double rho, double tol, int max_iters,
+                                  double time_budget, double jac_tol, double m_global, double n) {
+  st->m_global = m_global;
+  st->n = n;
+  const double sumsq = in_stats[0], maxabs = in_stats[1];
+  const double sigma1 = lz->sigma1;
+  st->lam = lam;
+  st->rho = rho;
+  st->tol = tol;
+  st->d_norm = sqrt(sumsq);                                   // pcp.py:238
+  st->sigma1 = sigma1;
+  st->mu = mu0 > 0.0 ? mu0 : 1.25 / sigma1;                   // pcp.py:101
+  st->scale = fmax(sigma1, maxabs / lam);                     // pcp.py:114
+  st->tau = 1.0 / st->mu;
+  st->mu_last = st->mu;
+  st->mu_final = st->mu;
+  st->nuclear = 0.0;
+  st->time_budget = time_budget;
+  st->jac_tol = jac_tol;
+  st->k = 1;
+  st->done = 0;
+  st->status = 0;
+  st->rank = 0;
+  st->max_iters = max_iters;
+  st->jac_sweeps = 0;
+  st->t0_ns = global_ns();
+}
+
+// Finalize iteration k from the (all-reduced) fine-pass stats at red[0..3):
+// history record, stopping rules (pcp.py:284-296), mu <- rho mu.
+__global__ void pcp_finalize_kernel(PcpDev* st, const double* __restrict__ red, double* __restrict__ hist,
+                                    const int* __restrict__ jac_result) {
+  if (st->done) return;
+  const int k = st->k;
+  const double res2 = red[0], l1 = red[1], nnz = red[2];
+  const double gap = sqrt(res2) / st->d_norm;
+  const double wall = (global_ns() - st->t0_ns) * 1e-9;
+  double* h = hist + (int64_t)(k - 1) * kHistCols;
+  h[0] = gap;
+  h[1] = st->nuclear + st->lam * l1;
+  h[2] = (double)st->rank;
+  h[3] = nnz / ((double)st->m_global * (double)st->n);
+  h[4] = wall;
+  h[5] = st->mu;
+  h[6] = (double)st->jac_sweeps;
+  h[7] = nnz;
+  st->mu_last = st->mu;
+  st->mu_final = st->mu * st->rho;
+  if (st->status != 0) {
+    st->done = 3;
+  } else if (gap <= st->tol) {
+    st->done = 1;
+  } else if (k >= st->max_iters || (st->time_budget > 0.0 && wall >= st->time_budget)) {
+    st->done = 2;
+  } else {
+    st->k = k + 1;
+    st->mu = st->mu * st->rho;
+    st->tau = 1.0 / st->mu;
+  }
+}
+
+__global__ void pcp_after_jacobi(PcpDev* st, const int* __restrict__ jac_result) {
+  if (st->done) return;
+  int r = jac_result[0];
+  st->jac_sweeps = r;
+  if (r <= 0) st->status = 3;
+}
+
+// ------------------------------------------------------------ fused row kernel
+enum RowMode { kStart = 0, kUpdate = 1, kOutput = 2 };
+
+template <typename T>
+struct StencilT;
+template <>
+struct StencilT<float> {
+  static __device__ __forceinline__ const float* w0(const ChainDev& c) { return c.w0f; }
+  static __device__ __forceinline__ const float* w1(const ChainDev& c) { return c.w1f; }
+};
+template <>
+struct StencilT<double> {
+  static __device__ __forceinline__ const double* w0(const ChainDev& c) { return c.w0; }
+  static __device__ __forceinline__ const double* w1(const ChainDev& c) { return c.w1; }
+};
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(512)
+pcp_row_kernel(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __restrict__ D, int64_t ldd,
+               const T* __restrict__ Yin, T* __restrict__ Yout, int64_t ldy, const T* __restrict__ Z,
+               T* __restrict__ A, T* __restrict__ Lout, T* __restrict__ Sout, int64_t ldo,
+               double* __restrict__ part) {
+  if (MODE == kUpdate && st->done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = ch.n, nh = ch.nh, np = ch.np;
+  T* zrow = reinterpret_cast<T*>(smem_raw);           // np + 2 (zero tail for c0+1)
+  T* wrow = zrow + np + 2;                            // n
+  if (threadIdx.x < 2) zrow[np + threadIdx.x] = T(0);
+  __shared__ double scratch[3 * 32];
+  const T* __restrict__ w0 = StencilT<T>::w0(ch);
+  const T* __restrict__ w1 = StencilT<T>::w1(ch);
+  const int* __restrict__ c0 = ch.c0;
+
+  const double mu_d = st->mu;
+  const T inv = (T)(1.0 / mu_d);
+  const T mu = (T)mu_d;
+  const T thr = (T)(st->lam * (1.0 / mu_d));
+  const T inv_next = (T)(1.0 / (mu_d * st->rho));
+  const T inv_scale = (T)(1.0 / st->scale);
+  (void)inv_scale;
+  double acc_res = 0.0, acc_l1 = 0.0, acc_nnz = 0.0;
+
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    __syncthreads();
+    if (MODE != kStart) {
+      for (int k = threadIdx.x; k < np; k += blockDim.x) zrow[k] = Z[i * np + k];
+      __syncthreads();
+    }
+    const T* drow = D + i * ldd;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const T d = drow[j];
+      if (MODE == kStart) {
+        // y = d / scale (pcp.py:115); work = y/mu + d (pcp.py:252-254, S = 0)
+        const T y = (T)((double)d / st->scale);
+        Yout[i * ldy + j] = y;
+        wrow[j] = y * inv + d;
+      } else {
+        const int c = c0[j];
+        const T l = w0[j] * zrow[c] + w1[j] * zrow[c + 1];
+        const T y = Yin[i * ldy + j];
+        const T w = y * inv + d - l;
+        const T s = soft_thr<T>(w, thr);
+        if (MODE == kOutput) {
+          Lout[i * ldo + j] = l;
+          Sout[i * ldo + j] = s;
+        } else {
+          const T res = (d - l) - s;
+          const T yn = y + res * mu;
+          Yout[i * ldy + j] = yn;
+          acc_res = fma((double)res, (double)res, acc_res);
+          acc_l1 += fabs((double)s);
+          acc_nnz += (s != T(0)) ? 1.0 : 0.0;
+          wrow[j] = yn * inv_next + d - s;
+        }
+      }
+    }
+    if (MODE == kOutput) continue;
+    __syncthreads();
+    // gather A[i, k] = sum_{j in [lo_k, hi_k)} W[i, j] R[j, k]
+    T* arow = A + i * np;
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+      T a = T(0);
+      if (k < nh) {
+        const int lo = ch.lo[k], hi = ch.hi[k];
+        for (int j = lo; j < hi; ++j) a += wrow[j] * (c0[j] == k ? w0[j] : w1[j]);
+      }
+      arow[k] = a;
+    }
+  }
+  if (MODE == kUpdate) {
+    double v[3] = {acc_res, acc_l1, acc_nnz};
+    block_sum<3>(v, scratch);
+    if (threadIdx.x == 0) {
+      part[3 * blockIdx.x + 0] = v[0];
+      part[3 * blockIdx.x + 1] = v[1];
+      part[3 * blockIdx.x + 2] = v[2];
+    }
+  }
+}
+
+__global__ void stats_reduce_kernel(const double* __restrict__ part, int nparts, int nv, double* __restrict__ out) {
+  const int q = threadIdx.x;
+  if (q < nv) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[nv * b + q];
+    out[q] = s;
+  }
+}
+
+// ------------------------------------------------------------ host-side drivers
+template <typename T>
+static int row_pass(int mode, PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy,
+                    void* Lout, void* Sout, int64_t ldo, cudaStream_t st) {
+  const int threads = 256;
+  size_t smem = sizeof(T) * (size_t)(p->ch.np + p->ch.n + 4);
+  if (smem > 200 * 1024) {
+    set_error("pcp row kernel: fine row does not fit in shared memory");
+    return kErrArg;
+  }
+  int blocks = p->row_blocks;
+  if (p->m_local == 0) return kOk;
+  const T* Dp = (const T*)D;
+#define MLR_ROW(MODE)                                                                               \
+  {                                                                                                 \
+    auto kern = pcp_row_kernel<T, MODE>;                                                            \
+    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+    kern<<<blocks, threads, smem, st>>>(p->dev, p->ch, p->m_local, Dp, ldd, (const T*)Yin, (T*)Yout, \
+                                        ldy, (const T*)p->Z, (T*)p->A, (T*)Lout, (T*)Sout, ldo,      \
+                                        p->row_part);                                               \
+  }
+  if (mode == kStart) MLR_ROW(kStart)
+  else if (mode == kUpdate) MLR_ROW(kUpdate)
+  else MLR_ROW(kOutput)
+#undef MLR_ROW
+  MLR_LAUNCH_CHECK("pcp_row_kernel");
+  return kOk;
+}
+
+int pcp_input_stats(PcpPlan* p, const void* D, int64_t ldd, double* out2, cudaStream_t st) {
+  int blocks = p->row_blocks;
+  if (p->m_local == 0) {
+    MLR_CUDA(cudaMemsetAsync(out2, 0, 3 * sizeof(double), st));
+    return kOk;
+  }
+  if (p->f32)
+    input_stats_kernel<float><<<blocks, 256, 0, st>>>((const float*)D, ldd, p->m_local, p->ch.n, p->row_part);
+  else
+    input_stats_kernel<double><<<blocks, 256, 0, st>>>((const double*)D, ldd, p->m_local, p->ch.n, p->row_part);
+  MLR_LAUNCH_CHECK("input_stats_kernel");
+  input_stats_finish<<<1, 32, 0, st>>>(p->row_part, blocks, out2);
+  MLR_LAUNCH_CHECK("input_stats_finish");
+  return kOk;
+}
+
+int matrix_stats(int64_t m, int n, bool f32, const void* D, int64_t ldd, double* part, int blocks, double* out3,
+                 cudaStream_t st) {
+  if (m == 0) {
+    MLR_CUDA(cudaMemsetAsync(out3, 0, 3 * sizeof(double), st));
+    return kOk;
+  }
+  if (f32)
+    input_stats_kernel<float><<<blocks, 256, 0, st>>>((const float*)D, ldd, m, n, part);
+  else
+    input_stats_kernel<double><<<blocks, 256, 0, st>>>((const double*)D, ldd, m, n, part);
+  MLR_LAUNCH_CHECK("input_stats_kernel");
+  input_stats_finish<<<1, 32, 0, st>>>(part, blocks, out3);
+  MLR_LAUNCH_CHECK("input_stats_finish");
+  return kOk;
+}
+
+int pcp_lanczos_init(PcpPlan* p, cudaStream_t st) {
+  lz_init_kernel<<<(int)ceil_div(p->ch.n, 256), 256, 0, st>>>(p->lz, p->lzQ, p->ch.n, p->lz_kmax);
+  MLR_LAUNCH_CHECK("lz_init_kernel");
+  return kOk;
+}
+
+int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out, cudaStream_t st) {
+  const int n = p->ch.n;
+  const int64_t m = p->m_local;
+  if (m == 0) {
+    MLR_CUDA(cudaMemsetAsync(wpart_out, 0, sizeof(double) * n, st));
+    return kOk;
+  }
+  int blocks = p->row_blocks;
+  if (p->f32)
+    lz_dv_kernel<float><<<blocks, 256, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzQ, p->lzT);
+  else
+    lz_dv_kernel<double><<<blocks, 256, 0, st>>>(p->lz, (const double*)D, ldd, m, n, p->lzQ, p->lzT);
+  MLR_LAUNCH_CHECK("lz_dv_kernel");
+  int splits = p->lz_splits;
+  int64_t rps = ceil_div(m, splits);
+  dim3 grid((unsigned)ceil_div(n, 128), (unsigned)splits);
+  if (p->f32)
+    lz_dtv_kernel<float><<<grid, 128, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzT, p->lzW, rps);
+  else
+    lz_dtv_kernel<double><<<grid, 128, 0, st>>>(p->lz, (const double*)D, ldd, m, n, p->lzT, p->lzW, rps);
+  MLR_LAUNCH_CHECK("lz_dtv_kernel");
+  return sum_slices(p->lzW, n, n, splits, wpart_out, st);
+}
+
+int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStream_t st) {
+  lz_update_kernel<<<1, 1024, 0, st>>>(p->lz, p->lzQ, w_reduced, p->lzWork, p->ch.n, tol);
+  MLR_LAUNCH_CHECK("lz_update_kernel");
+  return kOk;
+}
+
+int pcp_start(PcpPlan* p, const void* D, int64_t ldd, void* Y0, int64_t ldy, const double* in_stats, double lam,
+              double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
+              cudaStream_t st) {
+  p->jac_tol_host = jac_tol;
+  pcp_start_scalars<<<1, 1, 0, st>>>(p->dev, p->lz, in_stats, lam, mu0, rho, tol, max_iters, time_budget, jac_tol,
+                                     (double)p->m_global, (double)p->ch.n);
+  MLR_LAUNCH_CHECK("pcp_start_scalars");
+  MLR_CUDA(cudaMemsetAsync(p->hist, 0, sizeof(double) * kHistCols * p->max_iters, st));
+  return p->f32 ? row_pass<float>(kStart, p, D, ldd, nullptr, Y0, ldy, nullptr, nullptr, 0, st)
+                : row_pass<double>(kStart, p, D, ldd, nullptr, Y0, ldy, nullptr, nullptr, 0, st);
+}
+
+// K = A^T A (split over rows, deterministic) -> red[0 .. np*np), and the
+// previous fine pass's stats -> red[np*np .. np*np+3).
+int pcp_gram(PcpPlan* p, double* red, int with_stats, cudaStream_t st) {
+  const int np = p->ch.np;
+  const int64_t nn = (int64_t)np * np;
+  if (p->m_local > 0) {
+    GemmSpec g{};
+    g.M = np; g.N = np; g.K = (int)p->m_local;
+    g.A = p->A; g.lda = np; g.a_f32 = p->f32; g.trans_a = true;
+    g.B = p->A; g.ldb = np; g.b_f32 = p->f32; g.trans_b = false;
+    g.C = p->gram_part; g.ldc = np; g.c_f32 = false; g.c_slice = nn; g.splits = p->gram_splits; g.alpha = 1.0;
+    g.kscale = nullptr; g.skip = nullptr;
+    int rc = gemm_f64(g, st);
+    if (rc) return rc;
+    rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);
+    if (rc) return rc;
+  } else {
+    MLR_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * nn, st));
+  }
+  if (with_stats) {
+    if (p->m_local > 0) {
+      stats_reduce_kernel<<<1, 32, 0, st>>>(p->row_part, p->row_blocks, 3, red + nn);
+      MLR_LAUNCH_CHECK("stats_reduce_kernel");
+    } else {
+      MLR_CUDA(cudaMemsetAsync(red + nn, 0, 3 * sizeof(double), st));
+    }
+  }
+  return kOk;
+}
+
+int pcp_finalize(PcpPlan* p, const double* red, cudaStream_t st) {
+  const int64_t nn = (int64_t)p->ch.np * p->ch.np;
+  pcp_finalize_kernel<<<1, 1, 0, st>>>(p->dev, red + nn, p->hist, p->jac_result);
+  MLR_LAUNCH_CHECK("pcp_finalize_kernel");
+  return kOk;
+}
+
+// Coarse SVT from the (all-reduced) Gram in red: B = G^-1 K G^-1; Jacobi
+// on X = B V (warm start V); W~ = G^-1 V diag(f) V^T; Z = A W~.
+int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
+  const int np = p->ch.np;
+  const int* skip = &p->dev->done;
+  int rc;
+  // T1 = G^-1 K (column solves), B = G^-1 T1^T  (= G^-1 K G^-1, K symmetric)
+  if ((rc = ldl_solve(skip, p->ch, red, p->T1, 0, st))) return rc;
+  if ((rc = ldl_solve(skip, p->ch, p->T1, p->Bm, 1, st))) return rc;
+  // X = B V
+  GemmSpec g{};
+  g.M = np; g.N = np; g.K = np;
+  g.A = p->Bm; g.lda = np; g.a_f32 = false; g.trans_a = false;
+  g.B = p->Vm; g.ldb = np; g.b_f32 = false; g.trans_b = false;
+  g.C = p->Xm; g.ldc = np; g.c_f32 = false; g.c_slice = 0; g.splits = 1; g.alpha = 1.0;
+  g.kscale = nullptr; g.skip = skip;
+  if ((rc = gemm_f64(g, st))) return rc;
+  if ((rc = jacobi_eig(p->Xm, p->Vm, np, p->jac_tol_host, p->jac_max_sweeps, p->jac_partials, p->jac_off,
+                       p->jac_result, skip, st)))
+    return rc;
+  pcp_after_jacobi<<<1, 1, 0, st>>>(p->dev, p->jac_result);
+  MLR_LAUNCH_CHECK("pcp_after_jacobi");
+  if ((rc = svt_weights(skip, np, p->ch.nh, p->Xm, p->Vm, &p->dev->tau, p->sig, p->fw, &p->dev->rank,
+                        &p->dev->nuclear, st)))
+    return rc;
+  // P = V diag(f) V^T
+  g.A = p->Vm; g.trans_a = false; g.B = p->Vm; g.trans_b = true; g.C = p->T1; g.kscale = p->fw;
+  if ((rc = gemm_f64(g, st))) return rc;
+  // W~ = G^-1 P
+  if ((rc = ldl_solve(skip, p->ch, p->T1, p->Wm, 0, st))) return rc;
+  // Z = A W~
+  if (p->m_local > 0) {
+    GemmSpec z{};
+    z.M = (int)p->m_local; z.N = np; z.K = np;
+    z.A = p->A; z.lda = np; z.a_f32 = p->f32; z.trans_a = false;
+    z.B = p->Wm; z.ldb = np; z.b_f32 = false; z.trans_b = false;
+    z.C = p->Z; z.ldc = np; z.c_f32 = p->f32; z.c_slice = 0; z.splits = 1; z.alpha = 1.0;
+    z.kscale = nullptr; z.skip = skip;
+    if ((rc = gemm_f64(z, st))) return rc;
+  }
+  return kOk;
+}
+
+int pcp_update(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy, cudaStream_t st) {
+  return p->f32 ? row_pass<float>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st)
+                : row_pass<double>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st);
+}
+
+// Final L = Z R^T and S = shrink(D - L + Y_{k-1}/mu_k, lam/mu_k).
+__global__ void pcp_output_mu(PcpDev* st) { st->mu = st->mu_last; }
+__global__ void pcp_output_mu_restore(PcpDev* st) { st->mu = st->mu_final; }
+
+int pcp_outputs(PcpPlan* p, const void* D, int64_t ldd, const void* Yprev, int64_t ldy, void* L, void* S, int64_t ldo,
+                cudaStream_t st) {
+  pcp_output_mu<<<1, 1, 0, st>>>(p->dev);
+  int rc = p->f32 ? row_pass<float>(kOutput, p, D, ldd, Yprev, nullptr, ldy, L, S, ldo, st)
+                  : row_pass<double>(kOutput, p, D, ldd, Yprev, nullptr, ldy, L, S, ldo, st);
+  if (rc) return rc;
+  pcp_output_mu_restore<<<1, 1, 0, st>>>(p->dev);
+  MLR_LAUNCH_CHECK("pcp_output_mu");
+  return kOk;
+}
+
+}  // namespace mlr

@@ -1,0 +1,76 @@
+// Device state and plan for ML-PCP.
+#pragma once
+#include "kernels.h"
+
+namespace mlr {
+
+constexpr int kHistCols = 8;  // gap, objective, rank, sparsity, wall, mu, jacobi sweeps, nnz
+
+// Device-resident solver state (one instance in device memory per plan).
+struct PcpDev {
+  double lam, rho, tol, d_norm, sigma1, scale;
+  double mu;        // mu_k of the current iteration
+  double tau;       // 1/mu_k
+  double mu_last;   // mu of the last finalized iteration
+  double mu_final;  // mu after the final `mu *= rho` (reference PcpState.mu)
+  double nuclear;   // sum(sigma - tau)+ of the current SVT
+  double time_budget;
+  double jac_tol;
+  double t0_ns;
+  double m_global, n;
+  int k;            // current iteration (1-based)
+  int done;         // 0 running, 1 converged, 2 stopped, 3 error
+  int status;       // 0 ok, 3 Jacobi did not converge
+  int rank;
+  int max_iters;
+  int jac_sweeps;
+};
+
+struct LanczosDev {
+  int k, done, kmax, stable;
+  double theta, theta_prev, sigma1;
+  double alpha[512];
+  double beta[512];
+};
+
+struct PcpPlan {
+  ChainDev ch;
+  bool f32;
+  int64_t m_local, m_global;
+  int max_iters;
+  int row_blocks, gram_splits, lz_splits, lz_kmax;
+  double jac_tol_host;
+  int jac_max_sweeps;
+  // device buffers (carved from the caller's workspace)
+  PcpDev* dev;
+  LanczosDev* lz;
+  double* hist;        // [max_iters][kHistCols]
+  void* A;             // m_local x np (T)
+  void* Z;             // m_local x np (T)
+  double* gram_part;   // gram_splits x np x np
+  double* row_part;    // row_blocks x 4
+  double *T1, *Bm, *Xm, *Vm, *Wm;   // np x np
+  double *sig, *fw;    // np
+  double* jac_partials;
+  double* jac_off;     // 2
+  int* jac_result;     // 4
+  double *lzQ, *lzT, *lzW, *lzWork;
+};
+
+int pcp_input_stats(PcpPlan* p, const void* D, int64_t ldd, double* out2, cudaStream_t st);
+int matrix_stats(int64_t m, int n, bool f32, const void* D, int64_t ldd, double* part, int blocks, double* out3,
+                 cudaStream_t st);
+int pcp_lanczos_init(PcpPlan* p, cudaStream_t st);
+int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out, cudaStream_t st);
+int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStream_t st);
+int pcp_start(PcpPlan* p, const void* D, int64_t ldd, void* Y0, int64_t ldy, const double* in_stats, double lam,
+              double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
+              cudaStream_t st);
+int pcp_gram(PcpPlan* p, double* red, int with_stats, cudaStream_t st);
+int pcp_finalize(PcpPlan* p, const double* red, cudaStream_t st);
+int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st);
+int pcp_update(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy, cudaStream_t st);
+int pcp_outputs(PcpPlan* p, const void* D, int64_t ldd, const void* Yprev, int64_t ldy, void* L, void* S, int64_t ldo,
+                cudaStream_t st);
+
+}  // namespace mlr

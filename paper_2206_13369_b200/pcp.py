@@ -1,0 +1,154 @@
+"""ML-PCP drop-in: ``ml_ialm_solve`` (reference pcp.py:213-309) on B200.
+
+The host loop mirrors the reference's structure and stopping rules; every
+arithmetic step runs in the CUDA library.  Per iteration the host enqueues
+``svt -> update -> gram -> [all-reduce] -> finalize`` and polls the
+device-side stopping flag every ``check_every`` iterations, so the GPU is
+never idle waiting for Python.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .api_types import IterationRecord, PcpOptions, PcpState, SvdError
+from .backend import CudaPcp
+from .chain import build_chain, resolve_coarse_width
+from .runtime import SINGLE, Comm, as_device_matrix, give_back
+
+LANCZOS_TOL = 1e-15
+
+
+def _zero_state(shape, kind, like):
+    z = torch.zeros(shape, dtype=like.dtype, device=like.device)
+    rec = IterationRecord(1, 0.0, 0.0, 0, 0.0, 0.0)
+    return PcpState(l=give_back(z, kind), s=give_back(z.clone(), kind), y=give_back(z.clone(), kind), mu=0.0,
+                    iter=1, history=[rec], mu_history=[], converged=True)
+
+
+def _jacobi_tol(opts, f32):
+    if opts.jacobi_tol is not None:
+        return float(opts.jacobi_tol)
+    return 1e-10 if f32 else 64 * np.finfo(np.float64).eps
+
+
+def run_ialm(be, comm, D, m_global, n, opts, lam, check_every):
+    """Row-block host loop shared by the single-GPU and sharded entry points.
+
+    Returns (L, S, Y, state dict, history array) or None for a zero D."""
+    st3 = be.input_stats(D)
+    comm.sum(st3[0:1])
+    comm.max(st3[1:2])
+    comm.sum(st3[2:3])
+    sumsq, _, bad = st3[:3].tolist()
+    if bad > 0:
+        raise ValueError("d contains non-finite entries")
+    if sumsq == 0.0:
+        return None
+    opts.validate()
+    # sigma_1(D) by Lanczos on D^T D (pcp.py:100, 114)
+    be.lanczos_init()
+    steps = 0
+    while True:
+        for _ in range(4):
+            w = be.lanczos_matvec(D)
+            comm.sum(w)
+            be.lanczos_update(w, LANCZOS_TOL)
+            steps += 1
+        if be.lanczos_state()["done"]:
+            break
+        if steps > 2 * n + 16:
+            raise SvdError("Lanczos estimate of sigma_1(D) did not converge", iterations=steps)
+    f32 = D.dtype == torch.float32
+    Y = [be.empty(tuple(D.shape), D.dtype), be.empty(tuple(D.shape), D.dtype)]
+    be.start(D, Y[0], lam, opts.mu0, opts.rho, opts.tol_feasibility, opts.max_iters, opts.time_budget,
+             _jacobi_tol(opts, f32), 60)
+    nn, ns = be.stats_slice()
+    be.gram(0)
+    comm.sum(be.red[:nn])
+    calls = 0
+    while True:
+        for _ in range(check_every):
+            be.svt()
+            be.update(D, Y[calls % 2], Y[(calls + 1) % 2])
+            calls += 1
+            be.gram(1)
+            comm.sum(be.red[:ns])
+            be.finalize()
+        st = be.state()
+        if st["done"]:
+            break
+    if st["done"] == 3:
+        raise SvdError("coarse Jacobi eigensolver did not converge", iterations=-st["jac_sweeps"])
+    k = st["k"]
+    L = be.empty(tuple(D.shape), D.dtype)
+    S = be.empty(tuple(D.shape), D.dtype)
+    be.outputs(D, Y[(k - 1) % 2], L, S)
+    hist = be.history(k)
+    return L, S, Y[k % 2], st, hist
+
+
+def _state_from(L, S, Yk, st, hist, kind):
+    history = [IterationRecord(i + 1, float(h[0]), float(h[1]), int(round(h[2])), float(h[3]), float(h[4]))
+               for i, h in enumerate(hist)]
+    return PcpState(l=give_back(L, kind), s=give_back(S, kind), y=give_back(Yk, kind), mu=float(st["mu_final"]),
+                    iter=int(st["k"]), history=history, mu_history=[float(x) for x in hist[:, 5]],
+                    converged=st["done"] == 1)
+
+
+def ml_ialm_solve(d, opts=None):
+    """Multilevel inexact ALM (drop-in for mlrpca.ml_ialm_solve).
+
+    ``d`` may be a numpy array (any dtype coercible to float64; float32 input
+    runs the FP32 path), or a torch tensor (CPU or CUDA; results stay on the
+    input's side).  ``opts.levels`` is the coarse width n_H, as in the
+    reference.  Raises ValueError / LevelError / SvdError like the reference.
+    """
+    D, kind = as_device_matrix(d, "d")
+    m, n = D.shape
+    opts = opts if opts is not None else PcpOptions()
+    if opts.collect_diagnostics:
+        raise NotImplementedError("collect_diagnostics is not available on the GPU path yet")
+    lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m, n))
+    with torch.cuda.device(D.device):
+        opts_checked = _checked_width(n, m, opts)
+        chain = build_chain(n, opts_checked)
+        be = CudaPcp(chain, m, m, D.dtype == torch.float32, opts.max_iters, D.device)
+        try:
+            out = run_ialm(be, SINGLE, D, m, n, opts, lam, _check_every(opts))
+        finally:
+            be.close()
+    if out is None:
+        return _zero_state(tuple(D.shape), kind, D)
+    return _state_from(*out, kind)
+
+
+def _checked_width(n, m, opts):
+    return resolve_coarse_width(n, m, opts.levels, opts.rank_guess)
+
+
+def _check_every(opts):
+    if opts.check_every is not None:
+        return max(1, int(opts.check_every))
+    return 1 if opts.time_budget is not None else 4
+
+
+def ml_ialm_solve_rows(d_local, opts, m_global, group=None):
+    """Row-sharded ML-IALM: this rank holds rows of the global m_global x n
+    iterate; K = A^T A and the per-iteration reductions are all-reduced over
+    ``group`` (NCCL).  Returns a PcpState whose arrays are this rank's rows."""
+    D, kind = as_device_matrix(d_local, "d")
+    m, n = D.shape
+    comm = Comm(group)
+    lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m_global, n))
+    with torch.cuda.device(D.device):
+        chain = build_chain(n, _checked_width(n, m_global, opts))
+        be = CudaPcp(chain, m, m_global, D.dtype == torch.float32, opts.max_iters, D.device)
+        try:
+            out = run_ialm(be, comm, D, m_global, n, opts, lam, _check_every(opts))
+        finally:
+            be.close()
+    if out is None:
+        return _zero_state(tuple(D.shape), kind, D)
+    return _state_from(*out, kind)

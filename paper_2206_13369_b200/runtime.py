@@ -1,0 +1,83 @@
+"""Host-side plumbing shared by the solvers: input coercion/upload, output
+conversion, and the collective wrapper used for row-sharded runs."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+class Comm:
+    """Collectives over a torch.distributed group (NCCL on GPUs, gloo on CPU);
+    a world of one makes every call a no-op."""
+
+    def __init__(self, group=None, enabled=None):
+        if enabled is None:
+            enabled = dist.is_available() and dist.is_initialized()
+        self.enabled = bool(enabled)
+        self.group = group
+        self.world = dist.get_world_size(group) if self.enabled else 1
+        self.rank = dist.get_rank(group) if self.enabled else 0
+
+    def sum(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def max(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def gather(self, out, t):
+        """out (world * t.numel()) <- concatenation of every rank's t."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        else:
+            out.copy_(t)
+        return out
+
+
+SINGLE = Comm(enabled=False)
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2206_13369_b200 requires a CUDA (sm_100a) device; no CPU fallback exists")
+
+
+def as_device_matrix(x, name="d"):
+    """Validate like as_matrix (linalg.py:48-57, finiteness is checked on the
+    device) and return (tensor on GPU, kind) where kind records how to give
+    results back: "numpy", "torch-cpu" or "torch-cuda"."""
+    require_cuda()
+    if isinstance(x, torch.Tensor):
+        kind = "torch-cuda" if x.is_cuda else "torch-cpu"
+        t = x
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        if t.dim() != 2:
+            raise ValueError(f"{name} must be 2-D, got ndim={t.dim()}")
+        if t.shape[0] < 1 or t.shape[1] < 1:
+            raise ValueError(f"{name} must have positive dimensions, got {tuple(t.shape)}")
+        if not t.is_cuda:
+            t = t.to(torch.device("cuda", torch.cuda.current_device()), non_blocking=t.is_pinned())
+        return t.contiguous(), kind
+    a = np.asarray(x)
+    if a.dtype != np.float32:
+        a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got ndim={a.ndim}")
+    if a.shape[0] < 1 or a.shape[1] < 1:
+        raise ValueError(f"{name} must have positive dimensions, got {a.shape}")
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(torch.device("cuda", torch.cuda.current_device()))
+    return t, "numpy"
+
+
+def give_back(t, kind):
+    if kind == "torch-cuda":
+        return t
+    if kind == "torch-cpu":
+        return t.cpu()
+    return t.cpu().numpy()

@@ -1,0 +1,140 @@
+"""Generate golden vectors from the REAL reference package (run in the build
+container, where /root/reference exists; the outputs are committed so the GPU
+box can check without the reference).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Inputs are produced by the oracle's seeded generators (identical on both
+sides); every output below is computed by ``mlrpca`` itself
+(/root/reference/pkg/src/mlrpca, v0.1.0).
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import mlrpca  # noqa: E402  (reference)
+from oracle import mlrpca_oracle as O  # noqa: E402  (input generators only)
+
+
+def hist_arrays(history):
+    return {
+        "h_gap": np.array([h.feasibility_gap for h in history]),
+        "h_obj": np.array([h.objective for h in history]),
+        "h_rank": np.array([h.rank_l for h in history]),
+        "h_sparsity": np.array([h.sparsity_s for h in history]),
+    }
+
+
+def multilevel_kats():
+    out = {}
+    out["R6"] = mlrpca.build_interpolation(6).toarray()
+    for n, t in [(8, 2), (16, 4), (33, 9), (64, 8), (100, 25), (101, 13), (128, 32)]:
+        ch = mlrpca.build_chain(n, t, normalize=True)
+        out[f"R_{n}_{t}"] = ch.composite.toarray()
+        out[f"spec_{n}_{t}"] = np.array(ch.spectral_norm)
+    for n, t in [(500, 125), (2000, 250), (4000, 500), (1000, 125), (20000, 1250)]:
+        ch = mlrpca.build_chain(n, t, normalize=True)
+        r = ch.composite.tocsr()
+        out[f"Rcsr_{n}_{t}_data"] = r.data
+        out[f"Rcsr_{n}_{t}_indices"] = r.indices
+        out[f"Rcsr_{n}_{t}_indptr"] = r.indptr
+        out[f"spec_{n}_{t}"] = np.array(ch.spectral_norm)
+    out["coarse_sizes_400"] = np.array(mlrpca.multilevel.coarse_sizes(400))
+    out["select_1024_5_1_10000"] = np.array(mlrpca.select_levels(1024, 5, 1, 10000))
+    out["select_400_2_1_3072"] = np.array(mlrpca.select_levels(400, 2, 1, 3072))
+    x = np.random.default_rng(11).standard_normal((5, 100))
+    ch = mlrpca.build_chain(100, 25)
+    out["restrict_x"] = x
+    out["restrict_y"] = mlrpca.restrict(x, ch)
+    out["restrict_ls_y"] = mlrpca.restrict_least_squares(x, ch)
+    out["prolong_y"] = mlrpca.prolong(out["restrict_y"], ch)
+    np.savez_compressed(os.path.join(HERE, "multilevel.npz"), **out)
+
+
+def linalg_kats():
+    out = {}
+    out["st_in"] = np.array([[1.0, -0.3, 0.7]])
+    out["st_out"] = mlrpca.soft_threshold(out["st_in"], 0.5)
+    z, rank = mlrpca.svt(np.diag([3.0, 1.0]), 2.0)
+    out["svt_diag_z"], out["svt_diag_rank"] = z, np.array(rank)
+    z, rank = mlrpca.svt(np.diag([3.0, 2.0]), 2.0)
+    out["svt_tie_z"], out["svt_tie_rank"] = z, np.array(rank)
+    x = np.random.default_rng(8).standard_normal((40, 12))
+    out["svt_x"] = x
+    out["svt_z"], r = mlrpca.svt(x, 1.5)
+    out["svt_rank"] = np.array(r)
+    np.savez_compressed(os.path.join(HERE, "linalg.npz"), **out)
+
+
+def pcp_cases():
+    cases = {
+        # name: (m, n, rank, eta, seed, n_H, tol, dtype)
+        "pcp_f64_small": (120, 96, 6, 0.10, 3, 24, 1e-7, np.float64),
+        "pcp_f32_small": (200, 160, 8, 0.10, 4, 40, 1e-6, np.float32),
+        "pcp_f64_odd": (90, 77, 5, 0.08, 5, 20, 1e-7, np.float64),
+    }
+    for name, (m, n, r, eta, seed, nh, tol, dt) in cases.items():
+        d, _ = O.gaussian_rpca(m, n, r, eta, seed)
+        d = d.astype(dt).astype(np.float64)
+        st = mlrpca.ml_ialm_solve(d, mlrpca.PcpOptions(levels=nh, tol_feasibility=tol))
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), d=d, l=st.l, s=st.s, y=st.y,
+            mu=np.array(st.mu), iter=np.array(st.iter), n_coarse=np.array(nh),
+            tol=np.array(tol), converged=np.array(st.converged),
+            mu_history=np.array(st.mu_history), **hist_arrays(st.history))
+
+
+def pcp_c1_summary():
+    # C1 at full size: L/S are 2 MB each, so only fingerprints are committed;
+    # the full arrays are checked live against the oracle on the GPU box.
+    d, _ = O.make_config("C1", 0)
+    st = mlrpca.ml_ialm_solve(d, mlrpca.PcpOptions(
+        lam=1 / np.sqrt(500), tol_feasibility=1e-7, levels=125))
+    rows = np.arange(0, 500, 37)
+    np.savez_compressed(
+        os.path.join(HERE, "pcp_c1_summary.npz"),
+        d_sum=np.array(d.sum()), iter=np.array(st.iter), mu=np.array(st.mu),
+        l_fro=np.array(np.linalg.norm(st.l)), s_fro=np.array(np.linalg.norm(st.s)),
+        y_fro=np.array(np.linalg.norm(st.y)), l_rows=st.l[rows], s_rows=st.s[rows],
+        rows=rows, sigma1=np.array(np.linalg.norm(d, 2)), **hist_arrays(st.history))
+
+
+def fwt_cases():
+    cases = {
+        # name: (m, n, rank, eta, observe, seed, n_H, tol, max_iters, dtype)
+        "fwt_f64_small": (100, 80, 4, 0.10, 0.8, 5, 20, 1e-6, 300, np.float64),
+        "fwt_f32_small": (160, 128, 4, 0.10, 0.7, 6, 16, 1e-5, 200, np.float32),
+        "fwt_f64_full": (64, 50, 3, 0.10, None, 7, 13, 1e-6, 200, np.float64),
+    }
+    for name, (m, n, r, eta, obs, seed, nh, tol, iters, dt) in cases.items():
+        d, mask = O.gaussian_rpca(m, n, r, eta, seed, observe=obs)
+        d = d.astype(dt).astype(np.float64)
+        lam = 1 / np.sqrt(max(m, n))
+        om = mlrpca.ObservationMask(mask) if mask is not None else None
+        st = mlrpca.ml_fwt_solve(d, om, mlrpca.CpcpOptions(
+            lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=tol,
+            max_iters=iters, levels=nh, collect_rank=False))
+        extra = {"mask": mask} if mask is not None else {}
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), d=d, l=st.l, s=st.s,
+            t_l=np.array(st.t_l), t_s=np.array(st.t_s), u_l=np.array(st.u_l),
+            u_s=np.array(st.u_s), iter=np.array(st.iter), n_coarse=np.array(nh),
+            tol=np.array(tol), max_iters=np.array(iters), lam_l=np.array(lam),
+            lam_s=np.array(lam / np.sqrt(max(m, n))),
+            converged=np.array(st.converged), **hist_arrays(st.history), **extra)
+
+
+if __name__ == "__main__":
+    multilevel_kats()
+    linalg_kats()
+    pcp_cases()
+    pcp_c1_summary()
+    fwt_cases()
+    print("golden vectors written to", HERE)
