@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark: ML-PCP iterations/s on BASELINE config C2 (2000x2000 FP32,
+rank 100, 10% corruptions, n_H = 250, tol 1e-6), the configuration the
+BASELINE metric is quoted on.
+
+A "step" is one full solve (to tolerance) of the C2 instance.  `value` is
+iterations/s with D resident in HBM; `e2e` is the same metric through the
+public API with a pinned host matrix in and host L, S, Y out.  Rank r of N
+holds rows [r*m/N, (r+1)*m/N) (row sharding, NCCL all-reduce of the coarse
+Gram each iteration).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ML-PCP iterations/s (C2: 2000x2000 FP32, n_H=250, tol 1e-6)"
+UNIT = "iterations/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_solve(d32, cfg, threads):
+    """The reference algorithm (oracle port of pcp.py:213-309) on the host."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import mlrpca_oracle as O
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        r = O.ml_ialm(d32.astype(np.float64), lam=1 / np.sqrt(cfg["m"]), tol=cfg["tol"], levels=cfg["n_coarse"])
+        return r.iter, time.perf_counter() - t0
+
+
+def run_reference(args, cfg, d32):
+    threads = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        cpu_reference_solve(d32, cfg, threads)
+    iters = 0
+    secs = 0.0
+    for _ in range(args.steps):
+        it, s = cpu_reference_solve(d32, cfg, threads)
+        iters += it
+        secs += s
+    value = iters / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE C2 shapes/distributions)",
+        "config": {"workload": "C2 ML-PCP 2000x2000 rank 100, 10% sparse, n_H=250, tol 1e-6", "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full C2 solves (oracle port of mlrpca.ml_ialm_solve, numpy/"
+                                   "OpenBLAS, FP64 on the FP32-rounded input)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    from paper_2206_13369_b200.datasets import CONFIGS, make_config
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cfg = CONFIGS[args.config]
+    assert cfg["solver"] == "pcp", "bench.py times the ML-PCP workload"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        d32, _ = make_config(args.config, args.seed)
+        run_reference(args, cfg, d32)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2206_13369_b200 as pkg
+    from paper_2206_13369_b200 import pcp as pcp_mod
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    d_full, _ = make_config(args.config, args.seed)
+    m, n = d_full.shape
+    r0, r1 = rank * m // world, (rank + 1) * m // world
+    d_host = np.ascontiguousarray(d_full[r0:r1])
+    opts = pkg.PcpOptions(lam=1 / np.sqrt(max(m, n)), tol_feasibility=cfg["tol"], levels=cfg["n_coarse"])
+    D = torch.from_numpy(d_host).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def solve(x):
+        if world > 1:
+            return pkg.ml_ialm_solve_rows(x, opts, m, None)
+        return pkg.ml_ialm_solve(x, opts)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        solve(D)
+    # ---- value: D resident in HBM
+    sink = []
+    pcp_mod.TIMING_SINK = sink if world == 1 else None
+    barrier()
+    total_ms, iters = 0.0, 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = solve(D)
+            e1.record()
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            iters += st.iter
+    barrier()
+    pcp_mod.TIMING_SINK = None
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = iters / (total_ms / 1e3)
+
+    # ---- e2e: pinned host D in, host L/S/Y out, through the public API
+    d_pin = torch.from_numpy(d_host).pin_memory()
+    for _ in range(1):
+        solve(d_pin)
+    barrier()
+    e2e_ms, e2e_iters = 0.0, 0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = solve(d_pin)
+        torch.cuda.synchronize()
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+        e2e_iters += st.iter
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e_value = e2e_iters / (e2e_ms / 1e3)
+    bytes_el = d_host.dtype.itemsize
+    h2d = int(d_host.size * bytes_el)
+    d2h = int(3 * d_host.size * bytes_el)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant phase, from the live event timings
+    peaks = _peaks()
+    phases = {}
+    for s in sink:
+        for k, v in s.items():
+            if isinstance(v, tuple):
+                a = phases.setdefault(k, [0.0, 0])
+                a[0] += v[0]
+                a[1] += v[1]
+    nh = cfg["n_coarse"]
+    npad = (nh + 63) // 64 * 64
+    b = bytes_el
+    upd_bytes = b * (3 * m * n + 2 * m * npad)          # D, Y in; Y out; Z in; A' out
+    roof = None
+    phase_ms = {k: v[0] for k, v in phases.items()}
+    dominant = max(phase_ms, key=phase_ms.get) if phase_ms else None
+    sweeps = [x for s in sink for x in s.get("jac_sweeps", [])]
+    if dominant == "update" or dominant is None:
+        ms, cnt = phases.get("update", [float("nan"), 1])
+        ach = upd_bytes / (ms / cnt / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "pcp_row_kernel<float,kUpdate>", "achieved": ach,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
+                "algorithmic_bytes_per_launch": upd_bytes}
+    else:
+        ms, cnt = phases[dominant]
+        if dominant == "jacobi":
+            nb = npad // (32 if npad >= 1024 else 16)
+            per_sweep = 12.0 * npad ** 3 * (nb - 1) / nb
+            flops = per_sweep * (statistics.mean(sweeps) if sweeps else 1.0)
+            fp64_peak = 40.0
+            ach = flops / (ms / cnt / 1e3) / 1e12
+            roof = {"bound": "tensor", "kernel": "jacobi_kernel<16> (FP64 one-sided block Jacobi)",
+                    "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                    "peak_source": "nominal B200 FP64 (not in MEASURED_PEAKS.json)", "traffic": None,
+                    "algorithmic_flops_per_launch": flops, "mean_sweeps": statistics.mean(sweeps) if sweeps else None}
+        else:
+            roof = {"bound": "tensor", "kernel": dominant, "achieved": None, "peak": None, "unit": "TFLOP/s",
+                    "frac": None, "traffic": None}
+    upd = phases.get("update")
+    streaming = None
+    if upd:
+        ach = upd_bytes / (upd[0] / upd[1] / 1e3) / 1e9
+        streaming = {"kernel": "pcp_row_kernel (fused prolong/shrink/dual/restrict)", "achieved_gbs": ach,
+                     "frac_of_measured_hbm": ach / peaks["hbm_gbs"], "avg_us": 1e3 * upd[0] / upd[1]}
+    per_iter = {k: round(v / max(1, sum(s.get("iters", 0) for s in sink)), 4) for k, v in phase_ms.items()}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        it, secs = cpu_reference_solve(d_full, cfg, threads)
+        cpu = {"value": it / secs, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"1 full C2 solve ({it} iterations, oracle port of mlrpca.ml_ialm_solve, numpy/OpenBLAS FP64)"}
+
+    lz = statistics.mean(s.get("lanczos_steps", 0) for s in sink) if sink else 0
+    per_solve_launches = (14 * (iters / args.steps) + 4 * lz + 12)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator with BASELINE C2 shapes/distributions)",
+        "config": {"workload": "C2 ML-PCP 2000x2000 rank 100, 10% sparse U[-1,1], n_H=250, tol 1e-6",
+                   "seed": args.seed, "iterations_per_solve": iters / args.steps,
+                   "l2": "256 MB buffer written before every timed step",
+                   "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms / args.steps},
+        "roofline": roof,
+        "streaming_kernel": streaming,
+        "phase_ms_per_iter": per_iter,
+        "dominant_phase": dominant,
+        "time_to_tol_ms": total_ms / args.steps,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(per_solve_launches * args.steps),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -101,6 +101,12 @@ int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, 
 /* out16: k, done, status, rank, mu, mu_final, mu_last, nuclear, sigma1, d_norm, jac_sweeps, tau, scale, lam, 0, 0 */
 int mlr_pcp_state(void* plan, double* out16, void* stream);
 int mlr_pcp_history(void* plan, int count, double* out, void* stream); /* count x 8 */
+/* Per-phase CUDA-event timing: phases gram, pre (B, X=BV), jacobi, post
+ * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize.
+ * mlr_pcp_timing synchronises, returns total ms and launch counts per phase
+ * (7 entries each) and resets the accumulators. */
+int mlr_pcp_set_timing(void* plan, int enable);
+int mlr_pcp_timing(void* plan, double* ms7, int* counts7);
 
 /* ---------------------------------------------------------------- ML-CPCP
  * mask: bit-packed observation pattern, uint32 words, ldm words per row,

@@ -55,6 +55,8 @@ _SIGS = {
                                 c_void_p]),
     "mlr_pcp_state": (c_int, [c_void_p, c_void_p, c_void_p]),
     "mlr_pcp_history": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "mlr_pcp_set_timing": (c_int, [c_void_p, c_int]),
+    "mlr_pcp_timing": (c_int, [c_void_p, c_void_p, c_void_p]),
     # ML-CPCP
     "mlr_cpcp_workspace_bytes": (c_int64, [c_void_p, c_int64, c_int, c_int]),
     "mlr_cpcp_create": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_int, c_void_p,

@@ -116,6 +116,18 @@ class CudaPcp:
         _lib.check(self.lib.mlr_pcp_history(self.h, int(count), out.ctypes.data, _stream()))
         return out[:count]
 
+    PHASES = ("gram", "pre", "jacobi", "post", "recon", "update", "finalize")
+
+    def set_timing(self, on):
+        _lib.check(self.lib.mlr_pcp_set_timing(self.h, int(bool(on))))
+
+    def timing(self):
+        """{phase: (total ms, launches)} since the last call (synchronises)."""
+        ms = np.zeros(7)
+        cnt = np.zeros(7, dtype=np.int32)
+        _lib.check(self.lib.mlr_pcp_timing(self.h, ms.ctypes.data, cnt.ctypes.data))
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES)}
+
     def empty(self, shape, dtype):
         return torch.empty(shape, dtype=dtype, device=self.device)
 

@@ -70,13 +70,9 @@ __global__ void eye_kernel(double* V, int np) {
     V[e] = (e / np == e % np) ? 1.0 : 0.0;
 }
 
-__global__ void eig_values_kernel(int np, const double* __restrict__ X, const double* __restrict__ V,
-                                  double* __restrict__ lam) {
+__global__ void diag_kernel(int np, const double* __restrict__ X, double* __restrict__ lam) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= np) return;
-  double s = 0.0;
-  for (int r = 0; r < np; ++r) s = fma(V[(int64_t)r * np + i], X[(int64_t)r * np + i], s);
-  lam[i] = s;
+  if (i < np) lam[i] = X[(int64_t)i * (np + 1)];
 }
 
 // ------------------------------------------------------------ workspace carving
@@ -111,7 +107,8 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.Wm = c.take<double>(8 * nn);
   p.sig = c.take<double>(8 * np);
   p.fw = c.take<double>(8 * np);
-  p.jac_partials = c.take<double>(8 * (size_t)jacobi_partials_doubles(np));
+  p.qbuf = c.take<double>(8 * (size_t)jacobi2_qbuf_elems(np));
+  p.qflag = c.take<int>(4 * (size_t)(np / 32 + 1));
   p.jac_off = c.take<double>(8 * 2);
   p.jac_result = c.take<int>(4 * 4);
   p.lzQ = c.take<double>(8 * (size_t)n * (p.lz_kmax + 1));
@@ -186,6 +183,9 @@ using namespace mlr;
 extern "C" {
 
 int mlr_version(void) { return 1; }
+
+// debug: cycle breakdown of the Jacobi kernel (CTA 0); resets the counters
+int mlr_debug_j2prof(unsigned long long* out8) { return mlr::jacobi2_debug_prof(out8); }
 const char* mlr_last_error(void) { return g_err.c_str(); }
 int mlr_device_count(void) {
   int n = 0;
@@ -270,6 +270,18 @@ int mlr_chain_create(int n, int nh, const int32_t* c0, const double* w0, const d
   rc |= up((void**)&d.hi, hi.data(), sizeof(int) * nh);
   rc |= up((void**)&d.gl, gl.data(), sizeof(double) * gl.size());
   rc |= up((void**)&d.gd, gd.data(), sizeof(double) * nh);
+  {
+    // G_R^{-1} column by column from the LDL^T factors (cond(G_R) <= 5)
+    std::vector<double> gi((size_t)np * np, 0.0), col(nh);
+    for (int c = 0; c < nh; ++c) {
+      for (int k = 0; k < nh; ++k) col[k] = (k == c) ? 1.0 : 0.0;
+      for (int k = 1; k < nh; ++k) col[k] -= gl[k - 1] * col[k - 1];
+      col[nh - 1] /= gd[nh - 1];
+      for (int k = nh - 2; k >= 0; --k) col[k] = col[k] / gd[k] - gl[k] * col[k + 1];
+      for (int k = 0; k < nh; ++k) gi[(size_t)k * np + c] = col[k];
+    }
+    rc |= up((void**)&d.gi, gi.data(), sizeof(double) * gi.size());
+  }
   if (rc) {
     for (void* p : ch->allocs) cudaFree(p);
     delete ch;
@@ -319,23 +331,24 @@ int mlr_matrix_stats(int64_t m, int n, int f32, const void* D, int64_t ldd, doub
   return matrix_stats(m, n, f32 != 0, D, ldd, work, blocks, out3, (cudaStream_t)stream);
 }
 
-int64_t mlr_eigh_work_doubles(int np) { return (int64_t)np * np + jacobi_partials_doubles(np) + 64; }
+int64_t mlr_eigh_work_doubles(int np) { return (int64_t)np * np + jacobi2_qbuf_elems(np) + np + 64; }
 
 int mlr_eigh_psd(int np, const double* B, double* V, double* lam, double tol, int max_sweeps, double* work,
                  int* info, void* stream) {
   if (np <= 0 || np % 64) { set_error("mlr_eigh_psd: np must be a positive multiple of 64"); return kErrArg; }
   cudaStream_t st = (cudaStream_t)stream;
   double* X = work;
-  double* part = work + (int64_t)np * np;
-  double* off = part + jacobi_partials_doubles(np);
+  double* qbuf = X + (int64_t)np * np;
+  double* off = qbuf + jacobi2_qbuf_elems(np);
   int* res = (int*)(off + 4);
+  int* qflag = res + 4;
   MLR_CUDA(cudaMemcpyAsync(X, B, sizeof(double) * np * np, cudaMemcpyDeviceToDevice, st));
   eye_kernel<<<256, 256, 0, st>>>(V, np);
   MLR_LAUNCH_CHECK("eye_kernel");
-  int rc = jacobi_eig(X, V, np, tol, max_sweeps, part, off, res, nullptr, st);
+  int rc = jacobi2_eig(false, X, V, np, np, tol, 1e-17, max_sweeps, qbuf, qflag, off, res, nullptr, st);
   if (rc) return rc;
-  eig_values_kernel<<<(np + 127) / 128, 128, 0, st>>>(np, X, V, lam);
-  MLR_LAUNCH_CHECK("eig_values_kernel");
+  diag_kernel<<<(np + 127) / 128, 128, 0, st>>>(np, X, lam);
+  MLR_LAUNCH_CHECK("diag_kernel");
   MLR_CUDA(cudaMemcpyAsync(info, res, sizeof(int), cudaMemcpyDeviceToHost, st));
   MLR_CUDA(cudaStreamSynchronize(st));
   return kOk;
@@ -433,6 +446,14 @@ int mlr_pcp_state(void* plan, double* out16, void* stream) {
   double v[16] = {(double)h.k, (double)h.done, (double)h.status, (double)h.rank, h.mu, h.mu_final, h.mu_last,
                   h.nuclear, h.sigma1, h.d_norm, (double)h.jac_sweeps, h.tau, h.scale, h.lam, 0.0, 0.0};
   std::memcpy(out16, v, sizeof(v));
+  return kOk;
+}
+int mlr_pcp_set_timing(void* plan, int enable) {
+  PLAN->timer.on = enable != 0;
+  return kOk;
+}
+int mlr_pcp_timing(void* plan, double* ms, int* counts) {
+  PLAN->timer.collect(ms, counts);
   return kOk;
 }
 int mlr_pcp_history(void* plan, int count, double* out, void* stream) {

@@ -60,8 +60,9 @@ int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out
 // sigma_i = sqrt(lambda_i); SVT weight f_i = max(sigma_i - tau, 0)/sigma_i;
 // rank = #{sigma_i > tau} (strict, pcp.py:258); nuclear = sum(sigma_i - tau)+
 // (pcp.py:264-267).  One CTA; f feeds the k-scaled NT GEMM P = V diag(f) V^T.
-__global__ void svt_weights_kernel(const int* __restrict__ skip, int np, int nh, const double* __restrict__ X,
-                                   const double* __restrict__ V, const double* tau_p, double* __restrict__ sig_out,
+template <typename T>
+__global__ void svt_weights_kernel(const int* __restrict__ skip, int np, int nh, const T* __restrict__ Bd,
+                                   const double* tau_p, double* __restrict__ sig_out,
                                    double* __restrict__ f_out, int* rank_out, double* nuclear_out) {
   if (skip && *skip) return;
   __shared__ double scratch[2 * 32];
@@ -70,8 +71,7 @@ __global__ void svt_weights_kernel(const int* __restrict__ skip, int np, int nh,
   for (int i = threadIdx.x; i < np; i += blockDim.x) {
     double f = 0.0, s = 0.0;
     if (i < nh) {
-      double lam = 0.0;
-      for (int r = 0; r < np; ++r) lam = fma(V[(int64_t)r * np + i], X[(int64_t)r * np + i], lam);
+      const double lam = (double)Bd[(int64_t)i * (np + 1)];  // diagonalised B~
       s = sqrt(fmax(lam, 0.0));
       if (s > tau) {
         f = (s - tau) / s;
@@ -90,9 +90,14 @@ __global__ void svt_weights_kernel(const int* __restrict__ skip, int np, int nh,
   }
 }
 
-int svt_weights(const int* skip, int np, int nh, const double* X, const double* V, const double* tau,
-                double* sig_out, double* f_out, int* rank_out, double* nuclear_out, cudaStream_t st) {
-  svt_weights_kernel<<<1, 1024, 0, st>>>(skip, np, nh, X, V, tau, sig_out, f_out, rank_out, nuclear_out);
+int svt_weights(const int* skip, int np, int nh, bool f32, const void* Bd, const double* tau, double* sig_out,
+                double* f_out, int* rank_out, double* nuclear_out, cudaStream_t st) {
+  if (f32)
+    svt_weights_kernel<float><<<1, 1024, 0, st>>>(skip, np, nh, (const float*)Bd, tau, sig_out, f_out, rank_out,
+                                                  nuclear_out);
+  else
+    svt_weights_kernel<double><<<1, 1024, 0, st>>>(skip, np, nh, (const double*)Bd, tau, sig_out, f_out, rank_out,
+                                                   nuclear_out);
   MLR_LAUNCH_CHECK("svt_weights_kernel");
   return kOk;
 }

@@ -157,14 +157,19 @@ int gemm_f64(GemmSpec g, cudaStream_t st) {
       g.c_f32 == std::is_same<TC, float>::value && g.trans_a == XA && g.trans_b == XB)            \
     return launch<TA, TB, TC, XA, XB>(g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.C, g.ldc,         \
                                       g.c_slice, g.splits, g.alpha, g.kscale, g.skip, st);
-  // Gram: A^T A with A float or double, C double
-  MLR_G(float, float, double, true, false)
-  MLR_G(double, double, double, true, false)
-  // reconstruction Z = A W: A float/double, W double, C float/double
-  MLR_G(float, double, float, false, false)
-  MLR_G(double, double, double, false, false)
-  // coarse products (double only): NN, NT
-  MLR_G(double, double, double, false, true)
+#define MLR_G_TYPES(XA, XB)                 \
+  MLR_G(float, float, float, XA, XB)        \
+  MLR_G(float, float, double, XA, XB)       \
+  MLR_G(float, double, float, XA, XB)       \
+  MLR_G(float, double, double, XA, XB)      \
+  MLR_G(double, float, float, XA, XB)       \
+  MLR_G(double, float, double, XA, XB)      \
+  MLR_G(double, double, float, XA, XB)      \
+  MLR_G(double, double, double, XA, XB)
+  MLR_G_TYPES(false, false)
+  MLR_G_TYPES(true, false)
+  MLR_G_TYPES(false, true)
+#undef MLR_G_TYPES
 #undef MLR_G
   set_error("gemm_f64: unsupported type/transpose combination");
   return kErrArg;

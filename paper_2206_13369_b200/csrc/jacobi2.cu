@@ -1,0 +1,561 @@
+// Two-sided block Jacobi eigensolver for the coarse SVT (replaces gesdd in
+// svd_full, reference linalg.py:86-99, as called by pcp.py:257).
+//
+// Input: B (np x np, symmetric PSD, row-major, FP64) already rotated into
+// the previous iteration's eigenbasis (B~ = V0^T B V0, the warm start) and
+// V = V0.  Output: B diagonal (eigenvalues on the diagonal) and V = V0 J.
+//
+// Columns are grouped in blocks of 16; a round-robin tournament over the
+// nb = np/16 blocks pairs them, npairs = nb/2 pairs per step.  Step 0 of a
+// sweep pairs (2k, 2k+1) and runs a full cyclic inner sweep (31 rounds of 16
+// disjoint 2x2 rotations) on each 32x32 diagonal sub-block, which also
+// clears the intra-block pairs; steps 1..nb-1 run the 16 cross rounds
+// (i, 16+(i+r)%16).  Each step:
+//   phase A  pair owner k: load the 32x32 sub-block G of B; rotate; rotated
+//            pairs are zeroed exactly with the classical diagonal update
+//            (a - t g, b + t g) so tiny eigenvalues next to large ones do not
+//            stagnate; publish Q_k and the rotated G_k              -- barrier
+//   phase B  all CTAs: B[pq_k1, pq_k2] <- Q_k1^T B[..] Q_k2 (k1 < k2, plus
+//            the mirror), B[pq_k, pq_k] <- G_k, V[rows, pq_k] <- V[rows, pq_k] Q_k
+//                                                                   -- barrier
+// Barriers are cluster barriers when the solve fits one 16-CTA cluster
+// (np <= 512), grid barriers (cooperative launch) otherwise.
+// Convergence: over a sweep every inspected pair has |g_ij| <= abs_floor or
+// |g_ij| <= tol * sqrt(|g_ii g_jj|).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace mlr {
+
+constexpr int J2_BW = 16, J2_PW = 32, J2_THREADS = 256, J2_LD = J2_PW + 4;
+
+struct J2Smem {
+  double G[J2_PW][J2_LD];
+  double Q[J2_PW][J2_LD];
+  double X[J2_PW][J2_LD];
+  double Y[J2_PW][J2_LD];
+  double Q2[J2_PW][J2_LD];
+  double cs[J2_PW / 2][3];  // c, s, t
+  int pr[J2_PW / 2][2];
+  int rotated;
+  int active;             // any pair of this block above tolerance
+  int round_rot[J2_PW];   // per inner round: any rotation applied
+  int qf[2];
+  double red[32];
+};
+
+// Rotation (c, s, t) that annihilates g in [[a, g], [g, b]]:
+// z = (b - a) / 2g, t = sign(z) / (|z| + sqrt(1 + z^2)), c = 1/sqrt(1+t^2).
+// FP32 estimates refined by Newton steps in FP64; c and s share t, so the
+// rotation is orthogonal to FP64 precision.
+// Written without z = (b-a)/2g: with d = b - a and h = sqrt(d^2 + 4 g^2),
+// t = 2g / (d + sign(d) h) — one sqrt, one division, one rsqrt on the
+// critical path of every inner round.
+__device__ __forceinline__ void jac_rot(double a, double b, double g, double& c, double& s, double& t) {
+  const double d = b - a, g2 = 2.0 * g;
+  const double h = sqrt(fma(d, d, g2 * g2));
+  t = g2 / (d >= 0.0 ? d + h : d - h);
+  c = rsqrt(fma(t, t, 1.0));
+  s = c * t;
+}
+
+__device__ __forceinline__ void j2_pair(int step, int k, int nb, int& pa, int& pb) {
+  if (step == 0) {
+    pa = 2 * k;
+    pb = 2 * k + 1;
+    return;
+  }
+  const int m = nb - 1, t = step - 1;
+  if (k == 0) {
+    pa = t;
+    pb = m;
+  } else {
+    pa = (t + k) % m;
+    pb = (t - k + m) % m;
+  }
+}
+
+__device__ __forceinline__ int j2_col(int l, int pa, int pb) {
+  return l < J2_BW ? pa * J2_BW + l : pb * J2_BW + (l - J2_BW);
+}
+
+__device__ __forceinline__ void atomic_max_nonneg2(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+template <bool CLUSTER>
+__device__ __forceinline__ void j2_sync() {
+  if (CLUSTER) cg::this_cluster().sync();
+  else cg::this_grid().sync();
+}
+
+// Load a 32x32 tile whose rows/cols are the two 16-blocks of a pair.
+__device__ __forceinline__ void load_pair_tile(double (*dst)[J2_LD], const double* __restrict__ src, int np,
+                                               int ra, int rb, int ca, int cb) {
+  double v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * J2_THREADS;
+    const int i = e >> 5, j = e & 31;
+    v[q] = src[(int64_t)j2_col(i, ra, rb) * np + j2_col(j, ca, cb)];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * J2_THREADS;
+    dst[e >> 5][e & 31] = v[q];
+  }
+}
+
+__device__ __forceinline__ void load_dense_tile(double (*dst)[J2_LD], const double* __restrict__ src) {
+  double v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = src[threadIdx.x + q * J2_THREADS];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * J2_THREADS;
+    dst[e >> 5][e & 31] = v[q];
+  }
+}
+
+__device__ __forceinline__ void j2_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// 32x32 tile product op(A) * B on the FP64 DMMA path (mma.sync m8n8k4):
+// warp w owns rows 8*(w>>1)..+8 and columns 16*(w&1)..+16 (two 8x8 tiles).
+// Output element q (0..3) of the calling thread sits at (tm_row(), tm_col(q)).
+__device__ __forceinline__ int tm_row() { return 8 * ((threadIdx.x >> 5) >> 1) + ((threadIdx.x & 31) >> 2); }
+__device__ __forceinline__ int tm_col(int q) {
+  return 16 * ((threadIdx.x >> 5) & 1) + 8 * (q >> 1) + 2 * (threadIdx.x & 3) + (q & 1);
+}
+
+template <bool TA>
+__device__ __forceinline__ void tile_mm(const double (*A)[J2_LD], const double (*B)[J2_LD], double (&o)[4]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = 8 * (w >> 1) + (lane >> 2);  // A fragment row
+  const int kk = lane & 3;
+  const int c0 = 16 * (w & 1) + (lane >> 2);  // B fragment column (tile 0)
+  o[0] = o[1] = o[2] = o[3] = 0.0;
+#pragma unroll
+  for (int k4 = 0; k4 < J2_PW; k4 += 4) {
+    const double a = TA ? A[k4 + kk][r] : A[r][k4 + kk];
+    const double b0 = B[k4 + kk][c0], b1 = B[k4 + kk][c0 + 8];
+    j2_dmma(o[0], o[1], a, b0);
+    j2_dmma(o[2], o[3], a, b1);
+  }
+}
+
+// Cycle breakdown of CTA 0 (phase A load+measure, inner rounds, barrier 1,
+// phase B, barrier 2, steps) — read with mlr_debug_j2prof.
+__device__ unsigned long long g_j2prof[8];
+
+__device__ __forceinline__ void j2_mark(int slot, long long& t0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t = clock64();
+    atomicAdd(&g_j2prof[slot], (unsigned long long)(t - t0));
+    t0 = t;
+  }
+}
+
+// Per-CTA schedule built once per launch: the pair table of every step and
+// this CTA's phase-B items (so the step loop does no integer div/mod).
+struct J2Item {
+  short kA, kB;  // pairs (kA == kB for V items)
+  short r0;      // V row chunk start (-1 for B items)
+  short pad;
+};
+
+template <bool CLUSTER>
+__global__ void __launch_bounds__(J2_THREADS)
+jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows_v, double tol,
+               double abs_floor_rel, int max_sweeps, double* __restrict__ Qbuf, double* __restrict__ Gbuf,
+               int* __restrict__ qflag, double* __restrict__ off_slots, int* __restrict__ result,
+               const int* __restrict__ skip, int cache_q, double early_off) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  J2Smem& S = *reinterpret_cast<J2Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int nb = np / J2_BW;
+  const int npairs = nb / 2;
+  const int nctas = CLUSTER ? (int)cg::this_cluster().num_blocks() : (int)gridDim.x;
+  const int me = CLUSTER ? (int)cg::this_cluster().block_rank() : (int)blockIdx.x;
+  const int nbitems = npairs * (npairs - 1) / 2;  // off-diagonal pair blocks k1 < k2
+  const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
+  const int nitems = nbitems + npairs * vchunks;
+  const int my_items = (nitems - me + nctas - 1) / nctas;
+  // dynamic smem: [J2Smem][Qcache npairs x 32 x LD (optional)][sched nb*npairs int][items][qslot npairs int]
+  unsigned char* p = smem_raw + ((sizeof(J2Smem) + 127) & ~size_t(127));
+  double(*Qall)[J2_PW][J2_LD] = reinterpret_cast<double(*)[J2_PW][J2_LD]>(p);
+  if (cache_q) p += (size_t)npairs * J2_PW * J2_LD * sizeof(double);
+  int* sched = reinterpret_cast<int*>(p);
+  p += (size_t)nb * npairs * sizeof(int);
+  J2Item* items = reinterpret_cast<J2Item*>(p);
+  p += (size_t)my_items * sizeof(J2Item);
+  int* qslot = reinterpret_cast<int*>(p);  // my needed pairs -> cache slot (or -1)
+  __shared__ int qf_all[64];
+  const double tol2 = tol * tol;
+
+  for (int e = tid; e < nb * npairs; e += J2_THREADS) {
+    const int step = e / npairs, k = e % npairs;
+    int pa, pb;
+    j2_pair(step, k, nb, pa, pb);
+    sched[e] = pa | (pb << 16);
+  }
+  for (int q = tid; q < my_items; q += J2_THREADS) {
+    const int it = me + q * nctas;
+    J2Item x;
+    if (it < nbitems) {
+      int k1 = 0, rem = it;
+      while (rem >= npairs - 1 - k1) {
+        rem -= npairs - 1 - k1;
+        ++k1;
+      }
+      x.kA = (short)k1;
+      x.kB = (short)(k1 + 1 + rem);
+      x.r0 = -1;
+    } else {
+      const int v = it - nbitems;
+      x.kA = x.kB = (short)(v / vchunks);
+      x.r0 = (short)((v % vchunks) * J2_PW);
+    }
+    x.pad = 0;
+    items[q] = x;
+  }
+  __syncthreads();
+  if (tid == 0) {  // compact list of the rotations this CTA reads
+    for (int k = 0; k < npairs; ++k) qslot[k] = -1;
+    for (int q = 0; q < my_items; ++q) {
+      qslot[items[q].kA] = 0;
+      qslot[items[q].kB] = 0;
+    }
+    int s = 0;
+    for (int k = 0; k < npairs; ++k)
+      if (qslot[k] == 0) qslot[k] = s++;
+  }
+  // absolute floor: abs_floor_rel * max_i |B_ii| (identical in every CTA)
+  double dmax = 0.0;
+  for (int i = tid; i < np; i += J2_THREADS) dmax = fmax(dmax, fabs(B[(int64_t)i * (np + 1)]));
+  dmax = warp_max(dmax);
+  if ((tid & 31) == 0) S.red[tid >> 5] = dmax;
+  __syncthreads();
+  if (tid == 0)
+    for (int w = 1; w < J2_THREADS / 32; ++w) S.red[0] = fmax(S.red[0], S.red[w]);
+  __syncthreads();
+  const double abs_floor = abs_floor_rel * S.red[0];
+
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int step = 0; step < nb; ++step) {
+      long long t0 = clock64();
+      if (blockIdx.x == 0 && tid == 0) atomicAdd(&g_j2prof[5], 1ull);
+      const int* srow = sched + step * npairs;
+      // ------------------------------------------------ phase A: pair owners
+      for (int k = me; k < npairs; k += nctas) {
+        const int pa = srow[k] & 0xffff, pb = srow[k] >> 16;
+        __syncthreads();
+        load_pair_tile(S.G, B, np, pa, pb, pa, pb);
+        for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) S.Q[e >> 5][e & 31] = (e >> 5) == (e & 31) ? 1.0 : 0.0;
+        if (tid == 0) {
+          S.rotated = 0;
+          S.active = 0;
+        }
+        if (tid < J2_PW) S.round_rot[tid] = 0;
+        __syncthreads();
+        if (step == 0 && k == 0 && tid == 0) off_slots[(sweep + 1) & 1] = 0.0;
+        {
+          double mx = 0.0;
+          for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) {
+            const int i = e >> 5, j = e & 31;
+            if (i < j && (step == 0 || (i < J2_BW && j >= J2_BW))) {
+              const double g = fabs(S.G[i][j]);
+              if (g > abs_floor) {
+                const double d = fabs(S.G[i][i] * S.G[j][j]);
+                mx = fmax(mx, d > 0.0 ? g * rsqrt(d) : 1e300);
+              }
+            }
+          }
+          mx = warp_max(mx);
+          if ((tid & 31) == 0 && mx > 0.0) atomic_max_nonneg2(&off_slots[sweep & 1], mx);
+          // a block whose inspected pairs are all below tolerance would not
+          // rotate in any round: skip the rounds entirely
+          if ((tid & 31) == 0 && mx > tol) S.active = 1;
+        }
+        __syncthreads();
+        j2_mark(0, t0);
+        const int rounds = !S.active ? 0 : (step == 0 ? J2_PW - 1 : J2_BW);
+        // pair k of inner round rnd: circle method on 32 players for step 0,
+        // cross pairs (k, 16 + (k + rnd) % 16) otherwise (computed, not loaded)
+        auto pair_of = [&](int k, int rnd, int& i, int& j) {
+          if (step == 0) {
+            const int m = J2_PW - 1;
+            if (k == 0) { i = rnd; j = m; } else { i = (rnd + k) % m; j = (rnd - k + m) % m; }
+          } else {
+            i = k;
+            j = J2_BW + ((k + rnd) & (J2_BW - 1));
+          }
+        };
+        double2* cs2 = reinterpret_cast<double2*>(&S.cs[0][0]);  // (c, s) per pair
+        double* tt = &S.cs[0][0] + J2_PW;                         // t per pair
+        for (int rnd = 0; rnd < rounds; ++rnd) {
+          if (tid < J2_PW / 2) {
+            int i, j;
+            pair_of(tid, rnd, i, j);
+            const double a = S.G[i][i], b = S.G[j][j], g = S.G[i][j];
+            double c = 1.0, s = 0.0, t = 0.0;
+            if (fabs(g) > abs_floor && g * g > tol2 * fabs(a * b)) {
+              jac_rot(a, b, g, c, s, t);
+              S.rotated = 1;
+              S.round_rot[rnd] = 1;
+            }
+            cs2[tid] = make_double2(c, s);
+            tt[tid] = t;
+          }
+          __syncthreads();
+          if (!S.round_rot[rnd]) continue;  // identity round: nothing to apply
+          {
+            // thread (pp, q) owns rows {p1,p2} x cols {q1,q2} of both
+            // G <- J^T G J (two-sided) and Q <- Q J (columns only)
+            const int pp = tid >> 4, q = tid & 15;
+            int p1, p2, q1, q2;
+            pair_of(pp, rnd, p1, p2);
+            pair_of(q, rnd, q1, q2);
+            const double2 csp = cs2[pp], csq = cs2[q];
+            const double cp = csp.x, sp = csp.y, cq = csq.x, sq = csq.y;
+            const double g11 = S.G[p1][q1], g12 = S.G[p1][q2], g21 = S.G[p2][q1], g22 = S.G[p2][q2];
+            const double x11 = S.Q[p1][q1], x12 = S.Q[p1][q2], x21 = S.Q[p2][q1], x22 = S.Q[p2][q2];
+            if (pp == q && tt[pp] != 0.0) {
+              // the rotated pair itself: exact zero + classical diagonal update
+              const double t = tt[pp];
+              S.G[p1][p1] = g11 - t * g12;
+              S.G[p2][p2] = g22 + t * g12;
+              S.G[p1][p2] = 0.0;
+              S.G[p2][p1] = 0.0;
+            } else {
+              const double t11 = cq * g11 - sq * g12, t12 = sq * g11 + cq * g12;
+              const double t21 = cq * g21 - sq * g22, t22 = sq * g21 + cq * g22;
+              S.G[p1][q1] = cp * t11 - sp * t21;
+              S.G[p1][q2] = cp * t12 - sp * t22;
+              S.G[p2][q1] = sp * t11 + cp * t21;
+              S.G[p2][q2] = sp * t12 + cp * t22;
+            }
+            S.Q[p1][q1] = cq * x11 - sq * x12;
+            S.Q[p1][q2] = sq * x11 + cq * x12;
+            S.Q[p2][q1] = cq * x21 - sq * x22;
+            S.Q[p2][q2] = sq * x21 + cq * x22;
+          }
+          __syncthreads();
+        }
+        j2_mark(1, t0);
+        // publish Q_k; the rotated diagonal block goes straight back into B
+        double* qo = Qbuf + (int64_t)k * J2_PW * J2_PW;
+        const bool rot = S.rotated != 0;
+        for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) {
+          const int i = e >> 5, j = e & 31;
+          qo[e] = S.Q[i][j];
+          if (rot) B[(int64_t)j2_col(i, pa, pb) * np + j2_col(j, pa, pb)] = S.G[i][j];
+        }
+        if (tid == 0) qflag[k] = S.rotated;
+      }
+      __threadfence();
+      j2_mark(6, t0);
+      j2_sync<CLUSTER>();
+      j2_mark(2, t0);
+      // ------------------------------------------------ phase B: apply
+      for (int k = tid; k < npairs; k += J2_THREADS) qf_all[k] = qflag[k];
+      __syncthreads();
+      if (cache_q) {  // the rotations my items read (rotated pairs only), via cp.async
+        for (int e2 = tid; e2 < npairs * J2_PW * J2_PW / 2; e2 += J2_THREADS) {
+          const int e = 2 * e2;
+          const int k = e >> 10;
+          const int slot = qslot[k];
+          if (slot >= 0 && qf_all[k]) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(&Qall[slot][(e >> 5) & 31][e & 31]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(Qbuf + e));
+          }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
+      auto live = [&](int q) {
+        const J2Item x = items[q];
+        return x.r0 >= 0 ? qf_all[x.kA] != 0 : (qf_all[x.kA] || qf_all[x.kB]);
+      };
+      auto fetch = [&](int q, double (&reg)[4]) {
+        const J2Item x = items[q];
+        const int a1 = srow[x.kA] & 0xffff, b1 = srow[x.kA] >> 16;
+        const int a2 = srow[x.kB] & 0xffff, b2 = srow[x.kB] >> 16;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = tid + u * J2_THREADS;
+          const int i = e >> 5, j = e & 31;
+          if (x.r0 >= 0)
+            reg[u] = (x.r0 + i < nrows_v) ? V[(int64_t)(x.r0 + i) * np + j2_col(j, a1, b1)] : 0.0;
+          else
+            reg[u] = B[(int64_t)j2_col(i, a1, b1) * np + j2_col(j, a2, b2)];
+        }
+      };
+      double cur[4], nxt[4];
+      int q = 0;
+      while (q < my_items && !live(q)) ++q;
+      if (q < my_items) fetch(q, cur);
+      while (q < my_items) {
+        int q2 = q + 1;
+        while (q2 < my_items && !live(q2)) ++q2;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = tid + u * J2_THREADS;
+          S.X[e >> 5][e & 31] = cur[u];
+        }
+        if (q2 < my_items) fetch(q2, nxt);
+        const J2Item x = items[q];
+        const double(*QA)[J2_LD] = cache_q ? Qall[qslot[x.kA]] : S.Q;
+        const double(*QB)[J2_LD] = cache_q ? Qall[qslot[x.kB]] : S.Q2;
+        if (!cache_q) {
+          load_dense_tile(S.Q, Qbuf + (int64_t)x.kA * J2_PW * J2_PW);
+          load_dense_tile(S.Q2, Qbuf + (int64_t)x.kB * J2_PW * J2_PW);
+        }
+        __syncthreads();
+        const int a1 = srow[x.kA] & 0xffff, b1 = srow[x.kA] >> 16;
+        const int a2 = srow[x.kB] & 0xffff, b2 = srow[x.kB] >> 16;
+        const int rr = tm_row();
+        double o[4];
+        if (x.r0 >= 0) {
+          tile_mm<false>(S.X, QA, o);  // V rows * Q_k
+          if (x.r0 + rr < nrows_v)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) V[(int64_t)(x.r0 + rr) * np + j2_col(tm_col(u), a1, b1)] = o[u];
+        } else {
+          // identity rotations were not cached: substitute I on the fly
+          if (!qf_all[x.kB]) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = S.X[rr][tm_col(u)];
+          } else {
+            tile_mm<false>(S.X, QB, o);  // Y = X Q_k2
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) S.Y[rr][tm_col(u)] = o[u];
+          __syncthreads();
+          if (!qf_all[x.kA]) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = S.Y[rr][tm_col(u)];
+          } else {
+            tile_mm<true>(QA, S.Y, o);  // Q_k1^T Y
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int gi = j2_col(rr, a1, b1), gj = j2_col(tm_col(u), a2, b2);
+            B[(int64_t)gi * np + gj] = o[u];
+            B[(int64_t)gj * np + gi] = o[u];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+        q = q2;
+      }
+      __threadfence();
+      j2_mark(3, t0);
+      j2_sync<CLUSTER>();
+      j2_mark(4, t0);
+    }
+    const double off = *((volatile double*)&off_slots[sweep & 1]);
+    // converged: nothing above tol this sweep, or (quadratic convergence)
+    // everything was already so small that this sweep's rotations pushed
+    // the off-diagonal below tol
+    if (off <= tol || off <= early_off) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (me == 0 && tid == 0) result[0] = converged ? sweep : -sweep;
+}
+
+static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
+                     double* Qbuf, double* Gbuf, int* qflag, double* off_slots, int* result, const int* skip,
+                     cudaStream_t st) {
+  const int nb = np / J2_BW;
+  const int npairs = nb / 2;
+  const bool cluster = np <= 512;
+  int nctas = 16;
+  if (!cluster) {
+    int dev = 0, nsm = 0;
+    MLR_CUDA(cudaGetDevice(&dev));
+    MLR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    nctas = std::max(1, std::min(std::max(npairs, npairs * (npairs + 1) / 4), nsm));
+  }
+  const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
+  const int nitems = npairs * (npairs - 1) / 2 + npairs * vchunks;
+  const size_t sched = (size_t)nb * npairs * sizeof(int) + (size_t)((nitems + nctas - 1) / nctas) * 8 +
+                       (size_t)npairs * sizeof(int) + 64;
+  const size_t qcache = (size_t)npairs * J2_PW * J2_LD * sizeof(double);
+  const int cache_q = (sizeof(J2Smem) + qcache + sched <= 200 * 1024) ? 1 : 0;
+  const size_t smem = ((sizeof(J2Smem) + 127) & ~size_t(127)) + (cache_q ? qcache : 0) + sched;
+  if (smem > 220 * 1024) {
+    set_error("jacobi2: schedule does not fit in shared memory");
+    return kErrArg;
+  }
+  // quadratic convergence: a sweep that started with every pair below
+  // ~sqrt(tol) leaves the off-diagonal ~ below tol, no verification sweep
+  const double early_off = 0.03 * std::sqrt(tol);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(J2_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.gridDim = dim3(nctas);
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cluster) {
+    auto kern = jacobi2_kernel<true>;
+    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    MLR_CUDA(cudaLaunchKernelEx(&cfg, kern, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps, Qbuf, Gbuf, qflag,
+                                off_slots, result, skip, cache_q, early_off));
+  } else {
+    auto kern = jacobi2_kernel<false>;
+    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    MLR_CUDA(cudaLaunchKernelEx(&cfg, kern, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps, Qbuf, Gbuf, qflag,
+                                off_slots, result, skip, cache_q, early_off));
+  }
+  return kOk;
+}
+
+int jacobi2_debug_prof(unsigned long long* out8) {
+  MLR_CUDA(cudaMemcpyFromSymbol(out8, g_j2prof, sizeof(unsigned long long) * 8));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  MLR_CUDA(cudaMemcpyToSymbol(g_j2prof, z, sizeof(z)));
+  return kOk;
+}
+
+// Qbuf and Gbuf, npairs x 32 x 32 doubles each, stored back to back.
+int64_t jacobi2_qbuf_elems(int np) { return 2 * (int64_t)(np / J2_BW / 2) * J2_PW * J2_PW; }
+
+int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
+                void* Qbuf, int* qflag, double* off_slots, int* result, const int* skip, cudaStream_t st) {
+  (void)f32;  // the coarse eigenproblem is always solved in FP64
+  if (np % 64 != 0) {
+    set_error("jacobi2_eig: n_p must be a multiple of 64");
+    return kErrArg;
+  }
+  MLR_CUDA(cudaMemsetAsync(off_slots, 0, 2 * sizeof(double), st));
+  double* q = (double*)Qbuf;
+  double* g = q + jacobi2_qbuf_elems(np) / 2;
+  return launch_j2((double*)B, (double*)V, np, nrows_v, tol, abs_floor_rel, max_sweeps, q, g, qflag, off_slots,
+                   result, skip, st);
+}
+
+}  // namespace mlr

@@ -27,10 +27,6 @@ int gemm_f64(GemmSpec g, cudaStream_t st);
 int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- jacobi
-int jacobi_block_width(int np);
-int64_t jacobi_partials_doubles(int np);
-int jacobi_eig(double* X, double* V, int np, double tol, int max_sweeps, double* partials,
-               double* off_slots, int* result, const int* skip, cudaStream_t st);
 
 // ---------------------------------------------------------------- chain
 // Composite restriction R (n x n_h) in stencil form.  Fine column j has
@@ -44,12 +40,17 @@ struct ChainDev {
   int* lo; int* hi;     // [nh]
   double* gl;           // LDL^T of G_R = R^T R: multipliers l[k], k < nh-1
   double* gd;           // pivots d[k]
+  double* gi;           // dense G_R^{-1}, np x np (zero padded)
   int max_span;         // max hi-lo
 };
 
 int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out, int trans_in,
               cudaStream_t st);
-int svt_weights(const int* skip, int np, int nh, const double* X, const double* V, const double* tau,
-                double* sig_out, double* f_out, int* rank_out, double* nuclear_out, cudaStream_t st);
+int svt_weights(const int* skip, int np, int nh, bool f32, const void* Bd, const double* tau, double* sig_out,
+                double* f_out, int* rank_out, double* nuclear_out, cudaStream_t st);
+int64_t jacobi2_qbuf_elems(int np);
+int jacobi2_debug_prof(unsigned long long* out8);
+int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
+                void* Qbuf, int* qflag, double* off_slots, int* result, const int* skip, cudaStream_t st);
 
 }  // namespace mlr

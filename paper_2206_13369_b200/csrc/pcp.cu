@@ -57,17 +57,24 @@ __global__ void input_stats_kernel(const T* __restrict__ D, int64_t ldd, int64_t
   }
 }
 
-__global__ void input_stats_finish(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+__global__ void __launch_bounds__(256) input_stats_finish(const double* __restrict__ part, int nparts,
+                                                          double* __restrict__ out) {
+  __shared__ double scratch[2 * 32];
+  __shared__ double smx[32];
+  double v[2] = {0.0, 0.0}, mx = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+    v[0] += part[3 * b];
+    mx = fmax(mx, part[3 * b + 1]);
+    v[1] += part[3 * b + 2];
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+  block_sum<2>(v, scratch);
   if (threadIdx.x == 0) {
-    double s = 0.0, mx = 0.0, bad = 0.0;
-    for (int b = 0; b < nparts; ++b) {
-      s += part[3 * b];
-      mx = fmax(mx, part[3 * b + 1]);
-      bad += part[3 * b + 2];
-    }
-    out[0] = s;
-    out[1] = mx;
-    out[2] = bad;
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) smx[0] = fmax(smx[0], smx[w]);
+    out[0] = v[0];
+    out[1] = smx[0];
+    out[2] = v[1];
   }
 }
 
@@ -197,13 +204,14 @@ __global__ void __launch_bounds__(1024) lz_update_kernel(LanczosDev* lz, double*
   __syncthreads();
   // full reorthogonalisation, twice (classical Gram-Schmidt)
   for (int pass = 0; pass < 2; ++pass) {
-    for (int c = 0; c <= k; ++c) {
+    // h = Q^T w: one warp per basis vector (all dots in flight at once)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int c = wid; c <= k; c += nwarps) {
       const double* qc = Q + (int64_t)c * n;
       double d = 0.0;
-      for (int j = threadIdx.x; j < n; j += blockDim.x) d = fma(qc[j], w[j], d);
-      double vv[1] = {d};
-      block_sum<1>(vv, scratch);
-      if (threadIdx.x == 0) h[c] = vv[0];
+      for (int j = lane; j < n; j += 32) d = fma(qc[j], w[j], d);
+      d = warp_sum(d);
+      if (lane == 0) h[c] = d;
     }
     __syncthreads();
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -419,13 +427,16 @@ pcp_row_kernel(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* _
   }
 }
 
-__global__ void stats_reduce_kernel(const double* __restrict__ part, int nparts, int nv, double* __restrict__ out) {
-  const int q = threadIdx.x;
-  if (q < nv) {
-    double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += part[nv * b + q];
-    out[q] = s;
-  }
+// Sum nv-wide per-CTA partials (256 threads, fixed order -> deterministic).
+__global__ void __launch_bounds__(256) stats_reduce_kernel(const double* __restrict__ part, int nparts, int nv,
+                                                           double* __restrict__ out) {
+  __shared__ double scratch[3 * 32];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+    for (int q = 0; q < nv && q < 3; ++q) v[q] += part[nv * b + q];
+  block_sum<3>(v, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < nv && q < 3; ++q) out[q] = v[q];
 }
 
 // ------------------------------------------------------------ host-side drivers
@@ -468,7 +479,7 @@ int pcp_input_stats(PcpPlan* p, const void* D, int64_t ldd, double* out2, cudaSt
   else
     input_stats_kernel<double><<<blocks, 256, 0, st>>>((const double*)D, ldd, p->m_local, p->ch.n, p->row_part);
   MLR_LAUNCH_CHECK("input_stats_kernel");
-  input_stats_finish<<<1, 32, 0, st>>>(p->row_part, blocks, out2);
+  input_stats_finish<<<1, 256, 0, st>>>(p->row_part, blocks, out2);
   MLR_LAUNCH_CHECK("input_stats_finish");
   return kOk;
 }
@@ -484,7 +495,7 @@ int matrix_stats(int64_t m, int n, bool f32, const void* D, int64_t ldd, double*
   else
     input_stats_kernel<double><<<blocks, 256, 0, st>>>((const double*)D, ldd, m, n, part);
   MLR_LAUNCH_CHECK("input_stats_kernel");
-  input_stats_finish<<<1, 32, 0, st>>>(part, blocks, out3);
+  input_stats_finish<<<1, 256, 0, st>>>(part, blocks, out3);
   MLR_LAUNCH_CHECK("input_stats_finish");
   return kOk;
 }
@@ -529,6 +540,9 @@ int pcp_start(PcpPlan* p, const void* D, int64_t ldd, void* Y0, int64_t ldy, con
               double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
               cudaStream_t st) {
   p->jac_tol_host = jac_tol;
+  // off-diagonals below floor_rel * max(diag) count as converged: the Gram
+  // itself is only accurate to ~eps * |B| (FP64 accumulation of T-precision A)
+  p->jac_floor_rel = p->f32 ? 1e-13 : 1e-17;
   pcp_start_scalars<<<1, 1, 0, st>>>(p->dev, p->lz, in_stats, lam, mu0, rho, tol, max_iters, time_budget, jac_tol,
                                      (double)p->m_global, (double)p->ch.n);
   MLR_LAUNCH_CHECK("pcp_start_scalars");
@@ -542,6 +556,7 @@ int pcp_start(PcpPlan* p, const void* D, int64_t ldd, void* Y0, int64_t ldy, con
 int pcp_gram(PcpPlan* p, double* red, int with_stats, cudaStream_t st) {
   const int np = p->ch.np;
   const int64_t nn = (int64_t)np * np;
+  p->timer.begin(st);
   if (p->m_local > 0) {
     GemmSpec g{};
     g.M = np; g.N = np; g.K = (int)p->m_local;
@@ -558,19 +573,22 @@ int pcp_gram(PcpPlan* p, double* red, int with_stats, cudaStream_t st) {
   }
   if (with_stats) {
     if (p->m_local > 0) {
-      stats_reduce_kernel<<<1, 32, 0, st>>>(p->row_part, p->row_blocks, 3, red + nn);
+      stats_reduce_kernel<<<1, 256, 0, st>>>(p->row_part, p->row_blocks, 3, red + nn);
       MLR_LAUNCH_CHECK("stats_reduce_kernel");
     } else {
       MLR_CUDA(cudaMemsetAsync(red + nn, 0, 3 * sizeof(double), st));
     }
   }
+  p->timer.end(kPhGram, st);
   return kOk;
 }
 
 int pcp_finalize(PcpPlan* p, const double* red, cudaStream_t st) {
   const int64_t nn = (int64_t)p->ch.np * p->ch.np;
+  p->timer.begin(st);
   pcp_finalize_kernel<<<1, 1, 0, st>>>(p->dev, red + nn, p->hist, p->jac_result);
   MLR_LAUNCH_CHECK("pcp_finalize_kernel");
+  p->timer.end(kPhFinalize, st);
   return kOk;
 }
 
@@ -580,31 +598,40 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   const int np = p->ch.np;
   const int* skip = &p->dev->done;
   int rc;
-  // T1 = G^-1 K (column solves), B = G^-1 T1^T  (= G^-1 K G^-1, K symmetric)
-  if ((rc = ldl_solve(skip, p->ch, red, p->T1, 0, st))) return rc;
-  if ((rc = ldl_solve(skip, p->ch, p->T1, p->Bm, 1, st))) return rc;
-  // X = B V
-  GemmSpec g{};
-  g.M = np; g.N = np; g.K = np;
-  g.A = p->Bm; g.lda = np; g.a_f32 = false; g.trans_a = false;
-  g.B = p->Vm; g.ldb = np; g.b_f32 = false; g.trans_b = false;
-  g.C = p->Xm; g.ldc = np; g.c_f32 = false; g.c_slice = 0; g.splits = 1; g.alpha = 1.0;
-  g.kscale = nullptr; g.skip = skip;
-  if ((rc = gemm_f64(g, st))) return rc;
-  if ((rc = jacobi_eig(p->Xm, p->Vm, np, p->jac_tol_host, p->jac_max_sweeps, p->jac_partials, p->jac_off,
-                       p->jac_result, skip, st)))
+  // Warm start: with V the previous eigenvectors and U = G^-1 V,
+  //   B~ = V^T (G^-1 K G^-1) V = U^T K U       (M_H = A G^-1, B = M_H^T M_H)
+  p->timer.begin(st);
+  auto mm = [&](const double* A, bool ta, const double* Bp, bool tb, double* C, const double* ks) {
+    GemmSpec g{};
+    g.M = np; g.N = np; g.K = np;
+    g.A = A; g.lda = np; g.a_f32 = false; g.trans_a = ta;
+    g.B = Bp; g.ldb = np; g.b_f32 = false; g.trans_b = tb;
+    g.C = C; g.ldc = np; g.c_f32 = false; g.c_slice = 0; g.splits = 1; g.alpha = 1.0;
+    g.kscale = ks; g.skip = skip;
+    return gemm_f64(g, st);
+  };
+  if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;   // U = G^-1 V
+  if ((rc = mm(red, false, p->T1, false, p->Xm, nullptr))) return rc;        // T = K U
+  if ((rc = mm(p->T1, true, p->Xm, false, p->Bm, nullptr))) return rc;       // B~ = U^T T
+  p->timer.end(kPhPre, st);
+  p->timer.begin(st);
+  if ((rc = jacobi2_eig(false, p->Bm, p->Vm, np, np, p->jac_tol_host, p->jac_floor_rel, p->jac_max_sweeps, p->qbuf,
+                        p->qflag, p->jac_off, p->jac_result, skip, st)))
     return rc;
+  p->timer.end(kPhJacobi, st);
+  p->timer.begin(st);
   pcp_after_jacobi<<<1, 1, 0, st>>>(p->dev, p->jac_result);
   MLR_LAUNCH_CHECK("pcp_after_jacobi");
-  if ((rc = svt_weights(skip, np, p->ch.nh, p->Xm, p->Vm, &p->dev->tau, p->sig, p->fw, &p->dev->rank,
+  // lambda_i = diag(B~) after convergence; f_i = (sigma_i - tau)+ / sigma_i
+  if ((rc = svt_weights(skip, np, p->ch.nh, false, p->Bm, &p->dev->tau, p->sig, p->fw, &p->dev->rank,
                         &p->dev->nuclear, st)))
     return rc;
-  // P = V diag(f) V^T
-  g.A = p->Vm; g.trans_a = false; g.B = p->Vm; g.trans_b = true; g.C = p->T1; g.kscale = p->fw;
-  if ((rc = gemm_f64(g, st))) return rc;
-  // W~ = G^-1 P
-  if ((rc = ldl_solve(skip, p->ch, p->T1, p->Wm, 0, st))) return rc;
+  // W~ = G^-1 V diag(f) V^T = U' diag(f) V^T with U' = G^-1 V
+  if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;
+  if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw))) return rc;
+  p->timer.end(kPhPost, st);
   // Z = A W~
+  p->timer.begin(st);
   if (p->m_local > 0) {
     GemmSpec z{};
     z.M = (int)p->m_local; z.N = np; z.K = np;
@@ -614,12 +641,16 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
     z.kscale = nullptr; z.skip = skip;
     if ((rc = gemm_f64(z, st))) return rc;
   }
+  p->timer.end(kPhRecon, st);
   return kOk;
 }
 
 int pcp_update(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy, cudaStream_t st) {
-  return p->f32 ? row_pass<float>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st)
-                : row_pass<double>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st);
+  p->timer.begin(st);
+  int rc = p->f32 ? row_pass<float>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st)
+                  : row_pass<double>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st);
+  p->timer.end(kPhUpdate, st);
+  return rc;
 }
 
 // Final L = Z R^T and S = shrink(D - L + Y_{k-1}/mu_k, lam/mu_k).

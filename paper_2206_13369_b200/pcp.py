@@ -19,6 +19,10 @@ from .runtime import SINGLE, Comm, as_device_matrix, give_back
 
 LANCZOS_TOL = 1e-15
 
+# When set to a list, solves record per-phase CUDA-event timings into it
+# (one dict per solve; used by bench.py for the roofline figures).
+TIMING_SINK = None
+
 
 def _zero_state(shape, kind, like):
     z = torch.zeros(shape, dtype=like.dtype, device=like.device)
@@ -30,7 +34,7 @@ def _zero_state(shape, kind, like):
 def _jacobi_tol(opts, f32):
     if opts.jacobi_tol is not None:
         return float(opts.jacobi_tol)
-    return 1e-10 if f32 else 64 * np.finfo(np.float64).eps
+    return 1e-9 if f32 else 64 * np.finfo(np.float64).eps
 
 
 def run_ialm(be, comm, D, m_global, n, opts, lam, check_every):
@@ -47,14 +51,16 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every):
     if sumsq == 0.0:
         return None
     opts.validate()
-    # sigma_1(D) by Lanczos on D^T D (pcp.py:100, 114)
+    # sigma_1(D) by Lanczos on D^T D (pcp.py:100, 114); float32 data only
+    # needs sigma_1 to ~1e-10 (mu0 = 1.25/sigma_1 scales every later mu)
+    lz_tol = LANCZOS_TOL if D.dtype == torch.float64 else 1e-11
     be.lanczos_init()
     steps = 0
     while True:
         for _ in range(4):
             w = be.lanczos_matvec(D)
             comm.sum(w)
-            be.lanczos_update(w, LANCZOS_TOL)
+            be.lanczos_update(w, lz_tol)
             steps += 1
         if be.lanczos_state()["done"]:
             break
@@ -115,8 +121,16 @@ def ml_ialm_solve(d, opts=None):
         opts_checked = _checked_width(n, m, opts)
         chain = build_chain(n, opts_checked)
         be = CudaPcp(chain, m, m, D.dtype == torch.float32, opts.max_iters, D.device)
+        if TIMING_SINK is not None:
+            be.set_timing(True)
         try:
             out = run_ialm(be, SINGLE, D, m, n, opts, lam, _check_every(opts))
+            if TIMING_SINK is not None:
+                t = be.timing()
+                t["iters"] = out[3]["k"] if out is not None else 0
+                t["jac_sweeps"] = [int(x) for x in out[4][:, 6]] if out is not None else []
+                t["lanczos_steps"] = be.lanczos_state()["k"] + 1
+                TIMING_SINK.append(t)
         finally:
             be.close()
     if out is None:

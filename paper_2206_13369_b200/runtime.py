@@ -33,7 +33,12 @@ class Comm:
     def gather(self, out, t):
         """out (world * t.numel()) <- concatenation of every rank's t."""
         if self.world > 1:
-            dist.all_gather_into_tensor(out, t, group=self.group)
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(out, t, group=self.group)
+            else:
+                parts = [torch.empty_like(t) for _ in range(self.world)]
+                dist.all_gather(parts, t, group=self.group)
+                out.copy_(torch.cat(parts))
         else:
             out.copy_(t)
         return out

@@ -1,0 +1,150 @@
+"""Pins the CPU oracle (oracle/mlrpca_oracle.py) against the reference's own
+known-answer tests (pkg/tests/test_linalg.py, pkg/tests/test_multilevel.py)
+and against golden vectors produced by the real reference
+(tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+from numpy.testing import assert_allclose
+
+from oracle import mlrpca_oracle as O
+
+
+# ---------------------------------------------------------------- KATs (reference tests restated)
+
+def test_soft_threshold_kat():  # test_linalg.py:25-27
+    assert_allclose(O.soft_threshold(np.array([[1.0, -0.3, 0.7]]), 0.5), [[0.5, 0.0, 0.2]], atol=1e-15)
+
+
+def test_soft_threshold_composition():  # test_linalg.py:41-48
+    rng = np.random.default_rng(1)
+    for _ in range(10):
+        x = rng.standard_normal((6, 4)) * rng.uniform(0.1, 5)
+        a, b = rng.uniform(0, 1, size=2)
+        assert_allclose(O.soft_threshold(O.soft_threshold(x, b), a), O.soft_threshold(x, a + b), atol=1e-12)
+
+
+def test_soft_threshold_negative_tau():
+    with pytest.raises(ValueError):
+        O.soft_threshold(np.ones((2, 2)), -0.1)
+
+
+def test_svt_diag_and_tie():  # test_linalg.py:121-144
+    z, r = O.svt(np.diag([3.0, 1.0]), 2.0)
+    assert r == 1
+    assert_allclose(z, np.diag([1.0, 0.0]), atol=1e-12)
+    z, r = O.svt(np.diag([3.0, 2.0]), 2.0)
+    assert r == 1
+    assert_allclose(z, np.diag([1.0, 0.0]), atol=1e-12)
+
+
+def test_r6_worked_example():  # test_multilevel.py:17-27
+    expected = 0.5 * np.array([[2, 2, 1, 0, 0, 0], [0, 0, 1, 2, 1, 0], [0, 0, 0, 0, 1, 2]]).T
+    assert np.array_equal(O.build_interpolation(6).toarray(), expected)
+
+
+@pytest.mark.parametrize("n", [3, 5, 6, 7, 8, 13, 25, 64])
+def test_interpolation_row_sums(n):  # test_multilevel.py:34-48
+    assert_allclose(O.build_interpolation(n).toarray().sum(axis=1), np.ones(n), atol=0)
+
+
+def test_chain_normalised_and_left_inverse():  # test_multilevel.py:75-97
+    ch = O.build_chain(64, 8)
+    r = ch.composite.toarray()
+    assert abs(np.linalg.svd(r, compute_uv=False)[0] - 1.0) <= 1e-10
+    assert_allclose(np.linalg.pinv(r) @ r, np.eye(8), atol=1e-10)
+    with pytest.raises(ValueError, match="not reachable"):
+        O.build_chain(8, 3)
+
+
+def test_select_levels_cases():  # test_multilevel.py:100-117
+    assert O.select_levels(1024, 5, 1, 10000) == 8
+    assert O.coarse_sizes(400) == [400, 200, 100, 50, 25, 13, 7, 4, 2, 1]
+    assert O.select_levels(400, 2, 1, 3072) == 4
+    with pytest.raises(O.LevelError):
+        O.select_levels(6, 10, 1, 100)
+    with pytest.warns(RuntimeWarning):
+        O.select_levels(64, 30, 1, 10)
+
+
+def test_ls_restriction_inverts_prolong():  # test_multilevel.py:162-166
+    ch = O.build_chain(32, 8)
+    x = np.random.default_rng(4).standard_normal((6, 8))
+    assert_allclose(O.restrict_least_squares(O.prolong(x, ch), ch), x, atol=1e-10)
+
+
+# ---------------------------------------------------------------- golden vectors from the reference
+
+def test_golden_multilevel(golden):
+    g = golden("multilevel")
+    assert np.array_equal(O.build_interpolation(6).toarray(), g["R6"])
+    for key in [k for k in g if k.startswith("R_")]:
+        _, n, t = key.split("_")
+        ch = O.build_chain(int(n), int(t))
+        assert np.array_equal(ch.composite.toarray(), g[key]), key
+        assert ch.spectral_norm == float(g[f"spec_{n}_{t}"])
+    for key in [k for k in g if k.startswith("Rcsr_") and k.endswith("_data")]:
+        _, n, t, _ = key.split("_")
+        r = O.build_chain(int(n), int(t)).composite.tocsr()
+        assert np.array_equal(r.data, g[key])
+        assert np.array_equal(r.indices, g[f"Rcsr_{n}_{t}_indices"])
+    assert list(g["coarse_sizes_400"]) == O.coarse_sizes(400)
+    ch = O.build_chain(100, 25)
+    assert_allclose(O.restrict(g["restrict_x"], ch), g["restrict_y"], rtol=0, atol=1e-15)
+    assert_allclose(O.restrict_least_squares(g["restrict_x"], ch), g["restrict_ls_y"], atol=1e-13)
+    assert_allclose(O.prolong(g["restrict_y"], ch), g["prolong_y"], atol=1e-15)
+
+
+def test_golden_linalg(golden):
+    g = golden("linalg")
+    assert_allclose(O.soft_threshold(g["st_in"], 0.5), g["st_out"], atol=0)
+    z, r = O.svt(g["svt_x"], 1.5)
+    assert r == int(g["svt_rank"])
+    assert_allclose(z, g["svt_z"], atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["pcp_f64_small", "pcp_f32_small", "pcp_f64_odd"])
+def test_golden_ml_ialm(golden, name):
+    g = golden(name)
+    st = O.ml_ialm(g["d"], levels=int(g["n_coarse"]), tol=float(g["tol"]))
+    assert st.iter == int(g["iter"])
+    assert_allclose(st.l, g["l"], rtol=0, atol=1e-12 * np.abs(g["l"]).max())
+    assert_allclose(st.s, g["s"], rtol=0, atol=1e-12 * np.abs(g["s"]).max())
+    assert_allclose([h.feasibility_gap for h in st.history], g["h_gap"], rtol=1e-10)
+    assert [h.rank_l for h in st.history] == list(g["h_rank"])
+
+
+@pytest.mark.parametrize("name", ["fwt_f64_small", "fwt_f32_small", "fwt_f64_full"])
+def test_golden_ml_fwt(golden, name):
+    g = golden(name)
+    mask = g.get("mask")
+    st = O.ml_fwt(g["d"], mask, float(g["lam_l"]), float(g["lam_s"]), tol=float(g["tol"]),
+                  max_iters=int(g["max_iters"]), levels=int(g["n_coarse"]), collect_rank=False)
+    # same numpy/OpenBLAS build -> the restatement tracks the reference closely;
+    # FW-T is sensitive to rounding, so compare the objective
+    assert abs(st.iter - int(g["iter"])) <= 2
+    k = min(len(st.objective_history), len(g["h_obj"]))
+    assert_allclose(st.objective_history[:k], g["h_obj"][:k], rtol=1e-6)
+
+
+def test_golden_c1_summary(golden):
+    g = golden("pcp_c1_summary")
+    d, _ = O.make_config("C1", 0)
+    assert float(d.sum()) == float(g["d_sum"])
+    st = O.ml_ialm(d, lam=1 / np.sqrt(500), tol=1e-7, levels=125)
+    assert st.iter == int(g["iter"])
+    assert_allclose(np.linalg.norm(st.l), float(g["l_fro"]), rtol=1e-12)
+    assert_allclose(st.l[g["rows"]], g["l_rows"], atol=1e-12)
+
+
+def test_oracle_matches_live_reference(reference):
+    """In the build container: bitwise agreement with the real reference."""
+    d, mask = O.gaussian_rpca(90, 64, 4, 0.1, 11, observe=0.8)
+    ref = reference.ml_ialm_solve(d, reference.PcpOptions(levels=16))
+    got = O.ml_ialm(d, levels=16)
+    assert ref.iter == got.iter and np.array_equal(ref.l, got.l) and np.array_equal(ref.s, got.s)
+    lam = 1 / np.sqrt(90)
+    ref2 = reference.ml_fwt_solve(d, reference.ObservationMask(mask), reference.CpcpOptions(
+        lambda_l=lam, lambda_s=lam / np.sqrt(90), tol=1e-5, levels=16, collect_rank=False))
+    got2 = O.ml_fwt(d, mask, lam, lam / np.sqrt(90), tol=1e-5, levels=16, collect_rank=False)
+    assert ref2.iter == got2.iter and np.array_equal(ref2.l, got2.l)
