@@ -129,6 +129,9 @@ int mlr_cpcp_outputs(void* plan, void* L, int64_t ldl, void* stream);
 /* out32: k, done, status, t_l, t_s, u_l, u_s, sigma, passes, ga, gb, corner_l, corner_s, i_s, j_s, s2, ... */
 int mlr_cpcp_state(void* plan, double* out32, void* stream);
 int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, void* stream); /* count x 8, count */
+/* Per-phase CUDA-event timing (7 slots: gram, power, dots, qp, unused, update, finalize). */
+int mlr_cpcp_set_timing(void* plan, int enable);
+int mlr_cpcp_timing(void* plan, double* ms7, int* counts7);
 
 #ifdef __cplusplus
 }

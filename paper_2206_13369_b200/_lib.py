@@ -74,6 +74,8 @@ _SIGS = {
     "mlr_cpcp_outputs": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "mlr_cpcp_state": (c_int, [c_void_p, c_void_p, c_void_p]),
     "mlr_cpcp_history": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "mlr_cpcp_set_timing": (c_int, [c_void_p, c_int]),
+    "mlr_cpcp_timing": (c_int, [c_void_p, c_void_p, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

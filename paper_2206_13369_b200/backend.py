@@ -211,6 +211,17 @@ class CudaCpcp:
             d[k] = int(d[k])
         return d
 
+    PHASES = ("gram", "power", "dots", "qp", "unused", "update", "finalize")
+
+    def set_timing(self, on):
+        _lib.check(self.lib.mlr_cpcp_set_timing(self.h, int(bool(on))))
+
+    def timing(self):
+        ms = np.zeros(7)
+        cnt = np.zeros(7, dtype=np.int32)
+        _lib.check(self.lib.mlr_cpcp_timing(self.h, ms.ctypes.data, cnt.ctypes.data))
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES) if p != "unused"}
+
     def history(self, count):
         out = np.zeros((max(count, 1), 8))
         objs = np.zeros(max(count, 1))

@@ -20,6 +20,10 @@ from .chain import build_chain, resolve_coarse_width
 from .runtime import SINGLE, Comm, as_device_matrix, give_back
 
 
+# When set to a list, solves record per-phase CUDA-event timings into it.
+TIMING_SINK = None
+
+
 def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every):
     st = be.input_stats(D)
     comm.sum(st[2:3])
@@ -99,8 +103,14 @@ def ml_fwt_solve(d, mask=None, opts=None):
         radius = 1.0 / chain.sigma_max()
         bits = _mask_bits(mask, (m, n), D.device)
         be = CudaCpcp(chain, m, m, 0, D.dtype == torch.float32, opts.max_iters, 1, D.device)
+        if TIMING_SINK is not None:
+            be.set_timing(True)
         try:
             out = run_fwt(be, SINGLE, D, bits, m, opts, radius, _check_every(opts))
+            if TIMING_SINK is not None:
+                t = be.timing()
+                t["iters"] = out[2]["k"]
+                TIMING_SINK.append(t)
         finally:
             be.close()
     return _state_from(*out, kind)

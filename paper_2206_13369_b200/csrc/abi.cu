@@ -249,6 +249,11 @@ int mlr_chain_create(int n, int nh, const int32_t* c0, const double* w0, const d
   d.nh = nh;
   d.np = np;
   d.max_span = span;
+  {
+    bool dense = n > 0 && c0[0] == 0 && c0[n - 1] >= nh - 2;
+    for (int j = 1; j < n && dense; ++j) dense = c0[j] - c0[j - 1] <= 1;
+    d.keys_dense = dense ? 1 : 0;
+  }
   auto up = [&](void** dst, const void* src, size_t bytes) -> int {
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 8));
@@ -529,6 +534,14 @@ int mlr_cpcp_state(void* plan, double* out32, void* stream) {
                   (double)h.j_s, h.s2, h.pd_norm, h.sq, h.l1, h.nnz, h.ss, h.sr, h.r_is, h.s_is, h.spike,
                   (double)h.none, h.coef, 0, 0, 0, 0, 0};
   std::memcpy(out32, v, sizeof(v));
+  return kOk;
+}
+int mlr_cpcp_set_timing(void* plan, int enable) {
+  PLAN->timer.on = enable != 0;
+  return kOk;
+}
+int mlr_cpcp_timing(void* plan, double* ms, int* counts) {
+  PLAN->timer.collect(ms, counts);
   return kOk;
 }
 int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, void* stream) {

@@ -30,6 +30,7 @@ constexpr int kErrArg = 1;
 constexpr int kErrCuda = 2;
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+__host__ __device__ __forceinline__ int round_up_dev(int x, int a) { return (x + a - 1) / a * a; }
 inline int64_t ceil_div(int64_t x, int64_t a) { return (x + a - 1) / a; }
 
 // ---------------------------------------------------------------- reductions

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "cpcp.h"
 #include "kernels.h"
+#include "rows.h"
 
 namespace cg = cooperative_groups;
 
@@ -571,6 +572,8 @@ template <typename T, int MODE>
 static int cp_row(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
                   void* Lout, int64_t ldl, cudaStream_t st) {
   if (p->m_local == 0) return kOk;
+  if (rows_warp_ok(p->ch, p->f32))  // streaming warp-per-row path (rows.cu)
+    return cp_rows(p, MODE, D, ldd, mask, ldm, S, lds, Lout, ldl, st);
   size_t smem = sizeof(T) * (size_t)(p->ch.np + 2 + 2 * p->ch.n);
   if (smem > 200 * 1024) {
     set_error("cpcp row kernel: fine row does not fit in shared memory");
@@ -613,6 +616,7 @@ int cpcp_start(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, in
 int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st) {
   const int np = p->ch.np;
   const int64_t nn = (int64_t)np * np;
+  p->timer.begin(st);
   if (p->m_local > 0) {
     GemmSpec g{};
     g.M = np; g.N = np; g.K = (int)p->m_local;
@@ -632,6 +636,7 @@ int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st) {
     MLR_CUDA(cudaMemcpyAsync(amax, empty.data(), 4 * sizeof(double), cudaMemcpyHostToDevice, st));
     MLR_CUDA(cudaStreamSynchronize(st));
   }
+  p->timer.end(0, st);
   return kOk;
 }
 
@@ -663,10 +668,18 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  p->timer.begin(st);
   MLR_CUDA(cudaLaunchKernelEx(&cfg, cp_power_kernel, p->dev, (const double*)red, np, p->v, p->vin, fit ? 1 : 0));
   cp_lmo_scalars<<<1, 1, 0, st>>>(p->dev, amax_all, p->world);
   MLR_LAUNCH_CHECK("cp_lmo_scalars");
-  if (p->m_local > 0) {
+  p->timer.end(1, st);
+  p->timer.begin(st);
+  if (p->m_local > 0 && (size_t)p->ch.np * 16 + 8 * (size_t)(p->ch.np + 2) * 8 <= 200 * 1024) {
+    const int rc = cp_dots_rows(p, st);
+    if (rc) return rc;
+    cp_dots_reduce<<<1, 32, 0, st>>>(p->dots_part, p->row_blocks, dots, p->dev);
+    MLR_LAUNCH_CHECK("cp_dots_reduce");
+  } else if (p->m_local > 0) {
     const int blocks = p->row_blocks;
     if (p->f32)
       cp_dots_kernel<float><<<blocks, 256, 0, st>>>(p->dev, p->ch, p->m_local, p->row0, p->mask_dev, p->ldm_dev,
@@ -682,21 +695,29 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   } else {
     MLR_CUDA(cudaMemsetAsync(dots, 0, 3 * sizeof(double), st));
   }
+  p->timer.end(2, st);
   return kOk;
 }
 
 int cpcp_update(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
                 const double* dots, cudaStream_t st) {
+  p->timer.begin(st);
   cp_qp_kernel<<<1, 1, 0, st>>>(p->dev, dots);
   MLR_LAUNCH_CHECK("cp_qp_kernel");
-  return p->f32 ? cp_row<float, kCpUpdate>(p, D, ldd, mask, ldm, S, lds, nullptr, 0, st)
-                : cp_row<double, kCpUpdate>(p, D, ldd, mask, ldm, S, lds, nullptr, 0, st);
+  p->timer.end(3, st);
+  p->timer.begin(st);
+  int rc = p->f32 ? cp_row<float, kCpUpdate>(p, D, ldd, mask, ldm, S, lds, nullptr, 0, st)
+                  : cp_row<double, kCpUpdate>(p, D, ldd, mask, ldm, S, lds, nullptr, 0, st);
+  p->timer.end(5, st);
+  return rc;
 }
 
 int cpcp_finalize(CpcpPlan* p, const double* red, cudaStream_t st) {
   const int64_t nn = (int64_t)p->ch.np * p->ch.np;
+  p->timer.begin(st);
   cp_finalize_kernel<<<1, 1, 0, st>>>(p->dev, red + nn, p->hist, p->obj);
   MLR_LAUNCH_CHECK("cp_finalize_kernel");
+  p->timer.end(6, st);
   return kOk;
 }
 

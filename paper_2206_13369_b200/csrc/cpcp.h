@@ -24,6 +24,7 @@ struct CpcpDev {
 };
 
 struct CpcpPlan {
+  PhaseTimer timer;  // phases: gram, power, dots, qp, -, update, finalize
   ChainDev ch;
   bool f32;
   int64_t m_local, m_global, row0;

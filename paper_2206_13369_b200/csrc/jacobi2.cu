@@ -40,6 +40,7 @@ struct J2Smem {
   double Y[J2_PW][J2_LD];
   double Q2[J2_PW][J2_LD];
   double cs[J2_PW / 2][3];  // c, s, t
+  double2 csl[J2_PW][J2_PW / 2];  // rotation log of the inner rounds, replayed into Q
   int pr[J2_PW / 2][2];
   int rotated;
   int active;             // any pair of this block above tolerance
@@ -261,7 +262,6 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         const int pa = srow[k] & 0xffff, pb = srow[k] >> 16;
         __syncthreads();
         load_pair_tile(S.G, B, np, pa, pb, pa, pb);
-        for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) S.Q[e >> 5][e & 31] = (e >> 5) == (e & 31) ? 1.0 : 0.0;
         if (tid == 0) {
           S.rotated = 0;
           S.active = 0;
@@ -315,13 +315,14 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
               S.round_rot[rnd] = 1;
             }
             cs2[tid] = make_double2(c, s);
+            S.csl[rnd][tid] = make_double2(c, s);
             tt[tid] = t;
           }
           __syncthreads();
           if (!S.round_rot[rnd]) continue;  // identity round: nothing to apply
           {
-            // thread (pp, q) owns rows {p1,p2} x cols {q1,q2} of both
-            // G <- J^T G J (two-sided) and Q <- Q J (columns only)
+            // thread (pp, q) owns rows {p1,p2} x cols {q1,q2} of G <- J^T G J;
+            // Q is rebuilt from the rotation log after the rounds
             const int pp = tid >> 4, q = tid & 15;
             int p1, p2, q1, q2;
             pair_of(pp, rnd, p1, p2);
@@ -329,7 +330,6 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             const double2 csp = cs2[pp], csq = cs2[q];
             const double cp = csp.x, sp = csp.y, cq = csq.x, sq = csq.y;
             const double g11 = S.G[p1][q1], g12 = S.G[p1][q2], g21 = S.G[p2][q1], g22 = S.G[p2][q2];
-            const double x11 = S.Q[p1][q1], x12 = S.Q[p1][q2], x21 = S.Q[p2][q1], x22 = S.Q[p2][q2];
             if (pp == q && tt[pp] != 0.0) {
               // the rotated pair itself: exact zero + classical diagonal update
               const double t = tt[pp];
@@ -345,13 +345,31 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
               S.G[p2][q1] = sp * t11 + cp * t21;
               S.G[p2][q2] = sp * t12 + cp * t22;
             }
-            S.Q[p1][q1] = cq * x11 - sq * x12;
-            S.Q[p1][q2] = sq * x11 + cq * x12;
-            S.Q[p2][q1] = cq * x21 - sq * x22;
-            S.Q[p2][q2] = sq * x21 + cq * x22;
           }
           __syncthreads();
         }
+        // Q = J_0 J_1 ... : row r of Q evolves independently, so the 8 lanes
+        // owning a row (same warp) replay the log with only __syncwarp
+        {
+          const int r = tid >> 3, sub = tid & 7;
+          for (int e = sub; e < J2_PW; e += 8) S.Q[r][e] = (r == e) ? 1.0 : 0.0;
+          __syncwarp();
+          for (int rnd = 0; rnd < rounds; ++rnd) {
+            if (!S.round_rot[rnd]) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int kk = sub + 8 * h;
+              int i, j;
+              pair_of(kk, rnd, i, j);
+              const double2 c2 = S.csl[rnd][kk];
+              const double a = S.Q[r][i], b = S.Q[r][j];
+              S.Q[r][i] = c2.x * a - c2.y * b;
+              S.Q[r][j] = c2.y * a + c2.x * b;
+            }
+            __syncwarp();
+          }
+        }
+        __syncthreads();
         j2_mark(1, t0);
         // publish Q_k; the rotated diagonal block goes straight back into B
         double* qo = Qbuf + (int64_t)k * J2_PW * J2_PW;
@@ -429,9 +447,15 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         double o[4];
         if (x.r0 >= 0) {
           tile_mm<false>(S.X, QA, o);  // V rows * Q_k
-          if (x.r0 + rr < nrows_v)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) V[(int64_t)(x.r0 + rr) * np + j2_col(tm_col(u), a1, b1)] = o[u];
+          for (int u = 0; u < 4; ++u) S.Y[rr][tm_col(u)] = o[u];
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // coalesced 128-byte row segments
+            const int e = tid + u * J2_THREADS;
+            const int i = e >> 5, j = e & 31;
+            if (x.r0 + i < nrows_v) V[(int64_t)(x.r0 + i) * np + j2_col(j, a1, b1)] = S.Y[i][j];
+          }
         } else {
           // identity rotations were not cached: substitute I on the fly
           if (!qf_all[x.kB]) {
@@ -449,11 +473,20 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
           } else {
             tile_mm<true>(QA, S.Y, o);  // Q_k1^T Y
           }
+          // stage the tile and its transpose, then write both orientations
+          // with coalesced row segments
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int gi = j2_col(rr, a1, b1), gj = j2_col(tm_col(u), a2, b2);
-            B[(int64_t)gi * np + gj] = o[u];
-            B[(int64_t)gj * np + gi] = o[u];
+            S.X[rr][tm_col(u)] = o[u];
+            S.Q2[tm_col(u)][rr] = o[u];
+          }
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = tid + u * J2_THREADS;
+            const int i = e >> 5, j = e & 31;
+            B[(int64_t)j2_col(i, a1, b1) * np + j2_col(j, a2, b2)] = S.X[i][j];
+            B[(int64_t)j2_col(i, a2, b2) * np + j2_col(j, a1, b1)] = S.Q2[i][j];
           }
         }
 #pragma unroll

@@ -4,6 +4,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <utility>
+#include <vector>
 #include <string>
 #include <type_traits>
 
@@ -42,6 +44,7 @@ struct ChainDev {
   double* gd;           // pivots d[k]
   double* gi;           // dense G_R^{-1}, np x np (zero padded)
   int max_span;         // max hi-lo
+  int keys_dense;       // c0 starts at 0, steps by <= 1 and reaches nh-2 (segmented restriction valid)
 };
 
 int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out, int trans_in,
@@ -52,5 +55,63 @@ int64_t jacobi2_qbuf_elems(int np);
 int jacobi2_debug_prof(unsigned long long* out8);
 int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
                 void* Qbuf, int* qflag, double* off_slots, int* result, const int* skip, cudaStream_t st);
+
+// Optional per-phase CUDA-event timing (enabled by mlr_pcp_set_timing):
+// every launch of a phase is bracketed by an event pair on its stream.
+enum PcpPhase { kPhGram = 0, kPhPre, kPhJacobi, kPhPost, kPhRecon, kPhUpdate, kPhFinalize, kPhCount };
+
+struct PhaseTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhCount];
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t open = nullptr;
+  cudaEvent_t take() {
+    cudaEvent_t e;
+    if (!pool.empty()) {
+      e = pool.back();
+      pool.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
+  }
+  void begin(cudaStream_t st) {
+    if (!on) return;
+    open = take();
+    cudaEventRecord(open, st);
+  }
+  void end(int phase, cudaStream_t st) {
+    if (!on || !open) return;
+    cudaEvent_t e = take();
+    cudaEventRecord(e, st);
+    ev[phase].push_back({open, e});
+    open = nullptr;
+  }
+  // total ms and launch count per phase; recycles the events
+  void collect(double* ms, int* cnt) {
+    for (int ph = 0; ph < kPhCount; ++ph) {
+      double s = 0.0;
+      for (auto& pr : ev[ph]) {
+        float t = 0.f;
+        cudaEventSynchronize(pr.second);
+        cudaEventElapsedTime(&t, pr.first, pr.second);
+        s += t;
+        pool.push_back(pr.first);
+        pool.push_back(pr.second);
+      }
+      ms[ph] = s;
+      cnt[ph] = (int)ev[ph].size();
+      ev[ph].clear();
+    }
+  }
+  ~PhaseTimer() {
+    for (auto& v : ev)
+      for (auto& pr : v) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
 
 }  // namespace mlr

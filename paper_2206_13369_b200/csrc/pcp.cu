@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "pcp.h"
+#include "rows.h"
 
 namespace mlr {
 
@@ -444,13 +445,15 @@ template <typename T>
 static int row_pass(int mode, PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy,
                     void* Lout, void* Sout, int64_t ldo, cudaStream_t st) {
   const int threads = 256;
+  if (p->m_local == 0) return kOk;
+  if (rows_warp_ok(p->ch, p->f32))  // streaming warp-per-row path (rows.cu)
+    return pcp_rows(p, mode, D, ldd, Yin, Yout, ldy, Lout, Sout, ldo, st);
   size_t smem = sizeof(T) * (size_t)(p->ch.np + p->ch.n + 4);
   if (smem > 200 * 1024) {
     set_error("pcp row kernel: fine row does not fit in shared memory");
     return kErrArg;
   }
   int blocks = p->row_blocks;
-  if (p->m_local == 0) return kOk;
   const T* Dp = (const T*)D;
 #define MLR_ROW(MODE)                                                                               \
   {                                                                                                 \
@@ -647,8 +650,8 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
 
 int pcp_update(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy, cudaStream_t st) {
   p->timer.begin(st);
-  int rc = p->f32 ? row_pass<float>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st)
-                  : row_pass<double>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st);
+  const int rc = p->f32 ? row_pass<float>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st)
+                : row_pass<double>(kUpdate, p, D, ldd, Yin, Yout, ldy, nullptr, nullptr, 0, st);
   p->timer.end(kPhUpdate, st);
   return rc;
 }

@@ -36,64 +36,6 @@ struct LanczosDev {
   double beta[512];
 };
 
-// Optional per-phase CUDA-event timing (enabled by mlr_pcp_set_timing):
-// every launch of a phase is bracketed by an event pair on its stream.
-enum PcpPhase { kPhGram = 0, kPhPre, kPhJacobi, kPhPost, kPhRecon, kPhUpdate, kPhFinalize, kPhCount };
-
-struct PhaseTimer {
-  bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhCount];
-  std::vector<cudaEvent_t> pool;
-  cudaEvent_t open = nullptr;
-  cudaEvent_t take() {
-    cudaEvent_t e;
-    if (!pool.empty()) {
-      e = pool.back();
-      pool.pop_back();
-    } else {
-      cudaEventCreate(&e);
-    }
-    return e;
-  }
-  void begin(cudaStream_t st) {
-    if (!on) return;
-    open = take();
-    cudaEventRecord(open, st);
-  }
-  void end(int phase, cudaStream_t st) {
-    if (!on || !open) return;
-    cudaEvent_t e = take();
-    cudaEventRecord(e, st);
-    ev[phase].push_back({open, e});
-    open = nullptr;
-  }
-  // total ms and launch count per phase; recycles the events
-  void collect(double* ms, int* cnt) {
-    for (int ph = 0; ph < kPhCount; ++ph) {
-      double s = 0.0;
-      for (auto& pr : ev[ph]) {
-        float t = 0.f;
-        cudaEventSynchronize(pr.second);
-        cudaEventElapsedTime(&t, pr.first, pr.second);
-        s += t;
-        pool.push_back(pr.first);
-        pool.push_back(pr.second);
-      }
-      ms[ph] = s;
-      cnt[ph] = (int)ev[ph].size();
-      ev[ph].clear();
-    }
-  }
-  ~PhaseTimer() {
-    for (auto& v : ev)
-      for (auto& pr : v) {
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
-      }
-    for (auto e : pool) cudaEventDestroy(e);
-  }
-};
-
 struct PcpPlan {
   PhaseTimer timer;
   ChainDev ch;

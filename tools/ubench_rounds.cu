@@ -126,6 +126,46 @@ __global__ void rounds1_kernel(const double* Gin, int nrounds, long long* cycles
   if (tid == 0) sink[blockIdx.x] = G[cur][3][5] + Q[cur][7][9];
 }
 
+// Barrier-only and FP32-data variants of the 2-sync round (cost attribution).
+template <typename TT, int WORK>
+__global__ void rounds2_kernel(const double* Gin, int nrounds, long long* cycles, double* sink) {
+  __shared__ TT G[PW][LD], Q[PW][LD];
+  __shared__ TT cs[16][2];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < PW * PW; e += T) {
+    G[e >> 5][e & 31] = (TT)Gin[e];
+    Q[e >> 5][e & 31] = (e >> 5) == (e & 31);
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int rnd = 0; rnd < nrounds; ++rnd) {
+    if (WORK && tid < 16) {
+      const int i = tid, j = BW + ((tid + rnd) & 15);
+      const TT a = G[i][i], b = G[j][j], g = G[i][j];
+      cs[tid][0] = a * (TT)0.999 + g * (TT)1e-3;
+      cs[tid][1] = b * (TT)1e-3;
+    }
+    __syncthreads();
+    if (WORK) {
+      const int p = tid >> 4, q = tid & 15;
+      const int p1 = p, p2 = BW + ((p + rnd) & 15), q1 = q, q2 = BW + ((q + rnd) & 15);
+      const TT cp = cs[p][0], sp = cs[p][1], cq = cs[q][0], sq = cs[q][1];
+      const TT g11 = G[p1][q1], g12 = G[p1][q2], g21 = G[p2][q1], g22 = G[p2][q2];
+      const TT x11 = Q[p1][q1], x12 = Q[p1][q2], x21 = Q[p2][q1], x22 = Q[p2][q2];
+      const TT t11 = cq * g11 - sq * g12, t12 = sq * g11 + cq * g12;
+      const TT t21 = cq * g21 - sq * g22, t22 = sq * g21 + cq * g22;
+      G[p1][q1] = cp * t11 - sp * t21; G[p1][q2] = cp * t12 - sp * t22;
+      G[p2][q1] = sp * t11 + cp * t21; G[p2][q2] = sp * t12 + cp * t22;
+      Q[p1][q1] = cq * x11 - sq * x12; Q[p1][q2] = sq * x11 + cq * x12;
+      Q[p2][q1] = cq * x21 - sq * x22; Q[p2][q2] = sq * x21 + cq * x22;
+    }
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (tid == 0) cycles[blockIdx.x] = t1 - t0;
+  if (tid == 0) sink[blockIdx.x] = (double)(G[3][5] + Q[7][9]);
+}
+
 int main() {
   double hG[PW * PW];
   for (int i = 0; i < PW; ++i)
@@ -157,6 +197,15 @@ int main() {
     rounds1_kernel<2><<<1, T>>>(dG, n, cyc, sink);
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("1-sync nomath : %.1f cycles/round\n", (double)h / n);
+    rounds2_kernel<double, 0><<<1, T>>>(dG, n, cyc, sink);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("2 barriers only: %.1f cycles/round\n", (double)h / n);
+    rounds2_kernel<double, 1><<<1, T>>>(dG, n, cyc, sink);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("2-sync fp64 data, trivial params: %.1f cycles/round\n", (double)h / n);
+    rounds2_kernel<float, 1><<<1, T>>>(dG, n, cyc, sink);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("2-sync fp32 data, trivial params: %.1f cycles/round\n", (double)h / n);
   }
   printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
