@@ -108,9 +108,9 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.sig = c.take<double>(8 * np);
   p.fw = c.take<double>(8 * np);
   p.qbuf = c.take<double>(8 * (size_t)jacobi2_qbuf_elems(np));
-  p.qflag = c.take<int>(4 * (size_t)(np / 32 + 1));
-  p.jac_off = c.take<double>(8 * 2);
-  p.jac_result = c.take<int>(4 * 4);
+  p.qflag = c.take<int>(4 * (size_t)jacobi2_qflag_elems(np));
+  p.jac_off = c.take<double>(8 * 4);
+  p.jac_result = c.take<int>(4 * 16);
   p.lzQ = c.take<double>(8 * (size_t)n * (p.lz_kmax + 1));
   p.lzT = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
   p.lzW = c.take<double>(8 * (size_t)n * p.lz_splits);
@@ -336,7 +336,9 @@ int mlr_matrix_stats(int64_t m, int n, int f32, const void* D, int64_t ldd, doub
   return matrix_stats(m, n, f32 != 0, D, ldd, work, blocks, out3, (cudaStream_t)stream);
 }
 
-int64_t mlr_eigh_work_doubles(int np) { return (int64_t)np * np + jacobi2_qbuf_elems(np) + np + 64; }
+int64_t mlr_eigh_work_doubles(int np) {
+  return (int64_t)np * np + jacobi2_qbuf_elems(np) + jacobi2_qflag_elems(np) / 2 + 64;
+}
 
 int mlr_eigh_psd(int np, const double* B, double* V, double* lam, double tol, int max_sweeps, double* work,
                  int* info, void* stream) {
@@ -346,7 +348,7 @@ int mlr_eigh_psd(int np, const double* B, double* V, double* lam, double tol, in
   double* qbuf = X + (int64_t)np * np;
   double* off = qbuf + jacobi2_qbuf_elems(np);
   int* res = (int*)(off + 4);
-  int* qflag = res + 4;
+  int* qflag = res + 16;
   MLR_CUDA(cudaMemcpyAsync(X, B, sizeof(double) * np * np, cudaMemcpyDeviceToDevice, st));
   eye_kernel<<<256, 256, 0, st>>>(V, np);
   MLR_LAUNCH_CHECK("eye_kernel");

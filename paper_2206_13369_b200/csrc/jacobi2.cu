@@ -39,6 +39,9 @@ struct J2Smem {
   double X[J2_PW][J2_LD];
   double Y[J2_PW][J2_LD];
   double Q2[J2_PW][J2_LD];
+  double G2[J2_PW][J2_LD];       // ping-pong partner of G in the pipelined rounds
+  double2 csb[2][J2_PW / 2];     // (c, s) of rounds rnd, rnd + 1
+  double ttb[2][J2_PW / 2];      // t of rounds rnd, rnd + 1
   double cs[J2_PW / 2][3];  // c, s, t
   double2 csl[J2_PW][J2_PW / 2];  // rotation log of the inner rounds, replayed into Q
   int pr[J2_PW / 2][2];
@@ -63,6 +66,22 @@ __device__ __forceinline__ void jac_rot(double a, double b, double g, double& c,
   c = rsqrt(fma(t, t, 1.0));
   s = c * t;
 }
+
+// One 2x2 block of G <- J^T G J: rows {p1, p2} rotated by (cp, sp), columns
+// {q1, q2} by (cq, sq).  Explicit FMAs: the pipelined rounds recompute some
+// of these entries in the rotation warp and must match bit for bit.
+struct Blk {
+  double o11, o12, o21, o22;
+};
+__device__ __forceinline__ Blk j2_block(double cp, double sp, double cq, double sq, double g11, double g12,
+                                        double g21, double g22) {
+  const double t11 = fma(cq, g11, -sq * g12), t12 = fma(sq, g11, cq * g12);
+  const double t21 = fma(cq, g21, -sq * g22), t22 = fma(sq, g21, cq * g22);
+  return Blk{fma(cp, t11, -sp * t21), fma(cp, t12, -sp * t22), fma(sp, t11, cp * t21), fma(sp, t12, cp * t22)};
+}
+// classical diagonal update of the rotated pair itself
+__device__ __forceinline__ double j2_diag_lo(double t, double g, double a) { return fma(-t, g, a); }
+__device__ __forceinline__ double j2_diag_hi(double t, double g, double b) { return fma(t, g, b); }
 
 __device__ __forceinline__ void j2_pair(int step, int k, int nb, int& pa, int& pb) {
   if (step == 0) {
@@ -154,7 +173,7 @@ __device__ __forceinline__ void tile_mm(const double (*A)[J2_LD], const double (
 
 // Cycle breakdown of CTA 0 (phase A load+measure, inner rounds, barrier 1,
 // phase B, barrier 2, steps) — read with mlr_debug_j2prof.
-__device__ unsigned long long g_j2prof[8];
+__device__ unsigned long long g_j2prof[16];
 
 __device__ __forceinline__ void j2_mark(int slot, long long& t0) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -175,10 +194,11 @@ struct J2Item {
 template <bool CLUSTER>
 __global__ void __launch_bounds__(J2_THREADS)
 jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows_v, double tol,
-               double abs_floor_rel, int max_sweeps, double* __restrict__ Qbuf, double* __restrict__ Gbuf,
-               int* __restrict__ qflag, double* __restrict__ off_slots, int* __restrict__ result,
-               const int* __restrict__ skip, int cache_q, double early_off) {
+               double abs_floor_rel, int max_sweeps, double* __restrict__ Qlog, int cap,
+               int* __restrict__ qflag_log, double* __restrict__ off_slots, int* __restrict__ result,
+               const int* __restrict__ skip, int cache_q, double early_off, int vlog) {
   if (skip && *skip) return;
+  if (result[7] != 0) return;  // converged or out of sweeps in an earlier launch
   extern __shared__ __align__(16) unsigned char smem_raw[];
   J2Smem& S = *reinterpret_cast<J2Smem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -188,7 +208,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   const int me = CLUSTER ? (int)cg::this_cluster().block_rank() : (int)blockIdx.x;
   const int nbitems = npairs * (npairs - 1) / 2;  // off-diagonal pair blocks k1 < k2
   const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
-  const int nitems = nbitems + npairs * vchunks;
+  const int nitems = nbitems + (vlog ? 0 : npairs * vchunks);  // V items only without the log
   const int my_items = (nitems - me + nctas - 1) / nctas;
   // dynamic smem: [J2Smem][Qcache npairs x 32 x LD (optional)][sched nb*npairs int][items][qslot npairs int]
   unsigned char* p = smem_raw + ((sizeof(J2Smem) + 127) & ~size_t(127));
@@ -248,12 +268,19 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   if (tid == 0)
     for (int w = 1; w < J2_THREADS / 32; ++w) S.red[0] = fmax(S.red[0], S.red[w]);
   __syncthreads();
-  const double abs_floor = abs_floor_rel * S.red[0];
-
-  int sweep = 0;
+  // resume state (result[4..6]): sweep, next global step, first step not yet applied to V
+  int sweep = result[4];
+  int g = result[5];
+  const int g_applied = result[6];
+  const int g_start = g;
+  const double abs_floor = g_start == 0 ? abs_floor_rel * S.red[0] : off_slots[2];
   bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
-    for (int step = 0; step < nb; ++step) {
+    if (vlog && g + nb > g_applied + cap) break;  // rotation log full: pause, V catches up, resume
+    for (int step = 0; step < nb; ++step, ++g) {
+      const int slot = g % cap;
+      double* Qbuf = Qlog + (int64_t)slot * npairs * J2_PW * J2_PW;
+      int* qflag = qflag_log + slot * npairs;
       long long t0 = clock64();
       if (blockIdx.x == 0 && tid == 0) atomicAdd(&g_j2prof[5], 1ull);
       const int* srow = sched + step * npairs;
@@ -263,10 +290,8 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         __syncthreads();
         load_pair_tile(S.G, B, np, pa, pb, pa, pb);
         if (tid == 0) {
-          S.rotated = 0;
           S.active = 0;
         }
-        if (tid < J2_PW) S.round_rot[tid] = 0;
         __syncthreads();
         if (step == 0 && k == 0 && tid == 0) off_slots[(sweep + 1) & 1] = 0.0;
         {
@@ -303,83 +328,222 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         };
         double2* cs2 = reinterpret_cast<double2*>(&S.cs[0][0]);  // (c, s) per pair
         double* tt = &S.cs[0][0] + J2_PW;                         // t per pair
-        for (int rnd = 0; rnd < rounds; ++rnd) {
-          if (tid < J2_PW / 2) {
-            int i, j;
-            pair_of(tid, rnd, i, j);
-            const double a = S.G[i][i], b = S.G[j][j], g = S.G[i][j];
-            double c = 1.0, s = 0.0, t = 0.0;
-            if (fabs(g) > abs_floor && g * g > tol2 * fabs(a * b)) {
-              jac_rot(a, b, g, c, s, t);
-              S.rotated = 1;
-              S.round_rot[rnd] = 1;
+        unsigned rmask = 0;  // inner rounds that rotated (uniform: from __syncthreads_or)
+        double(*Gfin)[J2_LD] = S.G;  // where the rotated tile ends up
+        auto needs_rot = [&](double a, double b, double g) {
+          return fabs(g) > abs_floor && g * g > tol2 * fabs(a * b);
+        };
+        if (step == 0) {
+          // circle-method rounds: rotations, barrier, update, barrier
+          for (int rnd = 0; rnd < rounds; ++rnd) {
+            int rot_here = 0;
+            if (tid < J2_PW / 2) {
+              int i, j;
+              pair_of(tid, rnd, i, j);
+              const double a = S.G[i][i], b = S.G[j][j], g = S.G[i][j];
+              double c = 1.0, s = 0.0, t = 0.0;
+              if (needs_rot(a, b, g)) {
+                jac_rot(a, b, g, c, s, t);
+                rot_here = 1;
+              }
+              cs2[tid] = make_double2(c, s);
+              S.csl[rnd][tid] = make_double2(c, s);
+              tt[tid] = t;
             }
-            cs2[tid] = make_double2(c, s);
-            S.csl[rnd][tid] = make_double2(c, s);
-            tt[tid] = t;
-          }
-          __syncthreads();
-          if (!S.round_rot[rnd]) continue;  // identity round: nothing to apply
-          {
-            // thread (pp, q) owns rows {p1,p2} x cols {q1,q2} of G <- J^T G J;
-            // Q is rebuilt from the rotation log after the rounds
-            const int pp = tid >> 4, q = tid & 15;
-            int p1, p2, q1, q2;
-            pair_of(pp, rnd, p1, p2);
-            pair_of(q, rnd, q1, q2);
-            const double2 csp = cs2[pp], csq = cs2[q];
-            const double cp = csp.x, sp = csp.y, cq = csq.x, sq = csq.y;
-            const double g11 = S.G[p1][q1], g12 = S.G[p1][q2], g21 = S.G[p2][q1], g22 = S.G[p2][q2];
-            if (pp == q && tt[pp] != 0.0) {
-              // the rotated pair itself: exact zero + classical diagonal update
-              const double t = tt[pp];
-              S.G[p1][p1] = g11 - t * g12;
-              S.G[p2][p2] = g22 + t * g12;
-              S.G[p1][p2] = 0.0;
-              S.G[p2][p1] = 0.0;
-            } else {
-              const double t11 = cq * g11 - sq * g12, t12 = sq * g11 + cq * g12;
-              const double t21 = cq * g21 - sq * g22, t22 = sq * g21 + cq * g22;
-              S.G[p1][q1] = cp * t11 - sp * t21;
-              S.G[p1][q2] = cp * t12 - sp * t22;
-              S.G[p2][q1] = sp * t11 + cp * t21;
-              S.G[p2][q2] = sp * t12 + cp * t22;
+            if (!__syncthreads_or(rot_here)) continue;  // identity round: nothing to apply
+            rmask |= 1u << rnd;
+            {
+              // thread (pp, q) owns rows {p1,p2} x cols {q1,q2} of G <- J^T G J
+              const int pp = tid >> 4, q = tid & 15;
+              int p1, p2, q1, q2;
+              pair_of(pp, rnd, p1, p2);
+              pair_of(q, rnd, q1, q2);
+              const double2 csp = cs2[pp], csq = cs2[q];
+              const double g11 = S.G[p1][q1], g12 = S.G[p1][q2], g21 = S.G[p2][q1], g22 = S.G[p2][q2];
+              if (pp == q && tt[pp] != 0.0) {
+                // the rotated pair itself: exact zero + classical diagonal update
+                const double t = tt[pp];
+                S.G[p1][p1] = j2_diag_lo(t, g12, g11);
+                S.G[p2][p2] = j2_diag_hi(t, g12, g22);
+                S.G[p1][p2] = 0.0;
+                S.G[p2][p1] = 0.0;
+              } else {
+                const Blk o = j2_block(csp.x, csp.y, csq.x, csq.y, g11, g12, g21, g22);
+                S.G[p1][q1] = o.o11;
+                S.G[p1][q2] = o.o12;
+                S.G[p2][q1] = o.o21;
+                S.G[p2][q2] = o.o22;
+              }
             }
+            __syncthreads();
           }
-          __syncthreads();
+        } else if (rounds > 0) {
+          // Cross rounds, pipelined: pair i = (i, 16 + (i + rnd) % 16).  Warp
+          // 0 (lanes 0..15, one pair each) computes the rotations of round
+          // rnd + 1 while warps 1..7 apply round rnd from Gin into Gout: the
+          // entries round rnd + 1 needs after round rnd are its own diagonal
+          // update, that of pair i + 1 (whose second index j' becomes i's
+          // partner) and the (i, j') element of block (pair i, pair i + 1),
+          // all recomputed with the update's exact FMAs.  One barrier per round.
+          double(*Gin)[J2_LD] = S.G;
+          double(*Gout)[J2_LD] = S.G2;
+          const int lane = tid & 31;
+          double ra = 0.0, rb = 0.0, rg = 0.0, rc = 1.0, rs = 0.0, rt = 0.0;  // rotation warp: round rnd
+          int rot_here = 0;
+          if (tid < J2_BW) {
+            const int i = tid, j = J2_BW + i;
+            ra = Gin[i][i];
+            rb = Gin[j][j];
+            rg = Gin[i][j];
+            if (needs_rot(ra, rb, rg)) {
+              jac_rot(ra, rb, rg, rc, rs, rt);
+              rot_here = 1;
+            }
+            S.csb[0][i] = make_double2(rc, rs);
+            S.ttb[0][i] = rt;
+            S.csl[0][i] = make_double2(rc, rs);
+          }
+          int any = __syncthreads_or(rot_here);
+          for (int rnd = 0; rnd < rounds; ++rnd) {
+            const int par = rnd & 1;
+            if (any) rmask |= 1u << rnd;
+            int rot_next = 0;
+            if (tid < 32) {
+              // ---- rotation warp: round rnd + 1
+              const int i = lane & (J2_BW - 1);
+              const int i1 = (i + 1) & (J2_BW - 1);
+              const int src = (lane & 16) | i1;
+              const double qc = __shfl_sync(0xffffffffu, rc, src), qs = __shfl_sync(0xffffffffu, rs, src);
+              const double qt = __shfl_sync(0xffffffffu, rt, src), qb = __shfl_sync(0xffffffffu, rb, src);
+              const double qg = __shfl_sync(0xffffffffu, rg, src);
+              if (lane < J2_BW && rnd + 1 < rounds) {
+                const int j = J2_BW + ((i + rnd) & (J2_BW - 1));       // partner in round rnd
+                const int jn = J2_BW + ((i + rnd + 1) & (J2_BW - 1));  // partner in round rnd + 1
+                double a2, b2, g2;
+                if (any) {
+                  a2 = rt != 0.0 ? j2_diag_lo(rt, rg, ra) : ra;
+                  b2 = qt != 0.0 ? j2_diag_hi(qt, qg, qb) : qb;
+                  const Blk o = j2_block(rc, rs, qc, qs, Gin[i][i1], Gin[i][jn], Gin[j][i1], Gin[j][jn]);
+                  g2 = o.o12;
+                } else {
+                  a2 = ra;
+                  b2 = qb;
+                  g2 = Gin[i][jn];
+                }
+                ra = a2;
+                rb = b2;
+                rg = g2;
+                rc = 1.0;
+                rs = 0.0;
+                rt = 0.0;
+                if (needs_rot(ra, rb, rg)) {
+                  jac_rot(ra, rb, rg, rc, rs, rt);
+                  rot_next = 1;
+                }
+                S.csb[par ^ 1][i] = make_double2(rc, rs);
+                S.ttb[par ^ 1][i] = rt;
+                S.csl[rnd + 1][i] = make_double2(rc, rs);
+              }
+            } else if (any) {
+              // ---- update warps: the 256 2x2 blocks of round rnd, Gin -> Gout
+              for (int bi = tid - 32; bi < J2_BW * J2_BW; bi += J2_THREADS - 32) {
+                const int pp = bi >> 4, q = bi & 15;
+                const int p1 = pp, p2 = J2_BW + ((pp + rnd) & (J2_BW - 1));
+                const int q1 = q, q2 = J2_BW + ((q + rnd) & (J2_BW - 1));
+                const double2 csp = S.csb[par][pp], csq = S.csb[par][q];
+                const double g11 = Gin[p1][q1], g12 = Gin[p1][q2], g21 = Gin[p2][q1], g22 = Gin[p2][q2];
+                const double tp = S.ttb[par][pp];
+                if (pp == q && tp != 0.0) {
+                  Gout[p1][p1] = j2_diag_lo(tp, g12, g11);
+                  Gout[p2][p2] = j2_diag_hi(tp, g12, g22);
+                  Gout[p1][p2] = 0.0;
+                  Gout[p2][p1] = 0.0;
+                } else {
+                  const Blk o = j2_block(csp.x, csp.y, csq.x, csq.y, g11, g12, g21, g22);
+                  Gout[p1][q1] = o.o11;
+                  Gout[p1][q2] = o.o12;
+                  Gout[p2][q1] = o.o21;
+                  Gout[p2][q2] = o.o22;
+                }
+              }
+            }
+            const int any_next = __syncthreads_or(rot_next);
+            if (any) {
+              double(*tmp)[J2_LD] = Gin;
+              Gin = Gout;
+              Gout = tmp;
+            }
+            any = any_next;
+          }
+          Gfin = Gin;
         }
-        // Q = J_0 J_1 ... : row r of Q evolves independently, so the 8 lanes
-        // owning a row (same warp) replay the log with only __syncwarp
+        j2_mark(7, t0);
+        // Q = J_0 J_1 ... : row r of Q evolves independently; 8 lanes own a
+        // row, two pairs (kk = sub, sub + 8) each, and replay the log
+        double* qo = Qbuf + (int64_t)k * J2_PW * J2_PW;
+        const bool rot = rmask != 0;
         {
           const int r = tid >> 3, sub = tid & 7;
-          for (int e = sub; e < J2_PW; e += 8) S.Q[r][e] = (r == e) ? 1.0 : 0.0;
-          __syncwarp();
-          for (int rnd = 0; rnd < rounds; ++rnd) {
-            if (!S.round_rot[rnd]) continue;
+          if (step == 0) {  // circle-method pairs: replay in shared memory
+            for (int e = sub; e < J2_PW; e += 8) S.Q[r][e] = (r == e) ? 1.0 : 0.0;
+            __syncwarp();
+            for (int rnd = 0; rnd < rounds; ++rnd) {
+              if (!((rmask >> rnd) & 1u)) continue;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int kk = sub + 8 * h;
+                int i, j;
+                pair_of(kk, rnd, i, j);
+                const double2 c2 = S.csl[rnd][kk];
+                const double a = S.Q[r][i], b = S.Q[r][j];
+                S.Q[r][i] = c2.x * a - c2.y * b;
+                S.Q[r][j] = c2.y * a + c2.x * b;
+              }
+              __syncwarp();
+            }
+            for (int e = sub; e < J2_PW; e += 8) qo[r * J2_PW + e] = S.Q[r][e];
+          } else {
+            // cross pairs (kk, 16 + (kk + rnd) % 16): x = Q[r][kk] stays put,
+            // y = Q[r][partner] moves to pair kk - 1 after every round, a
+            // shuffle within the row's 8 lanes; everything in registers
+            double x[2], y[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              x[h] = r == sub + 8 * h ? 1.0 : 0.0;
+              y[h] = r == J2_BW + sub + 8 * h ? 1.0 : 0.0;
+            }
+            const int src = (tid & 31 & ~7) | ((sub + 1) & 7);
+            for (int rnd = 0; rnd < rounds; ++rnd) {
+              if ((rmask >> rnd) & 1u) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const double2 c2 = S.csl[rnd][sub + 8 * h];
+                  const double a = x[h], b = y[h];
+                  x[h] = c2.x * a - c2.y * b;
+                  y[h] = c2.y * a + c2.x * b;
+                }
+              }
+              const double v0 = __shfl_sync(0xffffffffu, y[0], src);
+              const double v1 = __shfl_sync(0xffffffffu, y[1], src);
+              y[0] = sub < 7 ? v0 : v1;
+              y[1] = sub < 7 ? v1 : v0;
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int kk = sub + 8 * h;
-              int i, j;
-              pair_of(kk, rnd, i, j);
-              const double2 c2 = S.csl[rnd][kk];
-              const double a = S.Q[r][i], b = S.Q[r][j];
-              S.Q[r][i] = c2.x * a - c2.y * b;
-              S.Q[r][j] = c2.y * a + c2.x * b;
+              qo[r * J2_PW + kk] = x[h];
+              qo[r * J2_PW + J2_BW + ((kk + rounds) & (J2_BW - 1))] = y[h];
             }
-            __syncwarp();
           }
         }
-        __syncthreads();
         j2_mark(1, t0);
-        // publish Q_k; the rotated diagonal block goes straight back into B
-        double* qo = Qbuf + (int64_t)k * J2_PW * J2_PW;
-        const bool rot = S.rotated != 0;
-        for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) {
-          const int i = e >> 5, j = e & 31;
-          qo[e] = S.Q[i][j];
-          if (rot) B[(int64_t)j2_col(i, pa, pb) * np + j2_col(j, pa, pb)] = S.G[i][j];
-        }
-        if (tid == 0) qflag[k] = S.rotated;
+        // the rotated diagonal block goes straight back into B
+        if (rot)
+          for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) {
+            const int i = e >> 5, j = e & 31;
+            B[(int64_t)j2_col(i, pa, pb) * np + j2_col(j, pa, pb)] = Gfin[i][j];
+          }
+        if (tid == 0) qflag[k] = rot ? 1 : 0;
       }
       __threadfence();
       j2_mark(6, t0);
@@ -508,12 +672,116 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       break;
     }
   }
-  if (me == 0 && tid == 0) result[0] = converged ? sweep : -sweep;
+  if (me == 0 && tid == 0) {
+    result[0] = converged ? sweep : -sweep;
+    result[4] = sweep;
+    result[5] = g;
+    result[7] = converged ? 1 : (sweep >= max_sweeps ? 2 : 0);
+    if (g_start == 0) off_slots[2] = abs_floor;
+  }
+}
+
+// ------------------------------------------------------------------ V update
+// The rotations of every step are logged (Qlog slot g % cap); V is updated
+// off the critical path by j2_vapply_kernel after the Jacobi launch: CTA b
+// keeps rows [16b, 16b+16) of V in shared memory and applies the logged
+// steps in order, V[rows, pair k cols] <- V[rows, pair k cols] Q_k, warp w
+// taking pairs w, w+16, ... with FP64 DMMA.  B fragments come straight from
+// L2 (each one feeds both 8-row groups); 16 warps keep enough loads in
+// flight to cover the L2 latency.
+constexpr int VA_R = 16, VA_THREADS = 512, VA_WARPS = VA_THREADS / 32;
+
+__global__ void __launch_bounds__(VA_THREADS)
+j2_vapply_kernel(double* __restrict__ V, int np, int nrows_v, const double* __restrict__ Qlog, int cap,
+                 const int* __restrict__ qflag_log, int* __restrict__ result, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int g0 = result[6], g1 = result[5];
+  const int nb = np / J2_BW, npairs = nb / 2;
+  const int ldt = np + 2;
+  extern __shared__ __align__(16) double va_smem[];
+  double* T = va_smem;  // VA_R x ldt
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int r0 = blockIdx.x * VA_R;
+  if (g1 > g0 && r0 < nrows_v) {
+    for (int e = tid; e < VA_R * np; e += VA_THREADS) {
+      const int r = e / np, c = e - r * np;
+      T[r * ldt + c] = r0 + r < nrows_v ? V[(int64_t)(r0 + r) * np + c] : 0.0;
+    }
+    for (int g = g0; g < g1; ++g) {
+      __syncthreads();  // step g-1 (or the tile load) complete
+      const int slot = g % cap, st = g % nb;
+      for (int k = w; k < npairs; k += VA_WARPS) {
+        if (!qflag_log[slot * npairs + k]) continue;
+        const double* q = Qlog + ((int64_t)slot * npairs + k) * J2_PW * J2_PW;
+        double b[8][4];
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4)
+#pragma unroll
+          for (int ct = 0; ct < 4; ++ct) b[k4][ct] = __ldg(q + (k4 * 4 + (lane & 3)) * J2_PW + ct * 8 + (lane >> 2));
+        int pa, pb;
+        j2_pair(st, k, nb, pa, pb);
+#pragma unroll
+        for (int rg = 0; rg < VA_R / 8; ++rg) {
+          double* trow = T + (rg * 8 + (lane >> 2)) * ldt;
+          double o[4][2] = {};
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) {
+            const double a = trow[j2_col(k4 * 4 + (lane & 3), pa, pb)];
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct) j2_dmma(o[ct][0], o[ct][1], a, b[k4][ct]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int ct = 0; ct < 4; ++ct)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) trow[j2_col(ct * 8 + 2 * (lane & 3) + e, pa, pb)] = o[ct][e];
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < VA_R * np; e += VA_THREADS) {
+      const int r = e / np, c = e - r * np;
+      if (r0 + r < nrows_v) V[(int64_t)(r0 + r) * np + c] = T[r * ldt + c];
+    }
+  }
+  // the last CTA to finish marks the logged range as applied
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&result[8], 1) + 1 == (int)gridDim.x) {
+      result[6] = g1;
+      result[8] = 0;
+      __threadfence();
+    }
+  }
+}
+
+static size_t vapply_smem(int np) { return (size_t)VA_R * (np + 2) * sizeof(double); }
+
+// Rotation-log capacity in steps: whole sweeps, up to 60, within ~128 MB.
+int jacobi2_log_steps(int np) {
+  const int nb = np / J2_BW, npairs = nb / 2;
+  if (npairs < 1) return 1;
+  const int64_t per_step = (int64_t)npairs * J2_PW * J2_PW * 8;
+  int64_t steps = ((int64_t)128 << 20) / per_step;
+  steps = std::min<int64_t>(steps, 60 * (int64_t)nb);
+  steps = std::max<int64_t>(steps / nb * nb, nb);
+  return (int)steps;
+}
+static bool j2_use_log(int np) { return vapply_smem(np) <= 200 * 1024; }
+
+int64_t jacobi2_qbuf_elems(int np) {
+  const int npairs = std::max(np / J2_BW / 2, 1);
+  return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs * J2_PW * J2_PW;
+}
+int64_t jacobi2_qflag_elems(int np) {
+  const int npairs = std::max(np / J2_BW / 2, 1);
+  return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs;
 }
 
 static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
-                     double* Qbuf, double* Gbuf, int* qflag, double* off_slots, int* result, const int* skip,
-                     cudaStream_t st) {
+                     double* Qlog, int cap, int* qflag_log, double* off_slots, int* result, const int* skip,
+                     int vlog, cudaStream_t st) {
   const int nb = np / J2_BW;
   const int npairs = nb / 2;
   const bool cluster = np <= 512;
@@ -525,7 +793,7 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
     nctas = std::max(1, std::min(std::max(npairs, npairs * (npairs + 1) / 4), nsm));
   }
   const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
-  const int nitems = npairs * (npairs - 1) / 2 + npairs * vchunks;
+  const int nitems = npairs * (npairs - 1) / 2 + (vlog ? 0 : npairs * vchunks);
   const size_t sched = (size_t)nb * npairs * sizeof(int) + (size_t)((nitems + nctas - 1) / nctas) * 8 +
                        (size_t)npairs * sizeof(int) + 64;
   const size_t qcache = (size_t)npairs * J2_PW * J2_LD * sizeof(double);
@@ -554,29 +822,43 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
     attr[0].val.clusterDim.x = nctas;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    MLR_CUDA(cudaLaunchKernelEx(&cfg, kern, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps, Qbuf, Gbuf, qflag,
-                                off_slots, result, skip, cache_q, early_off));
   } else {
-    auto kern = jacobi2_kernel<false>;
-    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLR_CUDA(cudaFuncSetAttribute(jacobi2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    MLR_CUDA(cudaLaunchKernelEx(&cfg, kern, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps, Qbuf, Gbuf, qflag,
-                                off_slots, result, skip, cache_q, early_off));
+  }
+  const size_t vsm = vapply_smem(np);
+  if (vlog) MLR_CUDA(cudaFuncSetAttribute(j2_vapply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+  // the log holds cap / nb sweeps: enough (jacobi, V) launch pairs for max_sweeps;
+  // launches after convergence return immediately
+  const int per_launch = vlog ? std::max(1, cap / nb) : max_sweeps;
+  const int launches = (max_sweeps + per_launch - 1) / per_launch;
+  for (int l = 0; l < std::max(launches, 1); ++l) {
+    if (cluster)
+      MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<true>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
+                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog));
+    else
+      MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<false>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
+                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog));
+    if (vlog) {
+      j2_vapply_kernel<<<(nrows_v + VA_R - 1) / VA_R, VA_THREADS, vsm, st>>>(V, np, nrows_v, Qlog, cap, qflag_log,
+                                                                            result, skip);
+      MLR_LAUNCH_CHECK("j2_vapply_kernel");
+    }
   }
   return kOk;
 }
 
 int jacobi2_debug_prof(unsigned long long* out8) {
-  MLR_CUDA(cudaMemcpyFromSymbol(out8, g_j2prof, sizeof(unsigned long long) * 8));
-  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  MLR_CUDA(cudaMemcpyFromSymbol(out8, g_j2prof, sizeof(unsigned long long) * 16));
+  unsigned long long z[16] = {};
   MLR_CUDA(cudaMemcpyToSymbol(g_j2prof, z, sizeof(z)));
   return kOk;
 }
 
-// Qbuf and Gbuf, npairs x 32 x 32 doubles each, stored back to back.
-int64_t jacobi2_qbuf_elems(int np) { return 2 * (int64_t)(np / J2_BW / 2) * J2_PW * J2_PW; }
-
+// Qbuf: the rotation log (jacobi2_qbuf_elems doubles); qflag:
+// jacobi2_qflag_elems ints; off_slots: 4 doubles; result: 16 ints
+// (result[0] = sweeps, negative when not converged).
 int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
                 void* Qbuf, int* qflag, double* off_slots, int* result, const int* skip, cudaStream_t st) {
   (void)f32;  // the coarse eigenproblem is always solved in FP64
@@ -584,11 +866,12 @@ int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, dou
     set_error("jacobi2_eig: n_p must be a multiple of 64");
     return kErrArg;
   }
-  MLR_CUDA(cudaMemsetAsync(off_slots, 0, 2 * sizeof(double), st));
-  double* q = (double*)Qbuf;
-  double* g = q + jacobi2_qbuf_elems(np) / 2;
-  return launch_j2((double*)B, (double*)V, np, nrows_v, tol, abs_floor_rel, max_sweeps, q, g, qflag, off_slots,
-                   result, skip, st);
+  MLR_CUDA(cudaMemsetAsync(off_slots, 0, 4 * sizeof(double), st));
+  MLR_CUDA(cudaMemsetAsync(result, 0, 16 * sizeof(int), st));
+  const int vlog = j2_use_log(np) ? 1 : 0;
+  const int cap = vlog ? jacobi2_log_steps(np) : 1;
+  return launch_j2((double*)B, (double*)V, np, nrows_v, tol, abs_floor_rel, max_sweeps, (double*)Qbuf, cap, qflag,
+                   off_slots, result, skip, vlog, st);
 }
 
 }  // namespace mlr

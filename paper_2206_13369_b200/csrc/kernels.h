@@ -51,7 +51,8 @@ int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out
               cudaStream_t st);
 int svt_weights(const int* skip, int np, int nh, bool f32, const void* Bd, const double* tau, double* sig_out,
                 double* f_out, int* rank_out, double* nuclear_out, cudaStream_t st);
-int64_t jacobi2_qbuf_elems(int np);
+int64_t jacobi2_qbuf_elems(int np);   // rotation log (doubles)
+int64_t jacobi2_qflag_elems(int np);  // rotation-log flags (ints)
 int jacobi2_debug_prof(unsigned long long* out8);
 int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
                 void* Qbuf, int* qflag, double* off_slots, int* result, const int* skip, cudaStream_t st);
