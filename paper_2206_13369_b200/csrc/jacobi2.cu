@@ -24,6 +24,8 @@
 // |g_ij| <= tol * sqrt(|g_ii g_jj|).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -107,6 +109,17 @@ __device__ __forceinline__ void atomic_max_nonneg2(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
+constexpr int J2_DF_MAXB = 128;  // dflow limit on the number of 16-blocks
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <bool CLUSTER>
 __device__ __forceinline__ void j2_sync() {
   if (CLUSTER) cg::this_cluster().sync();
@@ -171,6 +184,68 @@ __device__ __forceinline__ void tile_mm(const double (*A)[J2_LD], const double (
   }
 }
 
+// One off-diagonal pair-block item: out = Q_A^T X Q_B with X = B[pair
+// (a1, b1) columns, pair (a2, b2) columns]; ra / rb say whether Q_A / Q_B are
+// non-identity.  Leaves out in S.X (and its transpose in S.Q2); writes both
+// orientations back to B when `store` (the caller ensures ra || rb there).
+// Uses S.X, S.Y, S.Q, S.Q2; all threads; starts and ends with a barrier.
+template <typename Smem>
+__device__ __forceinline__ void j2_item(Smem& S, double* __restrict__ B, int np, int a1, int b1, int a2, int b2,
+                                        const double* __restrict__ QA, const double* __restrict__ QB, bool ra,
+                                        bool rb, bool store) {
+  const int tid = threadIdx.x;
+  double xr[4], qa[4], qb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {  // all three tiles in flight at once
+    const int e = tid + u * J2_THREADS;
+    xr[u] = B[(int64_t)j2_col(e >> 5, a1, b1) * np + j2_col(e & 31, a2, b2)];
+    qa[u] = ra ? QA[e] : 0.0;
+    qb[u] = rb ? QB[e] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * J2_THREADS;
+    S.X[e >> 5][e & 31] = xr[u];
+    if (ra) S.Q[e >> 5][e & 31] = qa[u];
+    if (rb) S.Q2[e >> 5][e & 31] = qb[u];
+  }
+  __syncthreads();
+  const int rr = tm_row();
+  double o[4];
+  if (!rb) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[u] = S.X[rr][tm_col(u)];
+  } else {
+    tile_mm<false>(S.X, S.Q2, o);  // Y = X Q_B
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) S.Y[rr][tm_col(u)] = o[u];
+  __syncthreads();
+  if (!ra) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[u] = S.Y[rr][tm_col(u)];
+  } else {
+    tile_mm<true>(S.Q, S.Y, o);  // Q_A^T Y
+  }
+  __syncthreads();  // everyone done reading S.X / S.Q2
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    S.X[rr][tm_col(u)] = o[u];
+    S.Q2[tm_col(u)][rr] = o[u];
+  }
+  __syncthreads();
+  if (store) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + u * J2_THREADS;
+      const int i = e >> 5, j = e & 31;
+      B[(int64_t)j2_col(i, a1, b1) * np + j2_col(j, a2, b2)] = S.X[i][j];
+      B[(int64_t)j2_col(i, a2, b2) * np + j2_col(j, a1, b1)] = S.Q2[i][j];
+    }
+  }
+}
+
 // Cycle breakdown of CTA 0 (phase A load+measure, inner rounds, barrier 1,
 // phase B, barrier 2, steps) — read with mlr_debug_j2prof.
 __device__ unsigned long long g_j2prof[16];
@@ -196,7 +271,7 @@ __global__ void __launch_bounds__(J2_THREADS)
 jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows_v, double tol,
                double abs_floor_rel, int max_sweeps, double* __restrict__ Qlog, int cap,
                int* __restrict__ qflag_log, double* __restrict__ off_slots, int* __restrict__ result,
-               const int* __restrict__ skip, int cache_q, double early_off, int vlog) {
+               const int* __restrict__ skip, int cache_q, double early_off, int vlog, int dflow) {
   if (skip && *skip) return;
   if (result[7] != 0) return;  // converged or out of sweeps in an earlier launch
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -209,7 +284,17 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   const int nbitems = npairs * (npairs - 1) / 2;  // off-diagonal pair blocks k1 < k2
   const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
   const int nitems = nbitems + (vlog ? 0 : npairs * vchunks);  // V items only without the log
-  const int my_items = (nitems - me + nctas - 1) / nctas;
+  // Dataflow steps (dflow, requires the rotation log): phase-B items run on
+  // the CTAs that own no pair when there are enough of them ("split"), the
+  // items holding a next-step pair's off-diagonal block first; each of those
+  // releases a per-pair flag that the next step's owner waits on instead of
+  // a cluster/grid barrier, so phase A of step t+1 overlaps phase B of step t.
+  const bool split = dflow && 2 * (nctas - npairs) >= npairs;
+  const int nworkers = split ? nctas - npairs : nctas;
+  const int widx = split ? me - npairs : me;  // < 0: owner only
+  const int my_items = (dflow || widx < 0) ? 0 : (nitems - widx + nworkers - 1) / nworkers;
+  int* cflag = qflag_log + cap * npairs;  // per next-step pair: step + 1 whose item is done
+  int* tctr = cflag + npairs;             // dflow item-queue ticket counters (2, by step parity)
   // dynamic smem: [J2Smem][Qcache npairs x 32 x LD (optional)][sched nb*npairs int][items][qslot npairs int]
   unsigned char* p = smem_raw + ((sizeof(J2Smem) + 127) & ~size_t(127));
   double(*Qall)[J2_PW][J2_LD] = reinterpret_cast<double(*)[J2_PW][J2_LD]>(p);
@@ -220,6 +305,8 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   p += (size_t)my_items * sizeof(J2Item);
   int* qslot = reinterpret_cast<int*>(p);  // my needed pairs -> cache slot (or -1)
   __shared__ int qf_all[64];
+  __shared__ short cur_pair[J2_DF_MAXB], nxt_pair[J2_DF_MAXB], nxt_partner[J2_DF_MAXB];
+  __shared__ int s_ticket;
   const double tol2 = tol * tol;
 
   for (int e = tid; e < nb * npairs; e += J2_THREADS) {
@@ -229,7 +316,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
     sched[e] = pa | (pb << 16);
   }
   for (int q = tid; q < my_items; q += J2_THREADS) {
-    const int it = me + q * nctas;
+    const int it = widx + q * nworkers;
     J2Item x;
     if (it < nbitems) {
       int k1 = 0, rem = it;
@@ -287,8 +374,73 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       // ------------------------------------------------ phase A: pair owners
       for (int k = me; k < npairs; k += nctas) {
         const int pa = srow[k] & 0xffff, pb = srow[k] >> 16;
+        // dflow: the off-diagonal block (pa, pb) comes from a phase-B item of
+        // the previous step (unless pa, pb were paired then) that may still run
+        bool loaded = false;
+        if (dflow && step > 0 && cur_pair[pa] != cur_pair[pb]) {
+          // (pa, pb) lies in the previous step's item (kA, kB), which the
+          // workers skip: the first pair of this step needing that item
+          // computes it, stores it and assembles its tile from it; a second
+          // one (same item) waits for the first one's flag and loads
+          const int k0a = cur_pair[pa], k0b = cur_pair[pb];
+          const int kA = min(k0a, k0b), kB = max(k0a, k0b);
+          int first = k;
+          for (int k2 = 0; k2 < k; ++k2) {
+            const int x = srow[k2];
+            const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
+            if (min(c1, c2) == kA && max(c1, c2) == kB) {
+              first = k2;
+              break;
+            }
+          }
+          if (first == k) {
+            const int* prow = sched + (step - 1) * npairs;
+            const int a1 = prow[kA] & 0xffff, b1 = prow[kA] >> 16;
+            const int a2 = prow[kB] & 0xffff, b2 = prow[kB] >> 16;
+            const int pslot = (g - 1) % cap;
+            const double* Qp = Qlog + (int64_t)pslot * npairs * J2_PW * J2_PW;
+            const int* qfp = qflag_log + pslot * npairs;
+            const bool ra = qfp[kA] != 0, rb = qfp[kB] != 0;
+            const double da = B[(int64_t)(pa * J2_BW + (tid >> 4)) * np + pa * J2_BW + (tid & 15)];
+            const double db = B[(int64_t)(pb * J2_BW + (tid >> 4)) * np + pb * J2_BW + (tid & 15)];
+            j2_item(S, B, np, a1, b1, a2, b2, Qp + (int64_t)kA * J2_PW * J2_PW, Qp + (int64_t)kB * J2_PW * J2_PW, ra,
+                    rb, ra || rb);
+            S.G[tid >> 4][tid & 15] = da;
+            S.G[J2_BW + (tid >> 4)][J2_BW + (tid & 15)] = db;
+            // my tile: diagonal blocks from B, the off-diagonal one from out
+            const bool pa_row = cur_pair[pa] == kA;  // pa indexes out's rows
+            const int hr = (pa_row ? (pa == a1 ? 0 : 1) : (pb == a1 ? 0 : 1)) * J2_BW;
+            const int hc = (pa_row ? (pb == a2 ? 0 : 1) : (pa == a2 ? 0 : 1)) * J2_BW;
+            for (int e = tid; e < J2_BW * J2_BW; e += J2_THREADS) {
+              const int i = e >> 4, j = e & 15;
+              const double v = pa_row ? S.X[hr + i][hc + j] : S.X[hr + j][hc + i];  // B[pa + i][pb + j]
+              S.G[i][J2_BW + j] = v;
+              S.G[J2_BW + j][i] = v;
+            }
+            loaded = true;
+            bool dup = false;
+            for (int k2 = k + 1; k2 < npairs; ++k2) {
+              const int x = srow[k2];
+              const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
+              if (min(c1, c2) == kA && max(c1, c2) == kB) dup = true;
+            }
+            if (dup) {
+              __syncthreads();
+              if (tid == 0) {
+                __threadfence();
+                for (int k2 = k + 1; k2 < npairs; ++k2) {
+                  const int x = srow[k2];
+                  const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
+                  if (min(c1, c2) == kA && max(c1, c2) == kB) st_release(cflag + k2, g + 1);
+                }
+              }
+            }
+          } else if (tid == 0) {
+            while (ld_acquire(cflag + k) < g + 1) __nanosleep(20);
+          }
+        }
         __syncthreads();
-        load_pair_tile(S.G, B, np, pa, pb, pa, pb);
+        if (!loaded) load_pair_tile(S.G, B, np, pa, pb, pa, pb);
         if (tid == 0) {
           S.active = 0;
         }
@@ -545,12 +697,31 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
           }
         if (tid == 0) qflag[k] = rot ? 1 : 0;
       }
-      __threadfence();
+      if (!CLUSTER) __threadfence();  // barrier.cluster.arrive/wait are release/acquire
       j2_mark(6, t0);
       j2_sync<CLUSTER>();
       j2_mark(2, t0);
       // ------------------------------------------------ phase B: apply
-      for (int k = tid; k < npairs; k += J2_THREADS) qf_all[k] = qflag[k];
+      if (!dflow || widx >= 0)
+        for (int k = tid; k < npairs; k += J2_THREADS) qf_all[k] = qflag[k];
+      const bool last_step = step == nb - 1;
+      if (dflow) {
+        // block -> pair maps of this step and the next (within the sweep)
+        for (int k = tid; k < npairs; k += J2_THREADS) {
+          const int pa = srow[k] & 0xffff, pb = srow[k] >> 16;
+          cur_pair[pa] = (short)k;
+          cur_pair[pb] = (short)k;
+          if (!last_step) {
+            const int nx = sched[(step + 1) * npairs + k];
+            const int na = nx & 0xffff, nbk = nx >> 16;
+            nxt_pair[na] = (short)k;
+            nxt_pair[nbk] = (short)k;
+            nxt_partner[na] = (short)nbk;
+            nxt_partner[nbk] = (short)na;
+          }
+        }
+      }
+      __syncthreads();
       __syncthreads();
       if (cache_q) {  // the rotations my items read (rotated pairs only), via cp.async
         for (int e2 = tid; e2 < npairs * J2_PW * J2_PW / 2; e2 += J2_THREADS) {
@@ -657,9 +828,67 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
         q = q2;
       }
-      __threadfence();
+      if (dflow && widx >= 0) {
+        // Dynamic item queue over the items that no next-step owner computes
+        // (see phase A).  Worker w's first ticket is w, the rest come from an
+        // atomic counter offset by nworkers; each worker ends with exactly
+        // one failing grab and the grab completing the count resets it.
+        unsigned char* dmark = reinterpret_cast<unsigned char*>(items);
+        int* ctr = tctr + (g & 1);
+        for (int it = tid; it < nbitems; it += J2_THREADS) dmark[it] = 0;
+        __syncthreads();
+        if (!last_step)
+          for (int k2 = tid; k2 < npairs; k2 += J2_THREADS) {
+            const int nx = sched[(step + 1) * npairs + k2];
+            const int ka = cur_pair[nx & 0xffff], kb = cur_pair[nx >> 16];
+            if (ka != kb) {
+              const int lo = min(ka, kb), hi = max(ka, kb);
+              dmark[lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1)] = 1;
+            }
+          }
+        __syncthreads();
+        const int total = nbitems;
+        const int grabs = (total > nworkers ? total - nworkers : 0) + nworkers;
+        auto grab = [&]() {
+          if (tid == 0) s_ticket = atomicAdd(ctr, 1);
+          __syncthreads();
+          const int v = s_ticket;
+          __syncthreads();
+          return v;
+        };
+        int tk = widx, last_v = -1;
+        for (;;) {
+          if (tk >= total) {
+            if (last_v < 0) {  // the pre-assigned ticket was past the end: make the failing grab
+              last_v = grab();
+              tk = nworkers + last_v;
+              continue;
+            }
+            break;
+          }
+          const int it = tk;
+          if (!dmark[it]) {
+            int kA = 0, rem = it;
+            while (rem >= npairs - 1 - kA) {
+              rem -= npairs - 1 - kA;
+              ++kA;
+            }
+            const int kB = kA + 1 + rem;
+            if (qf_all[kA] || qf_all[kB]) {
+              const int a1 = srow[kA] & 0xffff, b1 = srow[kA] >> 16;
+              const int a2 = srow[kB] & 0xffff, b2 = srow[kB] >> 16;
+              j2_item(S, B, np, a1, b1, a2, b2, Qbuf + (int64_t)kA * J2_PW * J2_PW,
+                      Qbuf + (int64_t)kB * J2_PW * J2_PW, qf_all[kA] != 0, qf_all[kB] != 0, true);
+            }
+          }
+          last_v = grab();
+          tk = nworkers + last_v;
+        }
+        if (tid == 0 && last_v == grabs - 1) atomicExch(ctr, 0);
+      }
+      if (!CLUSTER && (!dflow || last_step)) __threadfence();
       j2_mark(3, t0);
-      j2_sync<CLUSTER>();
+      if (!dflow || last_step) j2_sync<CLUSTER>();  // sweep end: convergence check, pause
       j2_mark(4, t0);
     }
     const double off = *((volatile double*)&off_slots[sweep & 1]);
@@ -774,9 +1003,9 @@ int64_t jacobi2_qbuf_elems(int np) {
   const int npairs = std::max(np / J2_BW / 2, 1);
   return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs * J2_PW * J2_PW;
 }
-int64_t jacobi2_qflag_elems(int np) {
+int64_t jacobi2_qflag_elems(int np) {  // log flags + the dataflow pair flags
   const int npairs = std::max(np / J2_BW / 2, 1);
-  return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs;
+  return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs + npairs + 2;
 }
 
 static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
@@ -794,10 +1023,15 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   }
   const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
   const int nitems = npairs * (npairs - 1) / 2 + (vlog ? 0 : npairs * vchunks);
-  const size_t sched = (size_t)nb * npairs * sizeof(int) + (size_t)((nitems + nctas - 1) / nctas) * 8 +
-                       (size_t)npairs * sizeof(int) + 64;
+  // dataflow steps (see jacobi2_kernel) when the per-CTA item lists fit
+  int dflow = 0;
+  if (vlog && nb <= J2_DF_MAXB) dflow = 1;
+  if (const char* e = getenv("MLR_J2_DFLOW")) dflow = dflow && e[0] != '0';
+  const int max_items = dflow ? 0 : (nitems + nctas - 1) / nctas;
+  const size_t item_bytes = dflow ? (size_t)nitems + 16 : (size_t)max_items * 8;
+  const size_t sched = (size_t)nb * npairs * sizeof(int) + item_bytes + (size_t)npairs * sizeof(int) + 64;
   const size_t qcache = (size_t)npairs * J2_PW * J2_LD * sizeof(double);
-  const int cache_q = (sizeof(J2Smem) + qcache + sched <= 200 * 1024) ? 1 : 0;
+  const int cache_q = (!dflow && sizeof(J2Smem) + qcache + sched <= 200 * 1024) ? 1 : 0;
   const size_t smem = ((sizeof(J2Smem) + 127) & ~size_t(127)) + (cache_q ? qcache : 0) + sched;
   if (smem > 220 * 1024) {
     set_error("jacobi2: schedule does not fit in shared memory");
@@ -836,10 +1070,10 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   for (int l = 0; l < std::max(launches, 1); ++l) {
     if (cluster)
       MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<true>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
-                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog));
+                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow));
     else
       MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<false>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
-                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog));
+                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow));
     if (vlog) {
       j2_vapply_kernel<<<(nrows_v + VA_R - 1) / VA_R, VA_THREADS, vsm, st>>>(V, np, nrows_v, Qlog, cap, qflag_log,
                                                                             result, skip);
@@ -868,6 +1102,7 @@ int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, dou
   }
   MLR_CUDA(cudaMemsetAsync(off_slots, 0, 4 * sizeof(double), st));
   MLR_CUDA(cudaMemsetAsync(result, 0, 16 * sizeof(int), st));
+  MLR_CUDA(cudaMemsetAsync(qflag, 0, sizeof(int) * jacobi2_qflag_elems(np), st));
   const int vlog = j2_use_log(np) ? 1 : 0;
   const int cap = vlog ? jacobi2_log_steps(np) : 1;
   return launch_j2((double*)B, (double*)V, np, nrows_v, tol, abs_floor_rel, max_sweeps, (double*)Qbuf, cap, qflag,
