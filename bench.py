@@ -32,6 +32,16 @@ METRIC = "ML-PCP iterations/s (C2: 2000x2000 FP32, n_H=250, tol 1e-6)"
 UNIT = "iterations/s"
 
 
+def _ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full capture (profiles/)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic_c2.json")
+    try:
+        with open(p) as f:
+            return json.load(f)["kernels"]
+    except (OSError, ValueError, KeyError):
+        return {}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -242,38 +252,41 @@ def main():
     nh = cfg["n_coarse"]
     npad = (nh + 63) // 64 * 64
     b = bytes_el
-    upd_bytes = b * (3 * m * n + 2 * m * npad)          # D, Y in; Y out; Z in; A' out
-    roof = None
+    # B_iter = b (3 m n + 2 m n_H) -- read D, Y, write Y; A' written/read once
+    upd_bytes = b * (3 * m * n + 2 * m * npad)
+    traffic = _ncu_traffic()
     phase_ms = {k: v[0] for k, v in phases.items()}
     dominant = max(phase_ms, key=phase_ms.get) if phase_ms else None
     sweeps = [x for s in sink for x in s.get("jac_sweeps", [])]
-    if dominant == "update" or dominant is None:
-        ms, cnt = phases.get("update", [float("nan"), 1])
-        ach = upd_bytes / (ms / cnt / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "pcp_row_kernel<float,kUpdate>", "achieved": ach,
-                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": None,
-                "algorithmic_bytes_per_launch": upd_bytes}
-    else:
-        ms, cnt = phases[dominant]
-        if dominant == "jacobi":
-            nb = npad // (32 if npad >= 1024 else 16)
-            per_sweep = 12.0 * npad ** 3 * (nb - 1) / nb
-            flops = per_sweep * (statistics.mean(sweeps) if sweeps else 1.0)
-            fp64_peak = 40.0
-            ach = flops / (ms / cnt / 1e3) / 1e12
-            roof = {"bound": "tensor", "kernel": "jacobi_kernel<16> (FP64 one-sided block Jacobi)",
-                    "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                    "peak_source": "nominal B200 FP64 (not in MEASURED_PEAKS.json)", "traffic": None,
-                    "algorithmic_flops_per_launch": flops, "mean_sweeps": statistics.mean(sweeps) if sweeps else None}
-        else:
-            roof = {"bound": "tensor", "kernel": dominant, "achieved": None, "peak": None, "unit": "TFLOP/s",
-                    "frac": None, "traffic": None}
+    mean_sweeps = statistics.mean(sweeps) if sweeps else 1.0
+    roof = None
+    if dominant == "jacobi":
+        # Two-sided block Jacobi on the n_p x n_p coarse Gram (FP64): per sweep the
+        # block rotations of B~ (8 n_p^3) and of V (4 n_p^3) -> 12 n_p^3 flops.
+        ms, cnt = phases["jacobi"]
+        flops = 12.0 * npad ** 3 * mean_sweeps
+        fp64_peak = 40.0
+        ach = flops / (ms / cnt / 1e3) / 1e12
+        t = traffic.get("jacobi2_kernel")
+        roof = {"bound": "tensor", "kernel": "jacobi2_kernel<cluster> + j2_vapply_kernel (FP64 two-sided block "
+                "Jacobi, 16-CTA cluster; latency-bound: one 32x32 rotation chain per round)",
+                "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                "peak_source": "nominal B200 FP64 tensor (FP64 not in MEASURED_PEAKS.json)",
+                "traffic": t["dram_bytes_per_launch"] if t else None,
+                "algorithmic_flops_per_launch": flops, "mean_sweeps": mean_sweeps,
+                "flops_formula": "12 n_p^3 per sweep"}
     upd = phases.get("update")
     streaming = None
     if upd:
         ach = upd_bytes / (upd[0] / upd[1] / 1e3) / 1e9
-        streaming = {"kernel": "pcp_row_kernel (fused prolong/shrink/dual/restrict)", "achieved_gbs": ach,
-                     "frac_of_measured_hbm": ach / peaks["hbm_gbs"], "avg_us": 1e3 * upd[0] / upd[1]}
+        t = traffic.get("pcp_rows_warp<float, 1>")
+        streaming = {"bound": "hbm", "kernel": "pcp_rows_warp<float,kUpdate> (fused prolong/shrink/dual/restrict, "
+                     "warp per row)", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": ach / peaks["hbm_gbs"], "traffic": t["dram_bytes_per_launch"] if t else None,
+                     "algorithmic_bytes_per_launch": upd_bytes, "avg_us": 1e3 * upd[0] / upd[1],
+                     "bytes_formula": "b (3 m n + 2 m n_p)"}
+        if roof is None:
+            roof = streaming
     per_iter = {k: round(v / max(1, sum(s.get("iters", 0) for s in sink)), 4) for k, v in phase_ms.items()}
 
     cpu = None
@@ -284,7 +297,10 @@ def main():
                "sample": f"1 full C2 solve ({it} iterations, oracle port of mlrpca.ml_ialm_solve, numpy/OpenBLAS FP64)"}
 
     lz = statistics.mean(s.get("lanczos_steps", 0) for s in sink) if sink else 0
-    per_solve_launches = (14 * (iters / args.steps) + 4 * lz + 12)
+    # launches per solve (see profiles/r01_bench_launches_c2.md): 15 per iteration
+    # (gram 2, pre 3, jacobi 2, after/weights 2, post 2, recon 1, update 2, finalize 1),
+    # 4 per Lanczos step, ~12 fixed (stats, start, outputs)
+    per_solve_launches = (15 * (iters / args.steps) + 4 * lz + 12)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

@@ -102,11 +102,11 @@ int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, 
 int mlr_pcp_state(void* plan, double* out16, void* stream);
 int mlr_pcp_history(void* plan, int count, double* out, void* stream); /* count x 8 */
 /* Per-phase CUDA-event timing: phases gram, pre (B, X=BV), jacobi, post
- * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize.
- * mlr_pcp_timing synchronises, returns total ms and launch counts per phase
- * (7 entries each) and resets the accumulators. */
+ * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize,
+ * lanczos (sigma_1 estimate).  mlr_pcp_timing synchronises, returns total ms
+ * and launch counts per phase (8 entries each) and resets the accumulators. */
 int mlr_pcp_set_timing(void* plan, int enable);
-int mlr_pcp_timing(void* plan, double* ms7, int* counts7);
+int mlr_pcp_timing(void* plan, double* ms8, int* counts8);
 
 /* ---------------------------------------------------------------- ML-CPCP
  * mask: bit-packed observation pattern, uint32 words, ldm words per row,
@@ -129,9 +129,9 @@ int mlr_cpcp_outputs(void* plan, void* L, int64_t ldl, void* stream);
 /* out32: k, done, status, t_l, t_s, u_l, u_s, sigma, passes, ga, gb, corner_l, corner_s, i_s, j_s, s2, ... */
 int mlr_cpcp_state(void* plan, double* out32, void* stream);
 int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, void* stream); /* count x 8, count */
-/* Per-phase CUDA-event timing (7 slots: gram, power, dots, qp, unused, update, finalize). */
+/* Per-phase CUDA-event timing (8 slots: gram, power, dots, qp, -, update, finalize, -). */
 int mlr_cpcp_set_timing(void* plan, int enable);
-int mlr_cpcp_timing(void* plan, double* ms7, int* counts7);
+int mlr_cpcp_timing(void* plan, double* ms8, int* counts8);
 
 #ifdef __cplusplus
 }

@@ -116,15 +116,15 @@ class CudaPcp:
         _lib.check(self.lib.mlr_pcp_history(self.h, int(count), out.ctypes.data, _stream()))
         return out[:count]
 
-    PHASES = ("gram", "pre", "jacobi", "post", "recon", "update", "finalize")
+    PHASES = ("gram", "pre", "jacobi", "post", "recon", "update", "finalize", "lanczos")
 
     def set_timing(self, on):
         _lib.check(self.lib.mlr_pcp_set_timing(self.h, int(bool(on))))
 
     def timing(self):
         """{phase: (total ms, launches)} since the last call (synchronises)."""
-        ms = np.zeros(7)
-        cnt = np.zeros(7, dtype=np.int32)
+        ms = np.zeros(8)
+        cnt = np.zeros(8, dtype=np.int32)
         _lib.check(self.lib.mlr_pcp_timing(self.h, ms.ctypes.data, cnt.ctypes.data))
         return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES)}
 
@@ -211,16 +211,16 @@ class CudaCpcp:
             d[k] = int(d[k])
         return d
 
-    PHASES = ("gram", "power", "dots", "qp", "unused", "update", "finalize")
+    PHASES = ("gram", "power", "dots", "qp", "unused", "update", "finalize", "unused2")
 
     def set_timing(self, on):
         _lib.check(self.lib.mlr_cpcp_set_timing(self.h, int(bool(on))))
 
     def timing(self):
-        ms = np.zeros(7)
-        cnt = np.zeros(7, dtype=np.int32)
+        ms = np.zeros(8)
+        cnt = np.zeros(8, dtype=np.int32)
         _lib.check(self.lib.mlr_cpcp_timing(self.h, ms.ctypes.data, cnt.ctypes.data))
-        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES) if p != "unused"}
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES) if not p.startswith("unused")}
 
     def history(self, count):
         out = np.zeros((max(count, 1), 8))

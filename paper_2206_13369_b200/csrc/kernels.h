@@ -59,7 +59,7 @@ int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, dou
 
 // Optional per-phase CUDA-event timing (enabled by mlr_pcp_set_timing):
 // every launch of a phase is bracketed by an event pair on its stream.
-enum PcpPhase { kPhGram = 0, kPhPre, kPhJacobi, kPhPost, kPhRecon, kPhUpdate, kPhFinalize, kPhCount };
+enum PcpPhase { kPhGram = 0, kPhPre, kPhJacobi, kPhPost, kPhRecon, kPhUpdate, kPhFinalize, kPhLanczos, kPhCount };
 
 struct PhaseTimer {
   bool on = false;

@@ -11,10 +11,14 @@
 // so each iteration reads D and Y once and writes Y once (plus m x n_H for
 // Z and A').  S is never stored: it is recomputed at exit from the previous
 // Y (double-buffered by the host).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "pcp.h"
 #include "rows.h"
+
+namespace cg = cooperative_groups;
 
 namespace mlr {
 
@@ -127,13 +131,24 @@ __global__ void lz_dtv_kernel(const LanczosDev* __restrict__ lz, const T* __rest
 }
 
 // True if the symmetric tridiagonal (a[0..k1), b[0..k1-1)) has an eigenvalue
-// above x (Sturm count via the LDL^T pivots of T - x I).
+// above x: T - x I has a positive LDL^T pivot d_i = p_i / p_(i-1), with the
+// leading principal minors p_i = (a_i - x) p_(i-1) - b_(i-1)^2 p_(i-2)
+// (division-free; rescaled when large, the ratio is scale-free).
 __device__ __forceinline__ bool tridiag_has_above(const double* a, const double* b, int k1, double x) {
-  double d = 1.0;
-  for (int i = 0; i < k1; ++i) {
-    d = (a[i] - x) - (i > 0 ? b[i - 1] * b[i - 1] / d : 0.0);
-    if (d == 0.0) d = -1e-300;
-    if (d > 0.0) return true;
+  double pm = 1.0, p = a[0] - x;
+  if (p > 0.0) return true;
+  if (p == 0.0) p = -1e-300;
+  for (int i = 1; i < k1; ++i) {
+    const double bb = b[i - 1] * b[i - 1];
+    double pn = fma(a[i] - x, p, -bb * pm);
+    if (pn == 0.0) pn = -1e-300 * copysign(1.0, p);
+    if ((pn > 0.0) == (p > 0.0)) return true;  // d_i = pn / p > 0
+    pm = p;
+    p = pn;
+    if (fabs(p) > 1e150) {
+      p *= 1e-150;
+      pm *= 1e-150;
+    }
   }
   return false;
 }
@@ -255,6 +270,143 @@ __global__ void __launch_bounds__(1024) lz_update_kernel(LanczosDev* lz, double*
     double* qn = Q + (int64_t)(k + 1) * n;
     const double inv = 1.0 / beta_s;
     for (int j = threadIdx.x; j < n; j += blockDim.x) qn[j] = w[j] * inv;
+  }
+}
+
+// One Lanczos step on a 16-CTA cluster: CTA r owns columns [r S, (r+1) S) of
+// every basis vector (S = ceil(n / 16)), so the two reorthogonalisation
+// passes stream the basis through 16 SMs.  Dot products are combined by
+// reading the 16 partials over DSMEM in a fixed order (identical in every
+// CTA); every CTA then evaluates the Ritz value redundantly.
+constexpr int LZ_CL = 16, LZ_T = 256;
+
+__device__ __forceinline__ double lz_cluster_sum(cg::cluster_group& cl, double* part_local, int idx) {
+  // partials are published by the caller (cl.sync() in between); lanes 0..15 of warp 0 gather
+  double v = 0.0;
+  const int lane = threadIdx.x & 31;
+  if (lane < LZ_CL) v = cl.map_shared_rank(part_local, lane)[idx];
+  return warp_sum(v);
+}
+
+__global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double* __restrict__ Q,
+                                                           const double* __restrict__ w_in, int n, double tol) {
+  if (lz->done) return;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int S = (n + LZ_CL - 1) / LZ_CL;
+  const int j0 = r * S, len = max(0, min(n, j0 + S) - j0);
+  const int k = lz->k;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  extern __shared__ __align__(16) double lzs[];
+  double* w = lzs;                  // S
+  double* part = w + S;             // partials: [0] alpha, [1] beta, [2..2+K) h pass 0, [2+K..2+2K) h pass 1
+  const int K = k + 1;
+  double* hfull = part + 2 + 2 * K;  // K
+  double* ta = hfull + K;            // tridiagonal alpha[0..K)
+  double* tb = ta + K;               // beta[0..K)
+  double* acc0 = tb + K;             // S: reorthogonalisation halves
+  double* acc1 = acc0 + S;           // S
+  __shared__ double scratch[32];
+  __shared__ double bcast;
+  const double* qk = Q + (int64_t)k * n + j0;
+  // alpha = q_k . w
+  double s = 0.0;
+  for (int j = tid; j < len; j += LZ_T) {
+    const double v = w_in[j0 + j];
+    w[j] = v;
+    s = fma(v, qk[j], s);
+  }
+  double v1[1] = {s};
+  block_sum<1>(v1, scratch);
+  if (tid == 0) part[0] = v1[0];
+  cl.sync();
+  if (wid == 0) {
+    const double a = lz_cluster_sum(cl, part, 0);
+    if (lane == 0) bcast = a;
+  }
+  __syncthreads();
+  const double alpha = bcast;
+  const double bprev = k > 0 ? lz->beta[k - 1] : 0.0;
+  for (int j = tid; j < len; j += LZ_T) {
+    double v = w[j] - alpha * qk[j];
+    if (k > 0) v -= bprev * Q[(int64_t)(k - 1) * n + j0 + j];
+    w[j] = v;
+  }
+  __syncthreads();
+  // full reorthogonalisation, twice (classical Gram-Schmidt)
+  for (int pass = 0; pass < 2; ++pass) {
+    double* ph = part + 2 + pass * K;
+    for (int c = wid; c < K; c += LZ_T / 32) {
+      const double* qc = Q + (int64_t)c * n + j0;
+      double d = 0.0;
+      for (int j = lane; j < len; j += 32) d = fma(qc[j], w[j], d);
+      d = warp_sum(d);
+      if (lane == 0) ph[c] = d;
+    }
+    cl.sync();
+    for (int c = wid; c < K; c += LZ_T / 32) {
+      const double h = lz_cluster_sum(cl, ph, c);
+      if (lane == 0) hfull[c] = h;
+    }
+    __syncthreads();
+    // w -= Q^T h: threads (half, j) split the basis vectors in two halves,
+    // 8 loads in flight per thread, halves combined through shared memory
+    {
+      const int half = tid / (LZ_T / 2), jt = tid % (LZ_T / 2);
+      const int c0 = half ? K / 2 : 0, c1 = half ? K : K / 2;
+      for (int j = jt; j < len; j += LZ_T / 2) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (int c = c0; c < c1; ++c) acc = fma(hfull[c], Q[(int64_t)c * n + j0 + j], acc);
+        (half ? acc1 : acc0)[j] = acc;
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < len; j += LZ_T) w[j] -= acc0[j] + acc1[j];
+    __syncthreads();
+  }
+  double nn = 0.0;
+  for (int j = tid; j < len; j += LZ_T) nn = fma(w[j], w[j], nn);
+  double v2[1] = {nn};
+  block_sum<1>(v2, scratch);
+  if (tid == 0) part[1] = v2[0];
+  cl.sync();
+  if (wid == 0) {
+    const double b2 = lz_cluster_sum(cl, part, 1);
+    if (lane == 0) bcast = sqrt(b2);
+  }
+  for (int c = tid; c < k; c += LZ_T) {
+    ta[c] = lz->alpha[c];
+    tb[c] = lz->beta[c];
+  }
+  __syncthreads();
+  const double beta = bcast;
+  if (tid == 0) {
+    ta[k] = alpha;
+    tb[k] = beta;
+  }
+  __syncthreads();
+  const double th = tridiag_max_eig_block(ta, tb, K);
+  const double rel = lz->theta > 0.0 ? fabs(th - lz->theta) / th : 1.0;
+  const int stable = (rel <= tol) ? lz->stable + 1 : 0;
+  const bool stop = (stable >= 2 && k >= 3) || beta <= 1e-300 * fmax(th, 1e-300) || k + 1 >= lz->kmax;
+  if (!stop) {
+    double* qn = Q + (int64_t)(k + 1) * n + j0;
+    const double inv = 1.0 / beta;
+    for (int j = tid; j < len; j += LZ_T) qn[j] = w[j] * inv;
+  }
+  cl.sync();  // every CTA has read lz and the remote partials
+  if (r == 0 && tid == 0) {
+    lz->alpha[k] = alpha;
+    lz->beta[k] = beta;
+    lz->theta_prev = lz->theta;
+    lz->theta = th;
+    lz->stable = stable;
+    if (stop) {
+      lz->done = 1;
+      lz->sigma1 = sqrt(fmax(th, 0.0));
+    }
+    lz->k = stop ? k : k + 1;
   }
 }
 
@@ -516,6 +668,7 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
     MLR_CUDA(cudaMemsetAsync(wpart_out, 0, sizeof(double) * n, st));
     return kOk;
   }
+  p->timer.begin(st);
   int blocks = p->row_blocks;
   if (p->f32)
     lz_dv_kernel<float><<<blocks, 256, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzQ, p->lzT);
@@ -530,12 +683,32 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
   else
     lz_dtv_kernel<double><<<grid, 128, 0, st>>>(p->lz, (const double*)D, ldd, m, n, p->lzT, p->lzW, rps);
   MLR_LAUNCH_CHECK("lz_dtv_kernel");
-  return sum_slices(p->lzW, n, n, splits, wpart_out, st);
+  const int rc = sum_slices(p->lzW, n, n, splits, wpart_out, st);
+  p->timer.end(kPhLanczos, st);
+  return rc;
 }
 
 int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStream_t st) {
-  lz_update_kernel<<<1, 1024, 0, st>>>(p->lz, p->lzQ, w_reduced, p->lzWork, p->ch.n, tol);
-  MLR_LAUNCH_CHECK("lz_update_kernel");
+  const int n = p->ch.n;
+  const int K = p->lz_kmax + 1;
+  const size_t smem = sizeof(double) * (3 * (size_t)ceil_div(n, LZ_CL) + 2 + 5 * (size_t)K + 8);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(LZ_CL);
+  cfg.blockDim = dim3(LZ_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = LZ_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MLR_CUDA(cudaFuncSetAttribute(lz_update_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MLR_CUDA(cudaFuncSetAttribute(lz_update_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  p->timer.begin(st);
+  MLR_CUDA(cudaLaunchKernelEx(&cfg, lz_update_cluster, p->lz, p->lzQ, w_reduced, n, tol));
+  p->timer.end(kPhLanczos, st);
   return kOk;
 }
 

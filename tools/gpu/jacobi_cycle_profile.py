@@ -16,4 +16,5 @@ for name in sys.argv[1:]:
     v = list(buf); steps = max(v[5], 1)
     names = ["A_load", "A_Q", "bar1", "B_apply", "bar2", "steps", "A_publish", "A_rounds"]
     print(name, 'iters', st.iter, 'steps', steps, {names[i]: round(v[i] / steps) for i in (0, 7, 1, 6, 2, 3, 4)}, 'total cycles/step', round(sum(v[i] for i in (0,1,2,3,4,6,7)) / steps), flush=True)
-
+    if v[10]:
+        print('   pipelined rounds', v[10], 'rotation warp cycles/round', round(v[8]/v[10]), 'update thread', round(v[9]/v[10]), 'incl barrier', round(v[11]/v[10]), flush=True)
