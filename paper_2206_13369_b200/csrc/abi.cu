@@ -253,6 +253,12 @@ int mlr_chain_create(int n, int nh, const int32_t* c0, const double* w0, const d
     bool dense = n > 0 && c0[0] == 0 && c0[n - 1] >= nh - 2;
     for (int j = 1; j < n && dense; ++j) dense = c0[j] - c0[j - 1] <= 1;
     d.keys_dense = dense ? 1 : 0;
+    int run = 0, best = 0;
+    for (int j = 0; j < n; ++j) {
+      run = (j > 0 && c0[j] == c0[j - 1]) ? run + 1 : 1;
+      best = std::max(best, run);
+    }
+    d.max_run = best;
   }
   auto up = [&](void** dst, const void* src, size_t bytes) -> int {
     void* p = nullptr;

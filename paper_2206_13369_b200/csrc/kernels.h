@@ -45,6 +45,7 @@ struct ChainDev {
   double* gi;           // dense G_R^{-1}, np x np (zero padded)
   int max_span;         // max hi-lo
   int keys_dense;       // c0 starts at 0, steps by <= 1 and reaches nh-2 (segmented restriction valid)
+  int max_run;          // longest run of equal c0
 };
 
 int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out, int trans_in,

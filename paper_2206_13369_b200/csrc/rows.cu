@@ -100,20 +100,20 @@ template <typename T, int NV>
 struct StencilVec {
   int key[NV];
   T w0[NV], w1[NV];
-  __device__ __forceinline__ void load(const ChainDev& ch, int j) {
+  __device__ __forceinline__ void load(const int* __restrict__ c0, const T* __restrict__ w0p,
+                                       const T* __restrict__ w1p, int n, int j) {
     using VT = Vec<T>;
-    const int n = ch.n;
     if (j + NV <= n) {
-      VT::unpacki(__ldg(reinterpret_cast<const typename VT::I*>(ch.c0 + j)), key);
-      VT::unpack(__ldg(reinterpret_cast<const typename VT::V*>(stencil_w0<T>(ch) + j)), w0);
-      VT::unpack(__ldg(reinterpret_cast<const typename VT::V*>(stencil_w1<T>(ch) + j)), w1);
+      VT::unpacki(__ldg(reinterpret_cast<const typename VT::I*>(c0 + j)), key);
+      VT::unpack(__ldg(reinterpret_cast<const typename VT::V*>(w0p + j)), w0);
+      VT::unpack(__ldg(reinterpret_cast<const typename VT::V*>(w1p + j)), w1);
     } else {
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
         const bool in = j + e < n;
-        key[e] = in ? __ldg(ch.c0 + j + e) : INT_MAX;
-        w0[e] = in ? __ldg(stencil_w0<T>(ch) + j + e) : T(0);
-        w1[e] = in ? __ldg(stencil_w1<T>(ch) + j + e) : T(0);
+        key[e] = in ? __ldg(c0 + j + e) : INT_MAX;
+        w0[e] = in ? __ldg(w0p + j + e) : T(0);
+        w1[e] = in ? __ldg(w1p + j + e) : T(0);
       }
     }
   }
@@ -121,24 +121,34 @@ struct StencilVec {
 
 // Streaming restriction of NB fine quantities x (one row) onto coarse keys.
 // Call chunk() once per chunk with every lane's NV values, then finish().
+// Per chunk: an in-lane then a warp segmented scan (`steps` shuffle steps
+// suffice when no run of equal c0 spans more than 2^steps lanes) gives every
+// run's w0 and w1 sums; runs that end in the chunk are ranked with ballots
+// and staged, and since keys are dense (run K ends before run K + 1), lane p
+// writes key K_p = T1(run K_p - 1) + T0(run K_p) straight to HBM (coalesced).
 template <typename T, int NB, int NV>
 struct SegRestrict {
-  static constexpr int RK = 64 * NV;  // key ring (2 * CH)
-  T* acc;                             // NB * RK, zero on entry and exit
-  int carry_key, kflush;
-  T carry0[NB], carry1[NB];
+  static constexpr int MAXE = 32 * NV;  // run ends per chunk (at most one per element)
+  static constexpr int STAGE_BYTES = MAXE * 4 + 2 * NB * MAXE * (int)sizeof(T);
+  int* skey;
+  T* st0;  // NB x MAXE
+  T* st1;  // NB x MAXE
+  int carry_key, last_key;
+  T carry0[NB], carry1[NB], prev1[NB];
 
-  __device__ __forceinline__ void begin(T* ring) {
-    acc = ring;
+  __device__ __forceinline__ void begin(unsigned char* stage) {
+    skey = reinterpret_cast<int*>(stage);
+    st0 = reinterpret_cast<T*>(stage + MAXE * 4);
+    st1 = st0 + NB * MAXE;
     carry_key = INT_MAX - 1;
-    kflush = -1;
+    last_key = -1;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) carry0[b] = carry1[b] = T(0);
+    for (int b = 0; b < NB; ++b) carry0[b] = carry1[b] = prev1[b] = T(0);
   }
 
   // next_key: c0 of the first fine column after this chunk (INT_MAX at the row end).
   __device__ __forceinline__ void chunk(const StencilVec<T, NV>& sv, const T (&x)[NB][NV], int next_key,
-                                        T* const (&out)[NB], int nh, int lane) {
+                                        T* const (&out)[NB], int lane, int steps) {
     const int(&key)[NV] = sv.key;
     T t0[NB][NV], t1[NB][NV];
 #pragma unroll
@@ -150,13 +160,14 @@ struct SegRestrict {
       }
     // in-lane segmented inclusive scan
 #pragma unroll
-    for (int e = 1; e < NV; ++e)
-      if (key[e] == key[e - 1])
+    for (int e = 1; e < NV; ++e) {
+      const bool same = key[e] == key[e - 1];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          t0[b][e] += t0[b][e - 1];
-          t1[b][e] += t1[b][e - 1];
-        }
+      for (int b = 0; b < NB; ++b) {
+        t0[b][e] += same ? t0[b][e - 1] : T(0);
+        t1[b][e] += same ? t1[b][e - 1] : T(0);
+      }
+    }
     // warp segmented inclusive scan of the lane tails (keys are monotone, so
     // equal tail keys imply every lane in between is one run)
     const int kt = key[NV - 1];
@@ -167,17 +178,17 @@ struct SegRestrict {
       s1[b] = t1[b][NV - 1];
     }
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int st = 0; st < 5; ++st) {
+      if (st >= steps) break;
+      const int o = 1 << st;
       const int kk = __shfl_up_sync(kFull, kt, o);
       const bool take = lane >= o && kk == kt;
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const T a = __shfl_up_sync(kFull, s0[b], o);
         const T c = __shfl_up_sync(kFull, s1[b], o);
-        if (take) {
-          s0[b] += a;
-          s1[b] += c;
-        }
+        s0[b] += take ? a : T(0);
+        s1[b] += take ? c : T(0);
       }
     }
     if (kt == carry_key)
@@ -202,81 +213,84 @@ struct SegRestrict {
         p1[b] = carry1[b];
       }
     }
-    if (kp == key[0])
-#pragma unroll
-      for (int e = 0; e < NV; ++e)
-        if (key[e] == key[0])
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            t0[b][e] += p0[b];
-            t1[b][e] += p1[b];
-          }
-    // run ends
-    int knext = __shfl_down_sync(kFull, key[0], 1);
-    if (lane == 31) knext = next_key;
-    bool end[NV];
-    int kmax = -1;
+    const bool head = kp == key[0];
 #pragma unroll
     for (int e = 0; e < NV; ++e) {
-      const int nk = e < NV - 1 ? key[e + 1] : knext;
-      end[e] = key[e] != INT_MAX && nk != key[e];
-      if (end[e]) kmax = key[e];
+      const bool add = head && key[e] == key[0];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        t0[b][e] += add ? p0[b] : T(0);
+        t1[b][e] += add ? p1[b] : T(0);
+      }
     }
+    // run ends, ranked across the warp
+    int knext = __shfl_down_sync(kFull, key[0], 1);
+    if (lane == 31) knext = next_key;
     carry_key = __shfl_sync(kFull, kt, 31);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       carry0[b] = __shfl_sync(kFull, s0[b], 31);
       carry1[b] = __shfl_sync(kFull, s1[b], 31);
     }
-    // fold: w0 runs into their key, then w1 runs into key + 1, then flush
+    const unsigned lt = (1u << lane) - 1u;
+    int r = 0, total = 0;
+    bool end[NV];
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      const int nk = e < NV - 1 ? key[e + 1] : knext;
+      end[e] = key[e] != INT_MAX && nk != key[e];
+      const unsigned bal = __ballot_sync(kFull, end[e]);
+      r += __popc(bal & lt);
+      total += __popc(bal);
+    }
 #pragma unroll
     for (int e = 0; e < NV; ++e)
-      if (end[e])
-#pragma unroll
-        for (int b = 0; b < NB; ++b) acc[b * RK + key[e] % RK] += t0[b][e];
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < NV; ++e)
-      if (end[e] && key[e] + 1 < nh)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) acc[b * RK + (key[e] + 1) % RK] += t1[b][e];
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < NV; ++e)
-      if (end[e])
+      if (end[e]) {
+        skey[r] = key[e];
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          T* slot = acc + b * RK + key[e] % RK;
-          out[b][key[e]] = *slot;
-          *slot = T(0);
+          st0[b * MAXE + r] = t0[b][e];
+          st1[b * MAXE + r] = t1[b][e];
         }
-    kflush = max(kflush, __reduce_max_sync(kFull, kmax));
+        ++r;
+      }
+    __syncwarp();
+    for (int q = lane; q < total; q += 32) {
+      const int K = skey[q];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const T pv = q > 0 ? st1[b * MAXE + q - 1] : prev1[b];
+        out[b][K] = pv + st0[b * MAXE + q];
+      }
+    }
+    if (total > 0) {
+      last_key = skey[total - 1];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) prev1[b] = st1[b * MAXE + total - 1];
+    }
     __syncwarp();
   }
 
-  // Flush the keys after the last w0 run (they hold w1 runs only) and zero
-  // the padded tail [nh, np).
+  // key last_key + 1 holds only the final run's w1 sum; the rest of [.., np) is zero
   __device__ __forceinline__ void finish(T* const (&out)[NB], int nh, int np, int lane) {
-    for (int k = kflush + 1 + lane; k < np; k += 32)
+    for (int k = last_key + 1 + lane; k < np; k += 32)
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (k < nh) {
-          T* slot = acc + b * RK + k % RK;
-          out[b][k] = *slot;
-          *slot = T(0);
-        } else {
-          out[b][k] = T(0);
-        }
-      }
-    __syncwarp();
+      for (int b = 0; b < NB; ++b) out[b][k] = (k == last_key + 1 && k < nh) ? prev1[b] : T(0);
   }
 };
+
+__host__ __device__ __forceinline__ int seg_scan_steps(int max_run, int nv) {
+  const int lanes = min(32, (max_run + 2 * nv - 2) / nv);  // lanes one run can touch
+  int s = 0;
+  while ((1 << s) < lanes) ++s;
+  return s;
+}
 
 // -------------------------------------------------------------------- ML-PCP
 enum RowModeW { kWStart = 0, kWUpdate = 1, kWOutput = 2 };
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(RW_THREADS)
+__global__ void __launch_bounds__(RW_THREADS, 3)
 pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __restrict__ D, int64_t ldd,
               const T* __restrict__ Yin, T* __restrict__ Yout, int64_t ldy, const T* __restrict__ Z,
               T* __restrict__ A, T* __restrict__ Lout, T* __restrict__ Sout, int64_t ldo, double* __restrict__ part) {
@@ -285,12 +299,15 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   constexpr int NV = Vec<T>::N, CH = 32 * NV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = ch.n, nh = ch.nh, np = ch.np;
+  const int* __restrict__ c0p = ch.c0;
+  const T* __restrict__ w0p = stencil_w0<T>(ch);
+  const T* __restrict__ w1p = stencil_w1<T>(ch);
+  const int steps = seg_scan_steps(ch.max_run, NV);
   const int zlen = round_up_dev(np + 2, 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* zrow = reinterpret_cast<T*>(smem_raw) + warp * (zlen + SR::RK);
-  T* ring = zrow + zlen;
-  for (int k = lane; k < SR::RK; k += 32) ring[k] = T(0);
-  __syncwarp();
+  unsigned char* wbase = smem_raw + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES);
+  T* zrow = reinterpret_cast<T*>(wbase);
+  unsigned char* stage = wbase + zlen * sizeof(T);
 
   const double mu_d = st->mu;
   const T inv = (T)(1.0 / mu_d);
@@ -308,16 +325,30 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
       __syncwarp();
     }
     const T* drow = D + i * ldd;
-    sr.begin(ring);
+    const T* yrow = Yin + i * ldy;
+    sr.begin(stage);
     T* const outp[1] = {A + i * np};
+    // one chunk of D (and Y) in flight ahead of the one being processed
+    T dn[NV], yn[NV];
+    load_vec<T, NV>(drow, lane * NV, n, vec, dn);
+    if (MODE != kWStart) load_vec<T, NV>(yrow, lane * NV, n, vec, yn);
     for (int cbase = 0; cbase < n; cbase += CH) {
       const int j = cbase + lane * NV;
-      StencilVec<T, NV> sv;
-      sv.load(ch, j);
       T dv[NV], yv[NV];
-      load_vec<T, NV>(drow, j, n, vec, dv);
-      if (MODE != kWStart) load_vec<T, NV>(Yin + i * ldy, j, n, vec, yv);
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        dv[e] = dn[e];
+        yv[e] = MODE != kWStart ? yn[e] : T(0);
+      }
+      if (cbase + CH < n) {
+        load_vec<T, NV>(drow, j + CH, n, vec, dn);
+        if (MODE != kWStart) load_vec<T, NV>(yrow, j + CH, n, vec, yn);
+      }
+      StencilVec<T, NV> sv;
+      sv.load(c0p, w0p, w1p, n, j);
       T x[1][NV], yo[NV], lo_v[NV], so_v[NV];
+      T c_res = T(0), c_l1 = T(0);
+      int c_nnz = 0;
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
         const T d = dv[e];
@@ -335,17 +366,20 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
           lo_v[e] = l;
           so_v[e] = s;
           if (MODE == kWUpdate) {
-            const T res = (d - l) - s;
-            const T yn = y + res * mu;
-            yo[e] = yn;
-            if (j + e < n) {
-              acc_res = fma((double)res, (double)res, acc_res);
-              acc_l1 += fabs((double)s);
-              acc_nnz += s != T(0) ? 1.0 : 0.0;
-            }
-            x[0][e] = yn * inv_next + d - s;
+            const T res = (d - l) - s;  // zero past n (d = l = s = 0 there)
+            const T ynew = y + res * mu;
+            yo[e] = ynew;
+            c_res = fma(res, res, c_res);
+            c_l1 += fabs(s);
+            c_nnz += s != T(0) ? 1 : 0;
+            x[0][e] = ynew * inv_next + d - s;
           }
         }
+      }
+      if (MODE == kWUpdate) {
+        acc_res += (double)c_res;
+        acc_l1 += (double)c_l1;
+        acc_nnz += (double)c_nnz;
       }
       if (MODE == kWOutput) {
         store_vec<T, NV>(Lout + i * ldo, j, n, vec, lo_v);
@@ -353,7 +387,7 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
         continue;
       }
       store_vec<T, NV>(Yout + i * ldy, j, n, vec, yo);
-      sr.chunk(sv, x, cbase + CH < n ? __ldg(ch.c0 + cbase + CH) : INT_MAX, outp, nh, lane);
+      sr.chunk(sv, x, cbase + CH < n ? __ldg(c0p + cbase + CH) : INT_MAX, outp, lane, steps);
     }
     if (MODE != kWOutput) sr.finish(outp, nh, np, lane);
     __syncwarp();
@@ -375,8 +409,8 @@ bool rows_warp_ok(const ChainDev& ch, bool) { return ch.keys_dense != 0; }
 int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy, void* Lout,
              void* Sout, int64_t ldo, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
-  const int nv = p->f32 ? 4 : 2;
-  const size_t smem = RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) + 64 * nv) * tb;
+  const size_t stage = p->f32 ? SegRestrict<float, 1, 4>::STAGE_BYTES : SegRestrict<double, 1, 2>::STAGE_BYTES;
+  const size_t smem = RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
   const int blocks = p->row_blocks;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
@@ -407,7 +441,7 @@ __device__ __forceinline__ void am_merge_w(AmRecW& a, const AmRecW& b) {
 enum CpModeW { kCWInit = 0, kCWUpdate = 1, kCWOutput = 2 };
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(RW_THREADS)
+__global__ void __launch_bounds__(RW_THREADS, 3)
 cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row0, int64_t m_global,
              const T* __restrict__ D, int64_t ldd, const uint32_t* __restrict__ mask, int64_t ldm, T* __restrict__ S,
              int64_t lds, T* __restrict__ LH, T* __restrict__ GH, T* __restrict__ SH, const double* __restrict__ u,
@@ -417,15 +451,18 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   constexpr int NV = Vec<T>::N, CH = 32 * NV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = ch.n, nh = ch.nh, np = ch.np;
+  const int* __restrict__ c0p = ch.c0;
+  const T* __restrict__ w0p = stencil_w0<T>(ch);
+  const T* __restrict__ w1p = stencil_w1<T>(ch);
+  const int steps = seg_scan_steps(ch.max_run, NV);
   const int zlen = round_up_dev(np + 2, 4);
   double* vs = reinterpret_cast<double*>(smem_raw);  // v (np), CTA-shared
-  unsigned char* p = smem_raw + round_up_dev(np * 8, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* lrow = reinterpret_cast<T*>(p) + warp * (zlen + 2 * SR::RK);
-  T* ring = lrow + zlen;
+  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES);
+  T* lrow = reinterpret_cast<T*>(wbase);
+  unsigned char* stage = wbase + zlen * sizeof(T);
   if (MODE == kCWUpdate)
     for (int k = threadIdx.x; k < np; k += blockDim.x) vs[k] = vg[k];
-  for (int k = lane; k < 2 * SR::RK; k += 32) ring[k] = T(0);
   __syncthreads();
 
   const double ga = MODE == kCWUpdate ? st->ga : 0.0;
@@ -438,7 +475,9 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   const int j_s = st->j_s;
   const T spike_add = (T)(gb * st->spike);
   double a_sq = 0.0, a_l1 = 0.0, a_nnz = 0.0, a_ss = 0.0, a_sr = 0.0;
-  AmRecW best{0.0, 0.0, 0.0, -1};
+  // arg-max |r| (ties: smallest column-major index); the index is formed only on ties
+  T bm = T(-1), bval = T(0), bsv = T(0);
+  long long bidx = -1;
   const bool vec = (ldd % NV == 0) && (lds % NV == 0) && (MODE != kCWOutput || ldl % NV == 0);
   SR sr;
 
@@ -461,12 +500,19 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
     const uint32_t* mrow = mask ? mask + i * ldm : nullptr;
     const long long gi = row0 + i;
     const bool spike_row = spike_on && gi == i_s;
-    sr.begin(ring);
+    sr.begin(stage);
     T* const outs[2] = {GH + i * np, SH + i * np};
+    T dn[NV], sn_[NV];
+    uint32_t bitn = 0xffffffffu;
+    if (MODE != kCWOutput) {
+      load_vec<T, NV>(drow, lane * NV, n, vec, dn);
+      if (MODE == kCWUpdate) load_vec_rw<T, NV>(sro, lane * NV, n, vec, sn_);
+      if (mrow && lane * NV < n) bitn = __ldg(mrow + ((lane * NV) >> 5)) >> ((lane * NV) & 31);
+    }
     for (int cbase = 0; cbase < n; cbase += CH) {
       const int j = cbase + lane * NV;
       StencilVec<T, NV> sv;
-      sv.load(ch, j);
+      sv.load(c0p, w0p, w1p, n, j);
       if (MODE == kCWOutput) {
         T lv[NV];
 #pragma unroll
@@ -477,49 +523,75 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
         store_vec<T, NV>(Lout + i * ldl, j, n, vec, lv);
         continue;
       }
-      T dv[NV], sv_old[NV];
-      load_vec<T, NV>(drow, j, n, vec, dv);
-      if (MODE == kCWUpdate) load_vec_rw<T, NV>(sro, j, n, vec, sv_old);
-      const uint32_t bits = mrow && j < n ? (__ldg(mrow + (j >> 5)) >> (j & 31)) : 0xffffffffu;
-      T x[2][NV];
+      T dv[NV], sold[NV];
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
-        const int jj = j + e;
-        const bool obs = (bits >> e) & 1u;
-        const T d = dv[e];
-        T r = T(0), sn = T(0);
-        if (MODE == kCWInit) {
-          r = obs ? -d : T(0);
-        } else {
+        dv[e] = dn[e];
+        sold[e] = MODE == kCWUpdate ? sn_[e] : T(0);
+      }
+      const uint32_t bits = bitn;
+      if (cbase + CH < n) {  // next chunk in flight
+        load_vec<T, NV>(drow, j + CH, n, vec, dn);
+        if (MODE == kCWUpdate) load_vec_rw<T, NV>(sro, j + CH, n, vec, sn_);
+        bitn = (mrow && j + CH < n) ? __ldg(mrow + ((j + CH) >> 5)) >> ((j + CH) & 31) : 0xffffffffu;
+      }
+      T x[2][NV];
+      if (MODE == kCWInit) {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          x[0][e] = ((bits >> e) & 1u) ? -dv[e] : T(0);  // r = -P[D]; zero past n
+          x[1][e] = T(0);
+        }
+      } else {
+        T sh[NV];
+#pragma unroll
+        for (int e = 0; e < NV; ++e) sh[e] = one_gb * sold[e];
+        if (spike_row) {
+#pragma unroll
+          for (int e = 0; e < NV; ++e)
+            if (j + e == j_s) sh[e] += spike_add;
+        }
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
           const int c = min(sv.key[e], np);
           const T l = sv.w0[e] * lrow[c] + sv.w1[e] * lrow[c + 1];
-          T sh = one_gb * sv_old[e];
-          if (spike_row && jj == j_s) sh += spike_add;
-          if (obs) {
-            const T rh = (l + sh) - d;         // r after the segment step
-            sn = soft_thr<T>(sh - rh, lam_s);  // cpcp.py:414-415
-            r = (l + sn) - d;
-          } else {
-            sn = soft_thr<T>(sh, lam_s);
-          }
-        }
-        if (jj >= n) r = sn = T(0);
-        x[0][e] = r;
-        x[1][e] = sn;
-        if (jj < n) {
-          const double rd = (double)r, sd = (double)sn;
-          a_sq = fma(rd, rd, a_sq);
-          a_l1 += fabs(sd);
-          a_nnz += sn != T(0) ? 1.0 : 0.0;
-          a_ss = fma(sd, sd, a_ss);
-          a_sr = fma(sd, rd, a_sr);
-          const double mg = fabs(rd);
-          const long long idx = (long long)jj * m_global + gi;
-          if (argmax_better(mg, idx, best.mag, best.idx)) best = AmRecW{mg, rd, sd, idx};
+          const T d = dv[e];
+          const bool obs = (bits >> e) & 1u;
+          const T rh = (l + sh[e]) - d;                       // r after the segment step
+          const T sn = soft_thr<T>(obs ? sh[e] - rh : sh[e], lam_s);  // cpcp.py:414-415
+          x[0][e] = obs ? (l + sn) - d : T(0);
+          x[1][e] = sn;
         }
       }
+      // statistics (per-chunk partials in T, then FP64) and the arg-max
+      T c_sq = T(0), c_l1 = T(0), c_ss = T(0), c_sr = T(0);
+      int c_nnz = 0;
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const T r = x[0][e], sn = x[1][e];
+        c_sq = fma(r, r, c_sq);
+        c_l1 += fabs(sn);
+        c_nnz += sn != T(0) ? 1 : 0;
+        c_ss = fma(sn, sn, c_ss);
+        c_sr = fma(sn, r, c_sr);
+        const T mg = fabs(r);
+        if (mg >= bm && j + e < n) {
+          const long long idx = (long long)(j + e) * m_global + gi;
+          if (mg > bm || idx < bidx) {
+            bm = mg;
+            bval = r;
+            bsv = sn;
+            bidx = idx;
+          }
+        }
+      }
+      a_sq += (double)c_sq;
+      a_l1 += (double)c_l1;
+      a_nnz += (double)c_nnz;
+      a_ss += (double)c_ss;
+      a_sr += (double)c_sr;
       if (MODE == kCWUpdate) store_vec<T, NV>(sro, j, n, vec, x[1]);
-      sr.chunk(sv, x, cbase + CH < n ? __ldg(ch.c0 + cbase + CH) : INT_MAX, outs, nh, lane);
+      sr.chunk(sv, x, cbase + CH < n ? __ldg(c0p + cbase + CH) : INT_MAX, outs, lane, steps);
     }
     if (MODE != kCWOutput) sr.finish(outs, nh, np, lane);
     __syncwarp();
@@ -529,6 +601,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   __shared__ AmRecW amw[RW_WARPS];
   double vals[5] = {a_sq, a_l1, a_nnz, a_ss, a_sr};
   block_sum<5>(vals, scratch);
+  AmRecW best{bidx >= 0 ? (double)bm : 0.0, (double)bval, (double)bsv, bidx};
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     AmRecW b;
@@ -555,9 +628,8 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
 int cp_rows(CpcpPlan* p, int mode, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S,
             int64_t lds, void* Lout, int64_t ldl, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
-  const int nv = p->f32 ? 4 : 2;
-  const size_t smem = (size_t)round_up(p->ch.np * 8, 16) +
-                      RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) + 2 * 64 * nv) * tb;
+  const size_t stage = p->f32 ? SegRestrict<float, 2, 4>::STAGE_BYTES : SegRestrict<double, 2, 2>::STAGE_BYTES;
+  const size_t smem = (size_t)round_up(p->ch.np * 8, 16) + RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
   const int blocks = p->row_blocks;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
