@@ -130,7 +130,7 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   int64_t splits = ceil_div(2 * sms, tiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
-  const int64_t col_blocks = ceil_div(ch.n, 128);
+  const int64_t col_blocks = ceil_div(ch.n, 2048);  // lz_dtv_kernel tiles: row blocks x 2048 columns
   int64_t ls = ceil_div(2 * sms, col_blocks);
   ls = std::min<int64_t>(ls, std::max<int64_t>(1, m_local / 32));
   p.lz_splits = (int)std::max<int64_t>(1, ls);

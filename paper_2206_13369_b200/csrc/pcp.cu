@@ -100,34 +100,102 @@ __global__ void lz_init_kernel(LanczosDev* lz, double* Q, int n, int kmax) {
   }
 }
 
+// t = D q (warp per row; 16-byte loads of D, FP64 q from L2, FP64 sums).
 template <typename T>
-__global__ void lz_dv_kernel(const LanczosDev* __restrict__ lz, const T* __restrict__ D, int64_t ldd,
-                             int64_t m, int n, const double* __restrict__ Q, double* __restrict__ t) {
+__global__ void __launch_bounds__(256) lz_dv_kernel(const LanczosDev* __restrict__ lz, const T* __restrict__ D,
+                                                    int64_t ldd, int64_t m, int n, const double* __restrict__ Q,
+                                                    double* __restrict__ t) {
   if (lz->done) return;
-  __shared__ double scratch[32];
-  const double* q = Q + (int64_t)lz->k * n;
-  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+  const double* __restrict__ q = Q + (int64_t)lz->k * n;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int NV = 16 / sizeof(T);
+  const bool vec = (n % NV == 0) && (ldd % NV == 0);
+  for (int64_t i = w0; i < m; i += nw) {
     const T* row = D + i * ldd;
-    double s = 0.0;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) s = fma((double)row[j], q[j], s);
-    double v[1] = {s};
-    block_sum<1>(v, scratch);
-    if (threadIdx.x == 0) t[i] = v[0];
+    double s0 = 0.0, s1 = 0.0;
+    if (vec) {
+      int j = lane * NV;
+      for (; j + 32 * NV < n; j += 64 * NV) {  // two vectors in flight
+        T a[NV], b[NV];
+        *reinterpret_cast<float4*>(a) = __ldg(reinterpret_cast<const float4*>(row + j));
+        *reinterpret_cast<float4*>(b) = __ldg(reinterpret_cast<const float4*>(row + j + 32 * NV));
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          s0 = fma((double)a[e], __ldg(q + j + e), s0);
+          s1 = fma((double)b[e], __ldg(q + j + 32 * NV + e), s1);
+        }
+      }
+      if (j < n) {
+        T a[NV];
+        *reinterpret_cast<float4*>(a) = __ldg(reinterpret_cast<const float4*>(row + j));
+#pragma unroll
+        for (int e = 0; e < NV; ++e) s0 = fma((double)a[e], __ldg(q + j + e), s0);
+      }
+    } else {
+      for (int j = lane; j < n; j += 32) s0 = fma((double)row[j], q[j], s0);
+    }
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) t[i] = s;
   }
 }
 
+// Partial w = D^T t over a tile of rows x 2048 columns: thread owns 8
+// consecutive columns (16-byte loads), 2 rows in flight; FP64 partials
+// wpart[row block][j], summed by sum_slices (deterministic).
+constexpr int LZ_COLS = 2048;
 template <typename T>
-__global__ void lz_dtv_kernel(const LanczosDev* __restrict__ lz, const T* __restrict__ D, int64_t ldd,
-                              int64_t m, int n, const double* __restrict__ t, double* __restrict__ wpart,
-                              int64_t rows_per_split) {
+__global__ void __launch_bounds__(256) lz_dtv_kernel(const LanczosDev* __restrict__ lz, const T* __restrict__ D,
+                                                     int64_t ldd, int64_t m, int n, const double* __restrict__ t,
+                                                     double* __restrict__ wpart, int64_t rows_per_split) {
   if (lz->done) return;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.x * LZ_COLS + threadIdx.x * 8;
   const int64_t r0 = blockIdx.y * rows_per_split;
   const int64_t r1 = min(m, r0 + rows_per_split);
-  if (j >= n) return;
-  double s = 0.0;
-  for (int64_t i = r0; i < r1; ++i) s = fma((double)D[i * ldd + j], t[i], s);
-  wpart[(int64_t)blockIdx.y * n + j] = s;
+  if (j0 >= n) return;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  constexpr int NV = 16 / sizeof(T);
+  const bool vec = (j0 + 8 <= n) && (n % NV == 0) && (ldd % NV == 0);
+  if (vec) {
+    int64_t i = r0;
+    for (; i + 1 < r1; i += 2) {
+      T a[8], b[8];
+      const T* ra = D + i * ldd + j0;
+      const T* rb = ra + ldd;
+#pragma unroll
+      for (int v = 0; v < 8 / NV; ++v) {
+        *reinterpret_cast<float4*>(a + v * NV) = __ldg(reinterpret_cast<const float4*>(ra + v * NV));
+        *reinterpret_cast<float4*>(b + v * NV) = __ldg(reinterpret_cast<const float4*>(rb + v * NV));
+      }
+      const double ta = __ldg(t + i), tb = __ldg(t + i + 1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fma((double)b[e], tb, fma((double)a[e], ta, acc[e]));
+    }
+    if (i < r1) {
+      T a[8];
+      const T* ra = D + i * ldd + j0;
+#pragma unroll
+      for (int v = 0; v < 8 / NV; ++v)
+        *reinterpret_cast<float4*>(a + v * NV) = __ldg(reinterpret_cast<const float4*>(ra + v * NV));
+      const double ta = __ldg(t + i);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fma((double)a[e], ta, acc[e]);
+    }
+  } else {
+    for (int64_t i = r0; i < r1; ++i) {
+      const double ti = t[i];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (j0 + e < n) acc[e] = fma((double)D[i * ldd + j0 + e], ti, acc[e]);
+    }
+  }
+  double* o = wpart + (int64_t)blockIdx.y * n + j0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (j0 + e < n) o[e] = acc[e];
 }
 
 // True if the symmetric tridiagonal (a[0..k1), b[0..k1-1)) has an eigenvalue
@@ -386,10 +454,14 @@ __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double
     tb[k] = beta;
   }
   __syncthreads();
-  const double th = tridiag_max_eig_block(ta, tb, K);
+  // the largest Ritz value (multisection) only every 4th step: it only
+  // feeds the stopping test, and the Sturm counts dominate this kernel
+  const bool close = lz->theta > 0.0 && fabs(lz->theta - lz->theta_prev) <= 1e-6 * lz->theta;
+  const bool eval = close || (k % 4 == 3) || k + 1 >= lz->kmax || beta <= 1e-300;
+  const double th = eval ? tridiag_max_eig_block(ta, tb, K) : lz->theta;
   const double rel = lz->theta > 0.0 ? fabs(th - lz->theta) / th : 1.0;
-  const int stable = (rel <= tol) ? lz->stable + 1 : 0;
-  const bool stop = (stable >= 2 && k >= 3) || beta <= 1e-300 * fmax(th, 1e-300) || k + 1 >= lz->kmax;
+  const int stable = !eval ? lz->stable : ((rel <= tol) ? lz->stable + 1 : 0);
+  const bool stop = (eval && stable >= 2 && k >= 3) || beta <= 1e-300 * fmax(th, 1e-300) || k + 1 >= lz->kmax;
   if (!stop) {
     double* qn = Q + (int64_t)(k + 1) * n + j0;
     const double inv = 1.0 / beta;
@@ -399,8 +471,10 @@ __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double
   if (r == 0 && tid == 0) {
     lz->alpha[k] = alpha;
     lz->beta[k] = beta;
-    lz->theta_prev = lz->theta;
-    lz->theta = th;
+    if (eval) {
+      lz->theta_prev = lz->theta;
+      lz->theta = th;
+    }
     lz->stable = stable;
     if (stop) {
       lz->done = 1;
@@ -669,7 +743,7 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
     return kOk;
   }
   p->timer.begin(st);
-  int blocks = p->row_blocks;
+  const int blocks = (int)std::min<int64_t>(ceil_div(m, 8), (int64_t)p->row_blocks);
   if (p->f32)
     lz_dv_kernel<float><<<blocks, 256, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzQ, p->lzT);
   else
@@ -677,11 +751,11 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
   MLR_LAUNCH_CHECK("lz_dv_kernel");
   int splits = p->lz_splits;
   int64_t rps = ceil_div(m, splits);
-  dim3 grid((unsigned)ceil_div(n, 128), (unsigned)splits);
+  dim3 grid((unsigned)ceil_div(n, LZ_COLS), (unsigned)splits);
   if (p->f32)
-    lz_dtv_kernel<float><<<grid, 128, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzT, p->lzW, rps);
+    lz_dtv_kernel<float><<<grid, 256, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzT, p->lzW, rps);
   else
-    lz_dtv_kernel<double><<<grid, 128, 0, st>>>(p->lz, (const double*)D, ldd, m, n, p->lzT, p->lzW, rps);
+    lz_dtv_kernel<double><<<grid, 256, 0, st>>>(p->lz, (const double*)D, ldd, m, n, p->lzT, p->lzW, rps);
   MLR_LAUNCH_CHECK("lz_dtv_kernel");
   const int rc = sum_slices(p->lzW, n, n, splits, wpart_out, st);
   p->timer.end(kPhLanczos, st);
