@@ -95,6 +95,38 @@ __device__ __forceinline__ void store_vec(T* p, int j, int n, bool vec, const T 
   }
 }
 
+// Per-lane asynchronous staging of the row chunks a warp will process
+// (cp.async, 16 bytes per lane per stream, RING_ST chunks deep, continuing
+// across the warp's rows): several chunks of D / Y / S and the mask word are
+// in flight without holding registers.  Each lane reads back only the bytes
+// it copied, so cp.async.wait_group alone orders the data.
+constexpr int RING_ST = 4;
+constexpr int RING_BYTES = RING_ST * (2 * 512 + 128);  // per warp: 2 streams + the mask word
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+struct LaneRing {
+  unsigned char* base;
+  __device__ __forceinline__ unsigned char* slot(int s, int q, int lane) const {
+    return base + ((s * 2 + q) * 32 + lane) * 16;
+  }
+  __device__ __forceinline__ uint32_t* mslot(int s, int lane) const {
+    return reinterpret_cast<uint32_t*>(base + RING_ST * 1024 + (s * 32 + lane) * 4);
+  }
+};
+
 // Stencil of NV consecutive fine columns; key = INT_MAX past n.
 template <typename T, int NV>
 struct StencilVec {
@@ -289,7 +321,7 @@ __host__ __device__ __forceinline__ int seg_scan_steps(int max_run, int nv) {
 // -------------------------------------------------------------------- ML-PCP
 enum RowModeW { kWStart = 0, kWUpdate = 1, kWOutput = 2 };
 
-template <typename T, int MODE>
+template <typename T, int MODE, bool RING>
 __global__ void __launch_bounds__(RW_THREADS, 3)
 pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __restrict__ D, int64_t ldd,
               const T* __restrict__ Yin, T* __restrict__ Yout, int64_t ldy, const T* __restrict__ Z,
@@ -305,9 +337,10 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   const int steps = seg_scan_steps(ch.max_run, NV);
   const int zlen = round_up_dev(np + 2, 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES);
+  unsigned char* wbase = smem_raw + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES + (RING ? RING_BYTES : 0));
   T* zrow = reinterpret_cast<T*>(wbase);
   unsigned char* stage = wbase + zlen * sizeof(T);
+  const LaneRing ring{stage + SR::STAGE_BYTES};
 
   const double mu_d = st->mu;
   const T inv = (T)(1.0 / mu_d);
@@ -317,9 +350,32 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   const double scale = st->scale;
   double acc_res = 0.0, acc_l1 = 0.0, acc_nnz = 0.0;
   const bool vec = (ldd % NV == 0) && (ldy % NV == 0) && (MODE != kWOutput || ldo % NV == 0);
+  const bool pipe = RING && vec;
   SR sr;
+  const int nc = (n + CH - 1) / CH;
+  const int64_t first = (int64_t)blockIdx.x * RW_WARPS + warp, stride = (int64_t)gridDim.x * RW_WARPS;
+  // prefetch cursor: (row, chunk, ring slot) of the next chunk to stage
+  int64_t irow = first;
+  int ic = 0, isl = 0;
+  auto issue = [&]() {
+    if (irow < m) {
+      const int jq = ic * CH + lane * NV;
+      const int bytes = jq < n ? min(16, (n - jq) * (int)sizeof(T)) : 0;
+      cp_async16(ring.slot(isl, 0, lane), D + irow * ldd + (bytes ? jq : 0), bytes);
+      if (MODE != kWStart) cp_async16(ring.slot(isl, 1, lane), Yin + irow * ldy + (bytes ? jq : 0), bytes);
+    }
+    cp_commit();
+    isl = (isl + 1) & (RING_ST - 1);
+    if (++ic == nc) {
+      ic = 0;
+      irow += stride;
+    }
+  };
+  if (pipe)
+    for (int q = 0; q < RING_ST - 1; ++q) issue();
+  int csl = 0;  // ring slot of the chunk being processed
 
-  for (int64_t i = (int64_t)blockIdx.x * RW_WARPS + warp; i < m; i += (int64_t)gridDim.x * RW_WARPS) {
+  for (int64_t i = first; i < m; i += stride) {
     if (MODE != kWStart) {
       for (int k = lane; k < zlen; k += 32) zrow[k] = k < np ? Z[i * np + k] : T(0);
       __syncwarp();
@@ -328,21 +384,36 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
     const T* yrow = Yin + i * ldy;
     sr.begin(stage);
     T* const outp[1] = {A + i * np};
-    // one chunk of D (and Y) in flight ahead of the one being processed
-    T dn[NV], yn[NV];
-    load_vec<T, NV>(drow, lane * NV, n, vec, dn);
-    if (MODE != kWStart) load_vec<T, NV>(yrow, lane * NV, n, vec, yn);
-    for (int cbase = 0; cbase < n; cbase += CH) {
+    T dn[NV], yn[NV];  // register path: one chunk in flight
+    if (!pipe) {
+      load_vec<T, NV>(drow, lane * NV, n, vec, dn);
+      if (MODE != kWStart) load_vec<T, NV>(yrow, lane * NV, n, vec, yn);
+    }
+    for (int c = 0; c < nc; ++c) {
+      const int cbase = c * CH;
       const int j = cbase + lane * NV;
       T dv[NV], yv[NV];
+      if (pipe) {
+        issue();
+        cp_wait<RING_ST - 1>();
+        const int sl = csl;
+        csl = (csl + 1) & (RING_ST - 1);
+        Vec<T>::unpack(*reinterpret_cast<const typename Vec<T>::V*>(ring.slot(sl, 0, lane)), dv);
+        if (MODE != kWStart)
+          Vec<T>::unpack(*reinterpret_cast<const typename Vec<T>::V*>(ring.slot(sl, 1, lane)), yv);
+        else
 #pragma unroll
-      for (int e = 0; e < NV; ++e) {
-        dv[e] = dn[e];
-        yv[e] = MODE != kWStart ? yn[e] : T(0);
-      }
-      if (cbase + CH < n) {
-        load_vec<T, NV>(drow, j + CH, n, vec, dn);
-        if (MODE != kWStart) load_vec<T, NV>(yrow, j + CH, n, vec, yn);
+          for (int e = 0; e < NV; ++e) yv[e] = T(0);
+      } else {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          dv[e] = dn[e];
+          yv[e] = MODE != kWStart ? yn[e] : T(0);
+        }
+        if (cbase + CH < n) {
+          load_vec<T, NV>(drow, j + CH, n, vec, dn);
+          if (MODE != kWStart) load_vec<T, NV>(yrow, j + CH, n, vec, yn);
+        }
       }
       StencilVec<T, NV> sv;
       sv.load(c0p, w0p, w1p, n, j);
@@ -392,6 +463,7 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
     if (MODE != kWOutput) sr.finish(outp, nh, np, lane);
     __syncwarp();
   }
+  cp_wait<0>();
   if (MODE == kWUpdate) {
     __shared__ double scratch[3 * 32];
     double v[3] = {acc_res, acc_l1, acc_nnz};
@@ -410,11 +482,14 @@ int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, 
              void* Sout, int64_t ldo, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
   const size_t stage = p->f32 ? SegRestrict<float, 1, 4>::STAGE_BYTES : SegRestrict<double, 1, 2>::STAGE_BYTES;
-  const size_t smem = RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
+  // the cp.async ring only while 3 CTAs per SM still fit (occupancy first)
+  const size_t base = RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
+  const bool ring = base + RW_WARPS * RING_BYTES <= 80 * 1024;
+  const size_t smem = base + (ring ? RW_WARPS * RING_BYTES : 0);
   const int blocks = p->row_blocks;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
-    auto kern = pcp_rows_warp<T, MODE>;                                                                         \
+    auto kern = ring ? pcp_rows_warp<T, MODE, true> : pcp_rows_warp<T, MODE, false>;                                                                         \
     MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
     kern<<<blocks, RW_THREADS, smem, st>>>(p->dev, p->ch, p->m_local, (const T*)D, ldd, (const T*)Yin, (T*)Yout, \
                                            ldy, (const T*)p->Z, (T*)p->A, (T*)Lout, (T*)Sout, ldo, p->row_part); \
@@ -440,7 +515,7 @@ __device__ __forceinline__ void am_merge_w(AmRecW& a, const AmRecW& b) {
 
 enum CpModeW { kCWInit = 0, kCWUpdate = 1, kCWOutput = 2 };
 
-template <typename T, int MODE>
+template <typename T, int MODE, bool RING>
 __global__ void __launch_bounds__(RW_THREADS, 3)
 cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row0, int64_t m_global,
              const T* __restrict__ D, int64_t ldd, const uint32_t* __restrict__ mask, int64_t ldm, T* __restrict__ S,
@@ -458,9 +533,11 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   const int zlen = round_up_dev(np + 2, 4);
   double* vs = reinterpret_cast<double*>(smem_raw);  // v (np), CTA-shared
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES);
+  unsigned char* wbase =
+      smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES + (RING ? RING_BYTES : 0));
   T* lrow = reinterpret_cast<T*>(wbase);
   unsigned char* stage = wbase + zlen * sizeof(T);
+  const LaneRing ring{stage + SR::STAGE_BYTES};
   if (MODE == kCWUpdate)
     for (int k = threadIdx.x; k < np; k += blockDim.x) vs[k] = vg[k];
   __syncthreads();
@@ -480,8 +557,31 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   long long bidx = -1;
   const bool vec = (ldd % NV == 0) && (lds % NV == 0) && (MODE != kCWOutput || ldl % NV == 0);
   SR sr;
+  const int nc = (n + CH - 1) / CH;
+  const int64_t first = (int64_t)blockIdx.x * RW_WARPS + warp, stride = (int64_t)gridDim.x * RW_WARPS;
+  const bool pipe = RING && vec && MODE != kCWOutput;
+  int64_t irow = first;
+  int ic = 0, isl = 0;
+  auto issue = [&]() {  // stage the next chunk of this warp's (row, chunk) sequence
+    if (irow < m) {
+      const int jq = ic * CH + lane * NV;
+      const int bytes = jq < n ? min(16, (n - jq) * (int)sizeof(T)) : 0;
+      cp_async16(ring.slot(isl, 0, lane), D + irow * ldd + (bytes ? jq : 0), bytes);
+      if (MODE == kCWUpdate) cp_async16(ring.slot(isl, 1, lane), S + irow * lds + (bytes ? jq : 0), bytes);
+      if (mask) cp_async4(ring.mslot(isl, lane), mask + irow * ldm + (jq < n ? (jq >> 5) : 0), jq < n ? 4 : 0);
+    }
+    cp_commit();
+    isl = (isl + 1) & (RING_ST - 1);
+    if (++ic == nc) {
+      ic = 0;
+      irow += stride;
+    }
+  };
+  if (pipe)
+    for (int q = 0; q < RING_ST - 1; ++q) issue();
+  int csl = 0;
 
-  for (int64_t i = (int64_t)blockIdx.x * RW_WARPS + warp; i < m; i += (int64_t)gridDim.x * RW_WARPS) {
+  for (int64_t i = first; i < m; i += stride) {
     T* lhrow = LH + i * np;
     if (MODE == kCWUpdate) {
       // coarse rank-1 update L_H <- (1-ga) L_H + ga * coef * u_i v^T (cpcp.py:399-402)
@@ -502,14 +602,15 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
     const bool spike_row = spike_on && gi == i_s;
     sr.begin(stage);
     T* const outs[2] = {GH + i * np, SH + i * np};
-    T dn[NV], sn_[NV];
+    T dn[NV], sn_[NV];  // register path: one chunk in flight
     uint32_t bitn = 0xffffffffu;
-    if (MODE != kCWOutput) {
+    if (!pipe && MODE != kCWOutput) {
       load_vec<T, NV>(drow, lane * NV, n, vec, dn);
       if (MODE == kCWUpdate) load_vec_rw<T, NV>(sro, lane * NV, n, vec, sn_);
-      if (mrow && lane * NV < n) bitn = __ldg(mrow + ((lane * NV) >> 5)) >> ((lane * NV) & 31);
+      bitn = mrow ? (lane * NV < n ? __ldg(mrow + ((lane * NV) >> 5)) >> ((lane * NV) & 31) : 0u) : 0xffffffffu;
     }
-    for (int cbase = 0; cbase < n; cbase += CH) {
+    for (int c = 0; c < nc; ++c) {
+      const int cbase = c * CH;
       const int j = cbase + lane * NV;
       StencilVec<T, NV> sv;
       sv.load(c0p, w0p, w1p, n, j);
@@ -524,16 +625,31 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
         continue;
       }
       T dv[NV], sold[NV];
+      uint32_t bits = 0xffffffffu;
+      if (pipe) {
+        issue();
+        cp_wait<RING_ST - 1>();
+        const int sl = csl;
+        csl = (csl + 1) & (RING_ST - 1);
+        Vec<T>::unpack(*reinterpret_cast<const typename Vec<T>::V*>(ring.slot(sl, 0, lane)), dv);
+        if (MODE == kCWUpdate)
+          Vec<T>::unpack(*reinterpret_cast<const typename Vec<T>::V*>(ring.slot(sl, 1, lane)), sold);
+        else
 #pragma unroll
-      for (int e = 0; e < NV; ++e) {
-        dv[e] = dn[e];
-        sold[e] = MODE == kCWUpdate ? sn_[e] : T(0);
-      }
-      const uint32_t bits = bitn;
-      if (cbase + CH < n) {  // next chunk in flight
-        load_vec<T, NV>(drow, j + CH, n, vec, dn);
-        if (MODE == kCWUpdate) load_vec_rw<T, NV>(sro, j + CH, n, vec, sn_);
-        bitn = (mrow && j + CH < n) ? __ldg(mrow + ((j + CH) >> 5)) >> ((j + CH) & 31) : 0xffffffffu;
+          for (int e = 0; e < NV; ++e) sold[e] = T(0);
+        if (mrow) bits = j < n ? (*ring.mslot(sl, lane) >> (j & 31)) : 0u;
+      } else {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          dv[e] = dn[e];
+          sold[e] = MODE == kCWUpdate ? sn_[e] : T(0);
+        }
+        bits = bitn;
+        if (cbase + CH < n) {
+          load_vec<T, NV>(drow, j + CH, n, vec, dn);
+          if (MODE == kCWUpdate) load_vec_rw<T, NV>(sro, j + CH, n, vec, sn_);
+          bitn = mrow ? (j + CH < n ? __ldg(mrow + ((j + CH) >> 5)) >> ((j + CH) & 31) : 0u) : 0xffffffffu;
+        }
       }
       T x[2][NV];
       if (MODE == kCWInit) {
@@ -596,6 +712,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
     if (MODE != kCWOutput) sr.finish(outs, nh, np, lane);
     __syncwarp();
   }
+  cp_wait<0>();
   if (MODE == kCWOutput) return;
   __shared__ double scratch[5 * 32];
   __shared__ AmRecW amw[RW_WARPS];
@@ -629,11 +746,13 @@ int cp_rows(CpcpPlan* p, int mode, const void* D, int64_t ldd, const uint32_t* m
             int64_t lds, void* Lout, int64_t ldl, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
   const size_t stage = p->f32 ? SegRestrict<float, 2, 4>::STAGE_BYTES : SegRestrict<double, 2, 2>::STAGE_BYTES;
-  const size_t smem = (size_t)round_up(p->ch.np * 8, 16) + RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
+  const size_t base = (size_t)round_up(p->ch.np * 8, 16) + RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
+  const bool ring = base + RW_WARPS * RING_BYTES <= 80 * 1024;
+  const size_t smem = base + (ring ? RW_WARPS * RING_BYTES : 0);
   const int blocks = p->row_blocks;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
-    auto kern = cp_rows_warp<T, MODE>;                                                                          \
+    auto kern = ring ? cp_rows_warp<T, MODE, true> : cp_rows_warp<T, MODE, false>;                                                                          \
     MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
     kern<<<blocks, RW_THREADS, smem, st>>>(p->dev, p->ch, p->m_local, p->row0, p->m_global, (const T*)D, ldd,    \
                                            mask, ldm, (T*)S, lds, (T*)p->LH, (T*)p->GH, (T*)p->SH, p->u, p->v, \
