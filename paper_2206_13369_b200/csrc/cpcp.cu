@@ -199,24 +199,35 @@ cp_row_kernel(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t ro
 
 // Reduce per-CTA partials: stats -> out[0..5), arg-max record -> am[0..4)
 // as (mag, val, sval, idx).
-__global__ void cp_part_reduce(const double* __restrict__ part, int nparts, double* __restrict__ out,
-                               double* __restrict__ am) {
-  if (threadIdx.x < kCpStats) {
-    double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += part[9 * b + threadIdx.x];
-    out[threadIdx.x] = s;
+// Sum the per-CTA stats and merge the arg-max records (256 threads; fixed
+// summation order; the arg-max merge is a total order, so order-free).
+__global__ void __launch_bounds__(256) cp_part_reduce(const double* __restrict__ part, int nparts,
+                                                      double* __restrict__ out, double* __restrict__ am) {
+  __shared__ double scratch[kCpStats * 32];
+  __shared__ AmRec amw[8];
+  double v[kCpStats];
+#pragma unroll
+  for (int q = 0; q < kCpStats; ++q) v[q] = 0.0;
+  AmRec b{0.0, 0.0, 0.0, -1};
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+    const double* p = part + 9 * i;
+#pragma unroll
+    for (int q = 0; q < kCpStats; ++q) v[q] += p[q];
+    am_merge(b, AmRec{p[5], p[6], p[7], (long long)p[8]});
   }
-  if (threadIdx.x == 32) {
-    AmRec b{0.0, 0.0, 0.0, -1};
-    for (int q = 0; q < nparts; ++q) {
-      const double* p = part + 9 * q;
-      AmRec c{p[5], p[6], p[7], (long long)p[8]};
-      am_merge(b, c);
-    }
-    am[0] = b.mag;
-    am[1] = b.val;
-    am[2] = b.sval;
-    am[3] = (double)b.idx;
+  block_sum<kCpStats>(v, scratch);
+  b = am_warp(b);
+  if ((threadIdx.x & 31) == 0) amw[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < kCpStats; ++q) out[q] = v[q];
+    AmRec r = amw[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) am_merge(r, amw[w]);
+    am[0] = r.mag;
+    am[1] = r.val;
+    am[2] = r.sval;
+    am[3] = (double)r.idx;
   }
 }
 
@@ -461,13 +472,21 @@ cp_dots_kernel(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t r
   }
 }
 
-__global__ void cp_dots_reduce(const double* __restrict__ part, int nparts, double* __restrict__ out,
-                               const CpcpDev* __restrict__ st) {
+__global__ void __launch_bounds__(256) cp_dots_reduce(const double* __restrict__ part, int nparts,
+                                                      double* __restrict__ out, const CpcpDev* __restrict__ st) {
   if (st->done) return;
-  if (threadIdx.x < 3) {
-    double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += part[3 * b + threadIdx.x];
-    out[threadIdx.x] = s;
+  __shared__ double scratch[3 * 32];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+    v[0] += part[3 * i];
+    v[1] += part[3 * i + 1];
+    v[2] += part[3 * i + 2];
+  }
+  block_sum<3>(v, scratch);
+  if (threadIdx.x == 0) {
+    out[0] = v[0];
+    out[1] = v[1];
+    out[2] = v[2];
   }
 }
 
@@ -628,7 +647,7 @@ int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st) {
     if (rc) return rc;
     rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);
     if (rc) return rc;
-    cp_part_reduce<<<1, 64, 0, st>>>(p->row_part, p->row_blocks, red + nn, amax);
+    cp_part_reduce<<<1, 256, 0, st>>>(p->row_part, p->row_blocks, red + nn, amax);
     MLR_LAUNCH_CHECK("cp_part_reduce");
   } else {
     MLR_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * (nn + kCpStats), st));
@@ -677,7 +696,7 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   if (p->m_local > 0 && (size_t)p->ch.np * 16 + 8 * (size_t)(p->ch.np + 2) * 8 <= 200 * 1024) {
     const int rc = cp_dots_rows(p, st);
     if (rc) return rc;
-    cp_dots_reduce<<<1, 32, 0, st>>>(p->dots_part, p->row_blocks, dots, p->dev);
+    cp_dots_reduce<<<1, 256, 0, st>>>(p->dots_part, p->row_blocks, dots, p->dev);
     MLR_LAUNCH_CHECK("cp_dots_reduce");
   } else if (p->m_local > 0) {
     const int blocks = p->row_blocks;
@@ -690,7 +709,7 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
                                                      (const double*)p->LH, (const double*)p->GH,
                                                      (const double*)p->SH, p->v, p->vin, p->u, p->dots_part);
     MLR_LAUNCH_CHECK("cp_dots_kernel");
-    cp_dots_reduce<<<1, 32, 0, st>>>(p->dots_part, blocks, dots, p->dev);
+    cp_dots_reduce<<<1, 256, 0, st>>>(p->dots_part, blocks, dots, p->dev);
     MLR_LAUNCH_CHECK("cp_dots_reduce");
   } else {
     MLR_CUDA(cudaMemsetAsync(dots, 0, 3 * sizeof(double), st));
