@@ -126,7 +126,7 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   p.max_iters = max_iters;
   const int sms = sm_count();
   p.row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m_local, (int64_t)sms * 8));
-  const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64);
+  const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64 + 1) / 2;  // symmetric Gram: upper-triangle tiles
   int64_t splits = ceil_div(2 * sms, tiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
@@ -169,7 +169,7 @@ static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_
   p.world = world;
   const int sms = sm_count();
   p.row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m_local, (int64_t)sms * 8));
-  const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64);
+  const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64 + 1) / 2;  // symmetric Gram: upper-triangle tiles
   int64_t splits = ceil_div(2 * sms, tiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);

@@ -643,6 +643,7 @@ int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st) {
     g.B = p->GH; g.ldb = np; g.b_f32 = p->f32; g.trans_b = false;
     g.C = p->gram_part; g.ldc = np; g.c_f32 = false; g.c_slice = nn; g.splits = p->gram_splits; g.alpha = 1.0;
     g.skip = &p->dev->done;
+    g.sym = true;  // Gram: upper-triangle tiles, mirrored
     int rc = gemm_f64(g, st);
     if (rc) return rc;
     rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);

@@ -24,6 +24,7 @@ struct GemmSpec {
   double alpha;
   const double* kscale;  // optional: op(A)[:, k] *= kscale[k]
   const int* skip;       // optional device flag: kernel is a no-op when *skip != 0
+  bool sym;              // C = op(A) op(B) is symmetric (Gram): upper-triangle tiles, mirrored
 };
 int gemm_f64(GemmSpec g, cudaStream_t st);
 int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st);

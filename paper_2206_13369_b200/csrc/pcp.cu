@@ -814,6 +814,7 @@ int pcp_gram(PcpPlan* p, double* red, int with_stats, cudaStream_t st) {
     g.B = p->A; g.ldb = np; g.b_f32 = p->f32; g.trans_b = false;
     g.C = p->gram_part; g.ldc = np; g.c_f32 = false; g.c_slice = nn; g.splits = p->gram_splits; g.alpha = 1.0;
     g.kscale = nullptr; g.skip = nullptr;
+    g.sym = true;  // Gram: upper-triangle tiles, mirrored
     int rc = gemm_f64(g, st);
     if (rc) return rc;
     rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);
