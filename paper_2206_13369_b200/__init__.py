@@ -20,6 +20,6 @@ from .api_types import (  # noqa: F401
     SvdError,
 )
 from .chain import LevelError, build_chain, coarse_sizes, select_levels  # noqa: F401
-from .cpcp import ml_fwt_solve, ml_fwt_solve_rows  # noqa: F401
+from .cpcp import fwt_solve, ml_fwt_solve, ml_fwt_solve_rows  # noqa: F401
 from .ops import eigh_psd, prolong, restrict  # noqa: F401
 from .pcp import ml_ialm_solve, ml_ialm_solve_rows  # noqa: F401

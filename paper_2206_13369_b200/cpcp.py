@@ -9,6 +9,7 @@ and the 5-iteration convergence window all run on the device.
 
 from __future__ import annotations
 
+import dataclasses
 import warnings
 
 import numpy as np
@@ -116,6 +117,20 @@ def ml_fwt_solve(d, mask=None, opts=None):
     return _state_from(*out, kind)
 
 
+def fwt_solve(d, mask=None, opts=None):
+    """Full-width Frank-Wolfe thresholding (drop-in for mlrpca.fwt_solve,
+    reference cpcp.py:459-477): the nuclear-ball linear minimisation step uses the leading
+    singular triple of the full gradient.  It is the same device loop as
+    ``ml_fwt_solve`` on the identity chain (R = I, radius 1), which the
+    reference itself reproduces bit for bit (ml_fwt_solve with levels = n)."""
+    if opts is None:
+        raise ValueError("CpcpOptions with penalty weights is required")
+    D, _ = as_device_matrix(d, "d")
+    n = D.shape[1]
+    full = dataclasses.replace(opts, levels=n)
+    return ml_fwt_solve(d, mask, full)
+
+
 def ml_fwt_solve_rows(d_local, mask_local, opts, m_global, row0, group=None):
     """Row-sharded ML-FWT: rows [row0, row0 + m_local) of the global problem
     on this rank; K_g, the stats, the QP dots and the l1 arg-max are combined
@@ -138,4 +153,4 @@ def ml_fwt_solve_rows(d_local, mask_local, opts, m_global, row0, group=None):
     return _state_from(*out, kind)
 
 
-__all__ = ["ml_fwt_solve", "ml_fwt_solve_rows", "CpcpOptions"]
+__all__ = ["ml_fwt_solve", "fwt_solve", "ml_fwt_solve_rows", "CpcpOptions"]

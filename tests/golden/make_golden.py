@@ -131,10 +131,44 @@ def fwt_cases():
             converged=np.array(st.converged), **hist_arrays(st.history), **extra)
 
 
+def fwt_full_cases():
+    """Full-width Frank-Wolfe thresholding (mlrpca.fwt_solve, cpcp.py:459-477)."""
+    cases = {
+        # name: (m, n, rank, eta, observe, seed, tol, max_iters, dtype)
+        "fwtfull_f64": (90, 70, 4, 0.10, 0.8, 11, 1e-6, 250, np.float64),
+        "fwtfull_f32": (120, 96, 4, 0.10, 0.7, 12, 1e-5, 200, np.float32),
+    }
+    for name, (m, n, r, eta, obs, seed, tol, iters, dt) in cases.items():
+        d, mask = O.gaussian_rpca(m, n, r, eta, seed, observe=obs)
+        d = d.astype(dt).astype(np.float64)
+        lam = 1 / np.sqrt(max(m, n))
+        om = mlrpca.ObservationMask(mask) if mask is not None else None
+        st = mlrpca.fwt_solve(d, om, mlrpca.CpcpOptions(
+            lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=tol, max_iters=iters, collect_rank=False))
+        # FW-T is chaotic (SURVEY.md fact 7): the envelope is the spread of the
+        # oracle itself under 1-ulp input perturbations (12 runs)
+        env_obj, env_it = 0.0, 0
+        for q in range(12):
+            rng = np.random.default_rng(1000 + q)
+            dp = d * (1 + rng.integers(-1, 2, d.shape) * np.finfo(np.float64).eps)
+            o = O.ml_fwt(dp, mask, lam, lam / np.sqrt(max(m, n)), tol=tol, max_iters=iters, levels=n,
+                         collect_rank=False)
+            env_obj = max(env_obj, abs(o.objective_history[-1] - st.objective_history[-1]) / st.objective_history[-1])
+            env_it = max(env_it, abs(o.iter - st.iter))
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), d=d, mask=mask, l=st.l, s=st.s,
+            env_obj=np.array(env_obj), env_iter=np.array(env_it),
+            t_l=np.array(st.t_l), t_s=np.array(st.t_s), u_l=np.array(st.u_l),
+            u_s=np.array(st.u_s), iter=np.array(st.iter), tol=np.array(tol), max_iters=np.array(iters),
+            lam_l=np.array(lam), lam_s=np.array(lam / np.sqrt(max(m, n))),
+            converged=np.array(st.converged), **hist_arrays(st.history))
+
+
 if __name__ == "__main__":
     multilevel_kats()
     linalg_kats()
     pcp_cases()
     pcp_c1_summary()
     fwt_cases()
+    fwt_full_cases()
     print("golden vectors written to", HERE)

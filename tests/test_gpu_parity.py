@@ -136,6 +136,26 @@ def test_ml_fwt_golden_envelope(golden, name):
     assert np.all(np.diff(obj) <= 1e-9 * obj[:-1])  # exact segment search: non-increasing
 
 
+@pytest.mark.parametrize("name", ["fwtfull_f64", "fwtfull_f32"])
+def test_fwt_full_golden_envelope(golden, name):
+    """Full-width fwt_solve against the reference's own fwt_solve output."""
+    g = golden(name)
+    d = g["d"].astype(np.float32) if "f32" in name else g["d"]
+    mask = pkg.ObservationMask(g["mask"]) if "mask" in g else None
+    st = pkg.fwt_solve(d, mask, pkg.CpcpOptions(
+        lambda_l=float(g["lam_l"]), lambda_s=float(g["lam_s"]), tol=float(g["tol"]),
+        max_iters=int(g["max_iters"]), collect_rank=False))
+    ref_obj = g["h_obj"]
+    it = int(g["iter"])
+    # iteration 1 is exact; after that the trajectory is compared with the
+    # envelope the oracle itself spans under 1-ulp input perturbations
+    assert abs(st.objective_history[0] - ref_obj[0]) <= (1e-6 if "f32" in name else 1e-9) * ref_obj[0]
+    assert abs(st.iter - it) <= max(2, 2 * int(g["env_iter"]))
+    assert abs(st.objective_history[-1] - ref_obj[-1]) / ref_obj[-1] <= max(1e-4, 2 * float(g["env_obj"]))
+    obj = np.array(st.objective_history)
+    assert np.all(np.diff(obj) <= 1e-9 * obj[:-1])  # exact segment search: non-increasing
+
+
 def test_ml_fwt_zero_observed_data():
     st = pkg.ml_fwt_solve(np.zeros((16, 12)), None, pkg.CpcpOptions(lambda_l=0.1, lambda_s=0.01, levels=6,
                                                                        collect_rank=False))

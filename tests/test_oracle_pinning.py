@@ -127,6 +127,21 @@ def test_golden_ml_fwt(golden, name):
     assert_allclose(st.objective_history[:k], g["h_obj"][:k], rtol=1e-6)
 
 
+@pytest.mark.parametrize("name", ["fwtfull_f64", "fwtfull_f32"])
+def test_golden_fwt_full(golden, name):
+    """Full-width FW-T (reference fwt_solve, cpcp.py:459-477) is the ML solver
+    on the identity chain (levels = n): the oracle reproduces the reference's
+    own fwt_solve output."""
+    g = golden(name)
+    n = g["d"].shape[1]
+    mask = g.get("mask")
+    st = O.ml_fwt(g["d"], mask, float(g["lam_l"]), float(g["lam_s"]), tol=float(g["tol"]),
+                  max_iters=int(g["max_iters"]), levels=n, collect_rank=False)
+    assert abs(st.iter - int(g["iter"])) <= 2
+    k = min(len(st.objective_history), len(g["h_obj"]))
+    assert_allclose(st.objective_history[:k], g["h_obj"][:k], rtol=1e-6)
+
+
 def test_golden_c1_summary(golden):
     g = golden("pcp_c1_summary")
     d, _ = O.make_config("C1", 0)
