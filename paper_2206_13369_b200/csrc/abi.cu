@@ -6,6 +6,8 @@
 #include <vector>
 
 #include "../../include/mlr_b200.h"
+#include <cstdlib>
+
 #include "common.cuh"
 #include "cpcp.h"
 #include "kernels.h"
@@ -152,9 +154,16 @@ static void carve_cpcp(CpcpPlan& p, Carver& c) {
   p.u = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
   p.v = c.take<double>(8 * np);
   p.vin = c.take<double>(8 * np);
-  p.gram_part = c.take<double>(8 * nn * p.gram_splits);
+  p.gram_part = c.take<double>(8 * (p.fine ? 1 : nn * p.gram_splits));
   p.row_part = c.take<double>(8 * 9 * (size_t)p.row_blocks);
   p.dots_part = c.take<double>(8 * 3 * (size_t)p.row_blocks);
+  if (p.fine) {
+    p.ft = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
+    p.fz = c.take<double>(8 * np);
+    p.fv0 = c.take<double>(8 * np);
+    p.fzpart = c.take<double>(8 * (size_t)p.fine_ctas * np);
+    p.fspart = c.take<double>(8 * 2 * (size_t)p.fine_ctas);
+  }
 }
 
 static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t m_global, int64_t row0, int f32,
@@ -174,6 +183,10 @@ static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
   p.cluster = ch.np >= 256 ? 16 : 8;
+  // full width (identity chain) on one rank: matvec power passes, no Gram
+  const char* e = getenv("MLR_CPCP_FINE");
+  p.fine = ch.nh == ch.n && world == 1 && !(e && e[0] == '0');
+  p.fine_ctas = sms;
 }
 
 }  // namespace mlr

@@ -375,6 +375,133 @@ cp_power_kernel(CpcpDev* __restrict__ st, const double* __restrict__ K, int np, 
   }
 }
 
+// Full-width LMO (identity chain, one rank): the _LeadingTriple passes
+// (cpcp.py:304-323) as matvecs on g = g_H (m x n_p, T), on a cooperative
+// grid: t = g v (warp per row) | z partials = g^T t over row blocks |
+// column-sliced fixed-order reduction of z, ||z||^2 | v <- z / ||z||.
+// s2 = ||g v||^2 is the same Rayleigh quotient the Gram path forms as v^T K v.
+constexpr int kFineThreads = 256;
+
+__device__ __forceinline__ double fine_sum(const double* __restrict__ part, int stride, int count) {
+  // fixed-order sum of count partials by one warp (identical in every CTA)
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i = lane; i < count; i += 32) s += part[i * stride];
+  return warp_sum(s);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kFineThreads)
+cp_power_fine_kernel(CpcpDev* __restrict__ st, const T* __restrict__ G, int64_t m, int np, double* __restrict__ v,
+                     double* __restrict__ vin, double* __restrict__ t, double* __restrict__ z,
+                     double* __restrict__ v0, double* __restrict__ zpart, double* __restrict__ spart) {
+  if (st->done) return;  // uniform: every CTA reads the same flag
+  cg::grid_group grid = cg::this_grid();
+  const int P = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int W = kFineThreads / 32;
+  __shared__ double red[W];
+  __shared__ double bc[2];
+  const double rtol = st->rtol;
+  const int maxp = st->max_passes;
+  const int cw = (np + P - 1) / P;  // column slice per CTA
+  const int c0 = b * cw, c1 = min(np, c0 + cw);
+  for (int j = c0 + tid; j < c1; j += kFineThreads) v0[j] = v[j];
+  const int64_t rb = (m + P - 1) / P;
+  const int64_t r0 = b * rb, r1 = min(m, r0 + rb);
+  double s2_prev = -1.0, s2 = 0.0, nwv = 0.0;
+  int none = 0, pass = 0;
+  for (pass = 1; pass <= maxp; ++pass) {
+    // t = g v and per-CTA partial of ||t||^2
+    double ss = 0.0;
+    for (int64_t i = (int64_t)b * W + wid; i < m; i += (int64_t)P * W) {
+      const T* row = G + i * np;
+      double acc = 0.0;
+      for (int j = lane; j < np; j += 32) acc = fma((double)row[j], v[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        t[i] = acc;
+        ss = fma(acc, acc, ss);
+      }
+    }
+    if (lane == 0) red[wid] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      double q = 0.0;
+      for (int w = 0; w < W; ++w) q += red[w];
+      spart[2 * b] = q;
+    }
+    grid.sync();
+    // z partials over this CTA's row block, 8 columns per thread
+    for (int j0 = tid * 8; j0 < np; j0 += kFineThreads * 8) {
+      double acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+      for (int64_t i = r0; i < r1; ++i) {
+        const double ti = t[i];
+        const T* row = G + i * np + j0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (j0 + e < np) acc[e] = fma((double)row[e], ti, acc[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (j0 + e < np) zpart[(int64_t)b * np + j0 + e] = acc[e];
+    }
+    grid.sync();
+    // z = sum of the partials (column slice), ||z||^2 partial
+    double zz = 0.0;
+    for (int j = c0 + tid; j < c1; j += kFineThreads) {
+      double acc = 0.0;
+      for (int q = 0; q < P; ++q) acc += zpart[(int64_t)q * np + j];
+      z[j] = acc;
+      zz = fma(acc, acc, zz);
+    }
+    zz = warp_sum(zz);
+    if (lane == 0) red[wid] = zz;
+    __syncthreads();
+    if (tid == 0) {
+      double q = 0.0;
+      for (int w = 0; w < W; ++w) q += red[w];
+      spart[2 * b + 1] = q;
+    }
+    grid.sync();
+    if (wid == 0) {
+      const double a = fine_sum(spart, 2, P);
+      const double c = fine_sum(spart + 1, 2, P);
+      if (lane == 0) {
+        bc[0] = a;
+        bc[1] = c;
+      }
+    }
+    __syncthreads();
+    s2 = bc[0];
+    const double kvn = sqrt(bc[1]);
+    if (s2 <= 0.0 || kvn == 0.0) {
+      none = 1;
+      break;
+    }
+    nwv = kvn / sqrt(s2);
+    for (int j = c0 + tid; j < c1; j += kFineThreads) {
+      vin[j] = v[j];
+      v[j] = z[j] / kvn;
+    }
+    const bool stop = fabs(s2 - s2_prev) <= rtol * s2;
+    s2_prev = s2;
+    grid.sync();  // v complete before the next pass reads it
+    if (stop) break;
+  }
+  if (pass > maxp) pass = maxp;
+  if (none) {  // the reference keeps its previous right vector
+    for (int j = c0 + tid; j < c1; j += kFineThreads) v[j] = v0[j];
+  }
+  if (b == 0 && tid == 0) {
+    st->none = none;
+    st->s2 = none ? 0.0 : s2;
+    st->sigma = none ? 0.0 : nwv;
+    st->passes = pass;
+  }
+}
+
 // Corner selection (cpcp.py:361-368), arg-max pick across ranks.
 __global__ void cp_lmo_scalars(CpcpDev* st, const double* __restrict__ am_all, int world) {
   if (st->done) return;
@@ -644,10 +771,12 @@ int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st) {
     g.C = p->gram_part; g.ldc = np; g.c_f32 = false; g.c_slice = nn; g.splits = p->gram_splits; g.alpha = 1.0;
     g.skip = &p->dev->done;
     g.sym = true;  // Gram: upper-triangle tiles, mirrored
-    int rc = gemm_f64(g, st);
-    if (rc) return rc;
-    rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);
-    if (rc) return rc;
+    if (!p->fine) {  // full width: the LMO works on g_H directly
+      int rc = gemm_f64(g, st);
+      if (rc) return rc;
+      rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);
+      if (rc) return rc;
+    }
     cp_part_reduce<<<1, 256, 0, st>>>(p->row_part, p->row_blocks, red + nn, amax);
     MLR_LAUNCH_CHECK("cp_part_reduce");
   } else {
@@ -689,7 +818,25 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   p->timer.begin(st);
-  MLR_CUDA(cudaLaunchKernelEx(&cfg, cp_power_kernel, p->dev, (const double*)red, np, p->v, p->vin, fit ? 1 : 0));
+  if (p->fine) {
+    cudaLaunchConfig_t fc = {};
+    fc.gridDim = dim3(p->fine_ctas);
+    fc.blockDim = dim3(kFineThreads);
+    fc.stream = st;
+    cudaLaunchAttribute fa[1];
+    fa[0].id = cudaLaunchAttributeCooperative;
+    fa[0].val.cooperative = 1;
+    fc.attrs = fa;
+    fc.numAttrs = 1;
+    if (p->f32)
+      MLR_CUDA(cudaLaunchKernelEx(&fc, cp_power_fine_kernel<float>, p->dev, (const float*)p->GH, p->m_local, np,
+                                  p->v, p->vin, p->ft, p->fz, p->fv0, p->fzpart, p->fspart));
+    else
+      MLR_CUDA(cudaLaunchKernelEx(&fc, cp_power_fine_kernel<double>, p->dev, (const double*)p->GH, p->m_local, np,
+                                  p->v, p->vin, p->ft, p->fz, p->fv0, p->fzpart, p->fspart));
+  } else {
+    MLR_CUDA(cudaLaunchKernelEx(&cfg, cp_power_kernel, p->dev, (const double*)red, np, p->v, p->vin, fit ? 1 : 0));
+  }
   cp_lmo_scalars<<<1, 1, 0, st>>>(p->dev, amax_all, p->world);
   MLR_LAUNCH_CHECK("cp_lmo_scalars");
   p->timer.end(1, st);

@@ -43,6 +43,15 @@ struct CpcpPlan {
   double* dots_part; // row_blocks x 3
   const uint32_t* mask_dev;  // bound at start (may be null: fully observed)
   int64_t ldm_dev;
+  // full-width solve (identity chain, one rank): the LMO's power passes run as
+  // matvecs on g_H = r instead of on the n x n Gram, which is never formed
+  bool fine;
+  int fine_ctas;
+  double* ft;        // m_local: t = g v
+  double* fz;        // np: z = g^T t
+  double* fv0;       // np: v at LMO entry (restored when g v = 0)
+  double* fzpart;    // fine_ctas x np
+  double* fspart;    // fine_ctas x 2
 };
 
 int cpcp_start(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
