@@ -12,6 +12,7 @@ reference instead multiplies by the dense ``n x n_H`` matrix
 from __future__ import annotations
 
 import ctypes
+import functools
 import warnings
 from dataclasses import dataclass, field
 
@@ -110,7 +111,18 @@ class Chain:
         return r
 
     def sigma_max(self):
-        """Largest singular value of R (cpcp.py:502 uses 1/sigma_1 as radius)."""
+        """Largest singular value of R (cpcp.py:502 uses 1/sigma_1 as radius).
+
+        R^T R is tridiagonal: dense eigvalsh for small n_H (bit-for-bit the
+        reference's call), LAPACK bisection on the tridiagonal for large n_H
+        (the dense solve is O(n_H^3)); the identity chain is exactly 1."""
+        if self.n_coarse == self.n_fine and not np.any(self.g_off) and np.all(self.g_diag == 1.0):
+            return 1.0
+        if self.n_coarse > 512:
+            from scipy.linalg import eigvalsh_tridiagonal
+            k = self.n_coarse - 1
+            top = eigvalsh_tridiagonal(self.g_diag, self.g_off, select="i", select_range=(k, k))[0]
+            return float(np.sqrt(max(top, 0.0)))
         g = np.diag(self.g_diag) + np.diag(self.g_off, 1) + np.diag(self.g_off, -1)
         return float(np.sqrt(max(np.linalg.eigvalsh(g)[-1], 0.0)))
 
@@ -147,6 +159,7 @@ class Chain:
 _CACHE: dict = {}
 
 
+@functools.lru_cache(maxsize=16)
 def build_chain(n, n_coarse_target):
     """Normalised chain from ``n`` down to ``n_coarse_target`` (reachable by
     repeated halving; ``n`` itself gives the identity).  Mirrors the checks
@@ -185,7 +198,10 @@ def build_chain(n, n_coarse_target):
     np.add.at(graw, (c0[has1] + 1, c0[has1] + 1), r1[has1] * r1[has1])
     np.add.at(graw, (c0[has1], c0[has1] + 1), r0[has1] * r1[has1])
     np.add.at(graw, (c0[has1] + 1, c0[has1]), r0[has1] * r1[has1])
-    spectral = float(np.sqrt(max(np.linalg.eigvalsh(graw)[-1], 0.0)))
+    if nfac == 0 and target == n:
+        spectral = 1.0  # no coarsening: raw = I and eigvalsh(I) is exactly 1
+    else:
+        spectral = float(np.sqrt(max(np.linalg.eigvalsh(graw)[-1], 0.0)))
     if spectral == 0.0:
         raise ValueError("composite operator is zero; cannot normalize")
     # scipy divides a sparse array by a scalar as a multiply by its reciprocal

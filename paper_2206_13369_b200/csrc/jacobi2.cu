@@ -556,6 +556,19 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             S.csl[0][i] = make_double2(rc, rs);
           }
           int any = __syncthreads_or(rot_here);
+          // Q = J_0 J_1 ... replayed inside the rounds by warps 1-4 (they have
+          // slack while warp 0 runs the rotation chain): 4 lanes per row of Q,
+          // pairs kk = sq + 4h; x = Q[r][kk] stays, y = Q[r][partner] moves to
+          // pair kk - 1 after every round (shuffle within the row's 4 lanes)
+          const bool replay = tid >= 32 && tid < 160;
+          const int rq = (tid - 32) >> 2, sq = (tid - 32) & 3;
+          double qx[4], qy[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            qx[h] = rq == sq + 4 * h ? 1.0 : 0.0;
+            qy[h] = rq == J2_BW + sq + 4 * h ? 1.0 : 0.0;
+          }
+          const int qsrc = (lane & ~3) | ((sq + 1) & 3);
           for (int rnd = 0; rnd < rounds; ++rnd) {
             const int par = rnd & 1;
             if (any) rmask |= 1u << rnd;
@@ -596,9 +609,9 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
                 S.ttb[par ^ 1][i] = rt;
                 S.csl[rnd + 1][i] = make_double2(rc, rs);
               }
-            } else if (any) {
+            } else {
               // ---- update warps: the 256 2x2 blocks of round rnd, Gin -> Gout
-              for (int bi = tid - 32; bi < J2_BW * J2_BW; bi += J2_THREADS - 32) {
+              for (int bi = any ? tid - 32 : J2_BW * J2_BW; bi < J2_BW * J2_BW; bi += J2_THREADS - 32) {
                 const int pp = bi >> 4, q = bi & 15;
                 const int p1 = pp, p2 = J2_BW + ((pp + rnd) & (J2_BW - 1));
                 const int q1 = q, q2 = J2_BW + ((q + rnd) & (J2_BW - 1));
@@ -618,6 +631,22 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
                   Gout[p2][q2] = o.o22;
                 }
               }
+              if (replay) {
+                if (any) {
+#pragma unroll
+                  for (int h = 0; h < 4; ++h) {
+                    const double2 c2 = S.csb[par][sq + 4 * h];
+                    const double a = qx[h], b = qy[h];
+                    qx[h] = c2.x * a - c2.y * b;
+                    qy[h] = c2.y * a + c2.x * b;
+                  }
+                }
+                double v[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) v[h] = __shfl_sync(0xffffffffu, qy[h], qsrc);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) qy[h] = sq < 3 ? v[h] : v[(h + 1) & 3];
+              }
             }
             const int any_next = __syncthreads_or(rot_next);
             if (any) {
@@ -628,6 +657,15 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             any = any_next;
           }
           Gfin = Gin;
+          if (replay) {
+            double* qo = Qbuf + (int64_t)k * J2_PW * J2_PW;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int kk = sq + 4 * h;
+              qo[rq * J2_PW + kk] = qx[h];
+              qo[rq * J2_PW + J2_BW + ((kk + rounds) & (J2_BW - 1))] = qy[h];
+            }
+          }
         }
         j2_mark(7, t0);
         // Q = J_0 J_1 ... : row r of Q evolves independently; 8 lanes own a
@@ -654,38 +692,6 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
               __syncwarp();
             }
             for (int e = sub; e < J2_PW; e += 8) qo[r * J2_PW + e] = S.Q[r][e];
-          } else {
-            // cross pairs (kk, 16 + (kk + rnd) % 16): x = Q[r][kk] stays put,
-            // y = Q[r][partner] moves to pair kk - 1 after every round, a
-            // shuffle within the row's 8 lanes; everything in registers
-            double x[2], y[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              x[h] = r == sub + 8 * h ? 1.0 : 0.0;
-              y[h] = r == J2_BW + sub + 8 * h ? 1.0 : 0.0;
-            }
-            const int src = (tid & 31 & ~7) | ((sub + 1) & 7);
-            for (int rnd = 0; rnd < rounds; ++rnd) {
-              if ((rmask >> rnd) & 1u) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const double2 c2 = S.csl[rnd][sub + 8 * h];
-                  const double a = x[h], b = y[h];
-                  x[h] = c2.x * a - c2.y * b;
-                  y[h] = c2.y * a + c2.x * b;
-                }
-              }
-              const double v0 = __shfl_sync(0xffffffffu, y[0], src);
-              const double v1 = __shfl_sync(0xffffffffu, y[1], src);
-              y[0] = sub < 7 ? v0 : v1;
-              y[1] = sub < 7 ? v1 : v0;
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int kk = sub + 8 * h;
-              qo[r * J2_PW + kk] = x[h];
-              qo[r * J2_PW + J2_BW + ((kk + rounds) & (J2_BW - 1))] = y[h];
-            }
           }
         }
         j2_mark(1, t0);
