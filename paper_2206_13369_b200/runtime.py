@@ -20,14 +20,28 @@ class Comm:
         self.world = dist.get_world_size(group) if self.enabled else 1
         self.rank = dist.get_rank(group) if self.enabled else 0
 
+    def _host(self, t):
+        """gloo works on host tensors: stage CUDA tensors through host memory."""
+        return self.world > 1 and t.is_cuda and dist.get_backend(self.group) != "nccl"
+
     def sum(self, t):
         if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            if self._host(t):
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
     def max(self, t):
         if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            if self._host(t):
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return t
 
     def gather(self, out, t):
@@ -36,8 +50,9 @@ class Comm:
             if dist.get_backend(self.group) == "nccl":
                 dist.all_gather_into_tensor(out, t, group=self.group)
             else:
-                parts = [torch.empty_like(t) for _ in range(self.world)]
-                dist.all_gather(parts, t, group=self.group)
+                h = t.cpu()
+                parts = [torch.empty_like(h) for _ in range(self.world)]
+                dist.all_gather(parts, h, group=self.group)
                 out.copy_(torch.cat(parts))
         else:
             out.copy_(t)
