@@ -191,7 +191,7 @@ def main():
         solve(D)
     # ---- value: D resident in HBM
     sink = []
-    pcp_mod.TIMING_SINK = sink if world == 1 else None
+    pcp_mod.TIMING_SINK = sink
     barrier()
     total_ms, iters = 0.0, 0
     with ClockSampler(local) as clk:

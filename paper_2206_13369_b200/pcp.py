@@ -159,8 +159,16 @@ def ml_ialm_solve_rows(d_local, opts, m_global, group=None):
     with torch.cuda.device(D.device):
         chain = build_chain(n, _checked_width(n, m_global, opts))
         be = CudaPcp(chain, m, m_global, D.dtype == torch.float32, opts.max_iters, D.device)
+        if TIMING_SINK is not None:
+            be.set_timing(True)
         try:
             out = run_ialm(be, comm, D, m_global, n, opts, lam, _check_every(opts))
+            if TIMING_SINK is not None:
+                t = be.timing()
+                t["iters"] = out[3]["k"] if out is not None else 0
+                t["jac_sweeps"] = [int(x) for x in out[4][:, 6]] if out is not None else []
+                t["lanczos_steps"] = be.lanczos_state()["k"] + 1
+                TIMING_SINK.append(t)
         finally:
             be.close()
     if out is None:
