@@ -109,3 +109,16 @@ def test_product_does_not_import_oracle():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg_dir, fn)).read()
             assert "oracle" not in src.replace("oracle atoms", "").replace("oracle_atoms", ""), fn
+
+
+def test_cli_bridge_rebinds_and_restores():
+    import types
+    from paper_2206_13369_b200 import cli_bridge, cpcp, pcp
+    cpu = object()
+    mod = types.SimpleNamespace(ialm_solve=cpu, ml_ialm_solve=cpu, fwt_solve=cpu, ml_fwt_solve=cpu)
+    prev = cli_bridge.install(mod)
+    assert mod.ml_ialm_solve is pcp.ml_ialm_solve
+    assert mod.fwt_solve is cpcp.fwt_solve and mod.ml_fwt_solve is cpcp.ml_fwt_solve
+    assert mod.ialm_solve is cpu  # full-width PCP stays on the CPU
+    cli_bridge.uninstall(mod, prev)
+    assert mod.ml_ialm_solve is cpu and mod.fwt_solve is cpu and mod.ml_fwt_solve is cpu
