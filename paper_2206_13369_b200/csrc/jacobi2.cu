@@ -267,7 +267,7 @@ struct J2Item {
 };
 
 template <bool CLUSTER>
-__global__ void __launch_bounds__(J2_THREADS)
+__global__ void __launch_bounds__(J2_THREADS, 2)
 jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows_v, double tol,
                double abs_floor_rel, int max_sweeps, double* __restrict__ Qlog, int cap,
                int* __restrict__ qflag_log, double* __restrict__ off_slots, int* __restrict__ result,
@@ -1027,6 +1027,7 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
     MLR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     nctas = std::max(1, std::min(std::max(npairs, npairs * (npairs + 1) / 4), nsm));
   }
+  int grid_per_sm = 1;  // cooperative path: a second CTA per SM doubles the phase-B workers
   const int vchunks = (nrows_v + J2_PW - 1) / J2_PW;
   const int nitems = npairs * (npairs - 1) / 2 + (vlog ? 0 : npairs * vchunks);
   // dataflow steps (see jacobi2_kernel) when the per-CTA item lists fit
@@ -1046,6 +1047,17 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   // quadratic convergence: a sweep that started with every pair below
   // ~sqrt(tol) leaves the off-diagonal ~ below tol, no verification sweep
   const double early_off = 0.03 * std::sqrt(tol);
+  if (!cluster && dflow) {
+    MLR_CUDA(cudaFuncSetAttribute(jacobi2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0, dev = 0, nsm = 0;
+    MLR_CUDA(cudaGetDevice(&dev));
+    MLR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    MLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi2_kernel<false>, J2_THREADS, smem));
+    grid_per_sm = std::max(1, std::min(occ, 2));
+    const int want = std::max(npairs, npairs * (npairs + 1) / 4);
+    if (const char* e = getenv("MLR_J2_PER_SM")) grid_per_sm = std::max(1, std::min(occ, atoi(e)));
+    nctas = std::max(1, std::min(want, nsm * grid_per_sm));
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(J2_THREADS);
   cfg.dynamicSmemBytes = smem;
