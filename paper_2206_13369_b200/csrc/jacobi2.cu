@@ -192,7 +192,9 @@ __device__ __forceinline__ void tile_mm(const double (*A)[J2_LD], const double (
 template <typename Smem>
 __device__ __forceinline__ void j2_item(Smem& S, double* __restrict__ B, int np, int a1, int b1, int a2, int b2,
                                         const double* __restrict__ QA, const double* __restrict__ QB, bool ra,
-                                        bool rb, bool store) {
+                                        bool rb, bool store, int skipmask = 0, const int* wait0 = nullptr,
+                                        const int* wait1 = nullptr, int waitval = 0, int* loaded0 = nullptr,
+                                        int* loaded1 = nullptr) {
   const int tid = threadIdx.x;
   double xr[4], qa[4], qb[4];
 #pragma unroll
@@ -211,6 +213,10 @@ __device__ __forceinline__ void j2_item(Smem& S, double* __restrict__ B, int np,
     if (rb) S.Q2[e >> 5][e & 31] = qb[u];
   }
   __syncthreads();
+  if (tid == 0) {  // X is read: its next-step owners may now overwrite their quadrants
+    if (loaded0) st_release(loaded0, waitval);
+    if (loaded1) st_release(loaded1, waitval);
+  }
   const int rr = tm_row();
   double o[4];
   if (!rb) {
@@ -234,16 +240,82 @@ __device__ __forceinline__ void j2_item(Smem& S, double* __restrict__ B, int np,
     S.X[rr][tm_col(u)] = o[u];
     S.Q2[tm_col(u)][rr] = o[u];
   }
+  if (tid == 0) {  // next-step owners read this item's X before we overwrite it
+    if (wait0)
+      while (ld_acquire(wait0) < waitval) __nanosleep(20);
+    if (wait1)
+      while (ld_acquire(wait1) < waitval) __nanosleep(20);
+  }
   __syncthreads();
   if (store) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = tid + u * J2_THREADS;
       const int i = e >> 5, j = e & 31;
+      if ((skipmask >> (((i >> 4) << 1) | (j >> 4))) & 1) continue;  // a next-step owner writes it
       B[(int64_t)j2_col(i, a1, b1) * np + j2_col(j, a2, b2)] = S.X[i][j];
       B[(int64_t)j2_col(i, a2, b2) * np + j2_col(j, a1, b1)] = S.Q2[i][j];
     }
   }
+}
+
+// The 16x16 quadrant (rows hr.., cols hc.. of the 32x32 result) of an item,
+// Q_A[:, hr..]^T X Q_B[:, hc..]: half of the first product, a quarter of the
+// second.  Leaves the quadrant in S.Y[32 + i][j]?  No: in S.X[i][j], i, j < 16.
+// Calls `loaded()` (thread 0, after a barrier) once X has been read.
+template <typename Smem, typename F>
+__device__ __forceinline__ void j2_quadrant(Smem& S, const double* __restrict__ B, int np, int a1, int b1, int a2,
+                                            int b2, const double* __restrict__ QA, const double* __restrict__ QB,
+                                            bool ra, bool rb, int hr, int hc, F loaded) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double xr[4], qa[4], qb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * J2_THREADS;
+    xr[u] = B[(int64_t)j2_col(e >> 5, a1, b1) * np + j2_col(e & 31, a2, b2)];
+    qa[u] = ra ? QA[e] : 0.0;
+    qb[u] = rb ? QB[e] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * J2_THREADS;
+    S.X[e >> 5][e & 31] = xr[u];
+    if (ra) S.Q[e >> 5][e & 31] = qa[u];
+    if (rb) S.Q2[e >> 5][e & 31] = qb[u];
+  }
+  __syncthreads();
+  if (tid == 0) loaded();
+  // Y (32 x 16) = X Q_B[:, hc..hc+16): warp w -> rows 8(w>>1).., cols 8(w&1)..
+  {
+    const int r = 8 * (w >> 1) + (lane >> 2), kk = lane & 3, c = 8 * (w & 1) + (lane >> 2);
+    double d0 = 0.0, d1 = 0.0;
+    if (rb) {
+#pragma unroll
+      for (int k4 = 0; k4 < J2_PW; k4 += 4) j2_dmma(d0, d1, S.X[r][k4 + kk], S.Q2[k4 + kk][hc + c]);
+    } else {
+      d0 = S.X[r][hc + 8 * (w & 1) + 2 * kk];
+      d1 = S.X[r][hc + 8 * (w & 1) + 2 * kk + 1];
+    }
+    S.Y[r][8 * (w & 1) + 2 * kk] = d0;
+    S.Y[r][8 * (w & 1) + 2 * kk + 1] = d1;
+  }
+  __syncthreads();
+  // quadrant (16 x 16) = Q_A[:, hr..hr+16)^T Y: warps 0..3
+  if (w < 4) {
+    const int r = 8 * (w >> 1) + (lane >> 2), kk = lane & 3, c = 8 * (w & 1) + (lane >> 2);
+    double d0 = 0.0, d1 = 0.0;
+    if (ra) {
+#pragma unroll
+      for (int k4 = 0; k4 < J2_PW; k4 += 4) j2_dmma(d0, d1, S.Q[k4 + kk][hr + r], S.Y[k4 + kk][c]);
+    } else {
+      d0 = S.Y[hr + r][8 * (w & 1) + 2 * kk];
+      d1 = S.Y[hr + r][8 * (w & 1) + 2 * kk + 1];
+    }
+    S.X[r][8 * (w & 1) + 2 * kk] = d0;
+    S.X[r][8 * (w & 1) + 2 * kk + 1] = d1;
+  }
+  __syncthreads();
 }
 
 // Cycle breakdown of CTA 0 (phase A load+measure, inner rounds, barrier 1,
@@ -289,12 +361,13 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   // items holding a next-step pair's off-diagonal block first; each of those
   // releases a per-pair flag that the next step's owner waits on instead of
   // a cluster/grid barrier, so phase A of step t+1 overlaps phase B of step t.
-  const bool split = dflow && 2 * (nctas - npairs) >= npairs;
+  const bool split = dflow && 2 * (nctas - npairs) >= npairs && dflow != 2;  // dflow 2: no owner/worker split
   const int nworkers = split ? nctas - npairs : nctas;
   const int widx = split ? me - npairs : me;  // < 0: owner only
   const int my_items = (dflow || widx < 0) ? 0 : (nitems - widx + nworkers - 1) / nworkers;
   int* cflag = qflag_log + cap * npairs;  // per next-step pair: step + 1 whose item is done
   int* tctr = cflag + npairs;             // dflow item-queue ticket counters (2, by step parity)
+  int* wflag = tctr + 2;                  // per next-step pair: step whose critical item has read X
   // dynamic smem: [J2Smem][Qcache npairs x 32 x LD (optional)][sched nb*npairs int][items][qslot npairs int]
   unsigned char* p = smem_raw + ((sizeof(J2Smem) + 127) & ~size_t(127));
   double(*Qall)[J2_PW][J2_LD] = reinterpret_cast<double(*)[J2_PW][J2_LD]>(p);
@@ -377,11 +450,11 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         // dflow: the off-diagonal block (pa, pb) comes from a phase-B item of
         // the previous step (unless pa, pb were paired then) that may still run
         bool loaded = false;
+        bool crit_quad = false;
         if (dflow && step > 0 && cur_pair[pa] != cur_pair[pb]) {
-          // (pa, pb) lies in the previous step's item (kA, kB), which the
-          // workers skip: the first pair of this step needing that item
-          // computes it, stores it and assembles its tile from it; a second
-          // one (same item) waits for the first one's flag and loads
+          // (pa, pb) is one quadrant of the previous step's item (kA, kB):
+          // compute just that quadrant (the workers compute and store the
+          // rest, after this CTA has read the item's X: flag cflag[k] = g)
           const int k0a = cur_pair[pa], k0b = cur_pair[pb];
           const int kA = min(k0a, k0b), kB = max(k0a, k0b);
           int first = k;
@@ -393,7 +466,54 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
               break;
             }
           }
-          if (first == k) {
+          if (!split) {
+            // owners are workers too: the first pair needing the item
+            // computes all of it (workers skip it), a second one waits
+            if (first == k) {
+              const int* prow = sched + (step - 1) * npairs;
+              const int a1 = prow[kA] & 0xffff, b1 = prow[kA] >> 16;
+              const int a2 = prow[kB] & 0xffff, b2 = prow[kB] >> 16;
+              const int pslot = (g - 1) % cap;
+              const double* Qp = Qlog + (int64_t)pslot * npairs * J2_PW * J2_PW;
+              const int* qfp = qflag_log + pslot * npairs;
+              const bool ra = qfp[kA] != 0, rb = qfp[kB] != 0;
+              const double da = B[(int64_t)(pa * J2_BW + (tid >> 4)) * np + pa * J2_BW + (tid & 15)];
+              const double db = B[(int64_t)(pb * J2_BW + (tid >> 4)) * np + pb * J2_BW + (tid & 15)];
+              j2_item(S, B, np, a1, b1, a2, b2, Qp + (int64_t)kA * J2_PW * J2_PW, Qp + (int64_t)kB * J2_PW * J2_PW, ra,
+                      rb, ra || rb);
+              S.G[tid >> 4][tid & 15] = da;
+              S.G[J2_BW + (tid >> 4)][J2_BW + (tid & 15)] = db;
+              const bool pa_row = cur_pair[pa] == kA;
+              const int hr = (pa_row ? (pa == a1 ? 0 : 1) : (pb == a1 ? 0 : 1)) * J2_BW;
+              const int hc = (pa_row ? (pb == a2 ? 0 : 1) : (pa == a2 ? 0 : 1)) * J2_BW;
+              for (int e = tid; e < J2_BW * J2_BW; e += J2_THREADS) {
+                const int i = e >> 4, j = e & 15;
+                const double v = pa_row ? S.X[hr + i][hc + j] : S.X[hr + j][hc + i];  // B[pa + i][pb + j]
+                S.G[i][J2_BW + j] = v;
+                S.G[J2_BW + j][i] = v;
+              }
+              loaded = true;
+              bool dup = false;
+              for (int k2 = k + 1; k2 < npairs; ++k2) {
+                const int x = srow[k2];
+                const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
+                if (min(c1, c2) == kA && max(c1, c2) == kB) dup = true;
+              }
+              if (dup) {
+                __syncthreads();
+                if (tid == 0) {
+                  __threadfence();
+                  for (int k2 = k + 1; k2 < npairs; ++k2) {
+                    const int x = srow[k2];
+                    const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
+                    if (min(c1, c2) == kA && max(c1, c2) == kB) st_release(cflag + k2, g + 1);
+                  }
+                }
+              }
+            } else if (tid == 0) {
+              while (ld_acquire(cflag + k) < g + 1) __nanosleep(20);
+            }
+          } else {
             const int* prow = sched + (step - 1) * npairs;
             const int a1 = prow[kA] & 0xffff, b1 = prow[kA] >> 16;
             const int a2 = prow[kB] & 0xffff, b2 = prow[kB] >> 16;
@@ -403,40 +523,22 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             const bool ra = qfp[kA] != 0, rb = qfp[kB] != 0;
             const double da = B[(int64_t)(pa * J2_BW + (tid >> 4)) * np + pa * J2_BW + (tid & 15)];
             const double db = B[(int64_t)(pb * J2_BW + (tid >> 4)) * np + pb * J2_BW + (tid & 15)];
-            j2_item(S, B, np, a1, b1, a2, b2, Qp + (int64_t)kA * J2_PW * J2_PW, Qp + (int64_t)kB * J2_PW * J2_PW, ra,
-                    rb, ra || rb);
-            S.G[tid >> 4][tid & 15] = da;
-            S.G[J2_BW + (tid >> 4)][J2_BW + (tid & 15)] = db;
-            // my tile: diagonal blocks from B, the off-diagonal one from out
-            const bool pa_row = cur_pair[pa] == kA;  // pa indexes out's rows
+            // my off-diagonal block is one quadrant of the item
+            const bool pa_row = cur_pair[pa] == kA;  // pa indexes the item's rows
             const int hr = (pa_row ? (pa == a1 ? 0 : 1) : (pb == a1 ? 0 : 1)) * J2_BW;
             const int hc = (pa_row ? (pb == a2 ? 0 : 1) : (pa == a2 ? 0 : 1)) * J2_BW;
-            for (int e = tid; e < J2_BW * J2_BW; e += J2_THREADS) {
-              const int i = e >> 4, j = e & 15;
-              const double v = pa_row ? S.X[hr + i][hc + j] : S.X[hr + j][hc + i];  // B[pa + i][pb + j]
+            j2_quadrant(S, B, np, a1, b1, a2, b2, Qp + (int64_t)kA * J2_PW * J2_PW, Qp + (int64_t)kB * J2_PW * J2_PW,
+                        ra, rb, hr, hc, [&]() { st_release(cflag + k, g); });
+            crit_quad = true;
+            S.G[tid >> 4][tid & 15] = da;
+            S.G[J2_BW + (tid >> 4)][J2_BW + (tid & 15)] = db;
+            {
+              const int i = tid >> 4, j = tid & 15;
+              const double v = pa_row ? S.X[i][j] : S.X[j][i];  // B[pa + i][pb + j]
               S.G[i][J2_BW + j] = v;
               S.G[J2_BW + j][i] = v;
             }
             loaded = true;
-            bool dup = false;
-            for (int k2 = k + 1; k2 < npairs; ++k2) {
-              const int x = srow[k2];
-              const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
-              if (min(c1, c2) == kA && max(c1, c2) == kB) dup = true;
-            }
-            if (dup) {
-              __syncthreads();
-              if (tid == 0) {
-                __threadfence();
-                for (int k2 = k + 1; k2 < npairs; ++k2) {
-                  const int x = srow[k2];
-                  const int c1 = cur_pair[x & 0xffff], c2 = cur_pair[x >> 16];
-                  if (min(c1, c2) == kA && max(c1, c2) == kB) st_release(cflag + k2, g + 1);
-                }
-              }
-            }
-          } else if (tid == 0) {
-            while (ld_acquire(cflag + k) < g + 1) __nanosleep(20);
           }
         }
         __syncthreads();
@@ -695,6 +797,13 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
           }
         }
         j2_mark(1, t0);
+        // split mode: the worker taking my critical item must have read its X
+        // (which contains my off-diagonal block) before I overwrite that block
+        if (rot && crit_quad) {
+          if (tid == 0)
+            while (ld_acquire(wflag + k) < g) __nanosleep(20);
+          __syncthreads();
+        }
         // the rotated diagonal block goes straight back into B
         if (rot)
           for (int e = tid; e < J2_PW * J2_PW; e += J2_THREADS) {
@@ -840,20 +949,31 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         // atomic counter offset by nworkers; each worker ends with exactly
         // one failing grab and the grab completing the count resets it.
         unsigned char* dmark = reinterpret_cast<unsigned char*>(items);
+        short* dcrit = reinterpret_cast<short*>(dmark + ((nbitems + 15) & ~15));  // critical items, first in the queue
         int* ctr = tctr + (g & 1);
         for (int it = tid; it < nbitems; it += J2_THREADS) dmark[it] = 0;
         __syncthreads();
-        if (!last_step)
-          for (int k2 = tid; k2 < npairs; k2 += J2_THREADS) {
-            const int nx = sched[(step + 1) * npairs + k2];
-            const int ka = cur_pair[nx & 0xffff], kb = cur_pair[nx >> 16];
-            if (ka != kb) {
-              const int lo = min(ka, kb), hi = max(ka, kb);
-              dmark[lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1)] = 1;
+        if (tid == 0) {
+          int nc = 0;
+          if (!last_step)
+            for (int k2 = 0; k2 < npairs; ++k2) {
+              const int nx = sched[(step + 1) * npairs + k2];
+              const int ka = cur_pair[nx & 0xffff], kb = cur_pair[nx >> 16];
+              if (ka != kb) {
+                const int lo = min(ka, kb), hi = max(ka, kb);
+                const int it = lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1);
+                if (!dmark[it]) {
+                  dmark[it] = 1;
+                  dcrit[nc++] = (short)it;
+                }
+              }
             }
-          }
+          s_ticket = nc;
+        }
         __syncthreads();
-        const int total = nbitems;
+        const int ncrit = s_ticket;
+        __syncthreads();
+        const int total = ncrit + nbitems;
         const int grabs = (total > nworkers ? total - nworkers : 0) + nworkers;
         auto grab = [&]() {
           if (tid == 0) s_ticket = atomicAdd(ctr, 1);
@@ -872,19 +992,52 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             }
             break;
           }
-          const int it = tk;
-          if (!dmark[it]) {
+          const int it = tk < ncrit ? dcrit[tk] : tk - ncrit;
+          if (tk >= ncrit && dmark[it]) {  // already taken as a critical item
+          } else {
             int kA = 0, rem = it;
             while (rem >= npairs - 1 - kA) {
               rem -= npairs - 1 - kA;
               ++kA;
             }
             const int kB = kA + 1 + rem;
-            if (qf_all[kA] || qf_all[kB]) {
+            // non-split: a next-step owner computes the whole item itself
+            if ((qf_all[kA] || qf_all[kB]) && !(dmark[it] && !split)) {
               const int a1 = srow[kA] & 0xffff, b1 = srow[kA] >> 16;
               const int a2 = srow[kB] & 0xffff, b2 = srow[kB] >> 16;
+              // quadrants that are a next-step pair's off-diagonal block are
+              // written by that pair's owner; wait until it has read X
+              int skipmask = 0;
+              const int* w0 = nullptr;
+              const int* w1 = nullptr;
+              int* l0 = nullptr;
+              int* l1 = nullptr;
+              if (dmark[it]) {
+                const int xs[2] = {a1, b1}, ys[2] = {a2, b2};
+                for (int qx = 0; qx < 2; ++qx)
+                  for (int qy = 0; qy < 2; ++qy)
+                    if (nxt_partner[xs[qx]] == ys[qy]) {
+                      skipmask |= 1 << (qx * 2 + qy);
+                      const int kn = nxt_pair[xs[qx]];
+                      if (!w0) {
+                        w0 = cflag + kn;
+                        l0 = wflag + kn;
+                      } else {
+                        w1 = cflag + kn;
+                        l1 = wflag + kn;
+                      }
+                    }
+              }
               j2_item(S, B, np, a1, b1, a2, b2, Qbuf + (int64_t)kA * J2_PW * J2_PW,
-                      Qbuf + (int64_t)kB * J2_PW * J2_PW, qf_all[kA] != 0, qf_all[kB] != 0, true);
+                      Qbuf + (int64_t)kB * J2_PW * J2_PW, qf_all[kA] != 0, qf_all[kB] != 0, true, skipmask, w0,
+                      w1, g + 1, l0, l1);
+            } else if (split && dmark[it] && tid == 0) {
+              // identity critical item: nothing to read, release its owners
+              const int xs[2] = {srow[kA] & 0xffff, srow[kA] >> 16};
+              for (int qx = 0; qx < 2; ++qx) {
+                const int y = nxt_partner[xs[qx]];
+                if (cur_pair[y] == kB) st_release(wflag + nxt_pair[xs[qx]], g + 1);
+              }
             }
           }
           last_v = grab();
@@ -1011,7 +1164,7 @@ int64_t jacobi2_qbuf_elems(int np) {
 }
 int64_t jacobi2_qflag_elems(int np) {  // log flags + the dataflow pair flags
   const int npairs = std::max(np / J2_BW / 2, 1);
-  return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs + npairs + 2;
+  return (int64_t)(j2_use_log(np) ? jacobi2_log_steps(np) : 1) * npairs + 2 * npairs + 2;
 }
 
 static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
@@ -1033,9 +1186,9 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   // dataflow steps (see jacobi2_kernel) when the per-CTA item lists fit
   int dflow = 0;
   if (vlog && nb <= J2_DF_MAXB) dflow = 1;
-  if (const char* e = getenv("MLR_J2_DFLOW")) dflow = dflow && e[0] != '0';
+  if (const char* e = getenv("MLR_J2_DFLOW")) dflow = !dflow ? 0 : (e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1));
   const int max_items = dflow ? 0 : (nitems + nctas - 1) / nctas;
-  const size_t item_bytes = dflow ? (size_t)nitems + 16 : (size_t)max_items * 8;
+  const size_t item_bytes = dflow ? (size_t)nitems + 2 * (size_t)npairs + 32 : (size_t)max_items * 8;
   const size_t sched = (size_t)nb * npairs * sizeof(int) + item_bytes + (size_t)npairs * sizeof(int) + 64;
   const size_t qcache = (size_t)npairs * J2_PW * J2_LD * sizeof(double);
   const int cache_q = (!dflow && sizeof(J2Smem) + qcache + sched <= 200 * 1024) ? 1 : 0;
