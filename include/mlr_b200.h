@@ -105,6 +105,11 @@ int mlr_pcp_history(void* plan, int count, double* out, void* stream); /* count 
  * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize,
  * lanczos (sigma_1 estimate).  mlr_pcp_timing synchronises, returns total ms
  * and launch counts per phase (8 entries each) and resets the accumulators. */
+/* Truncated SVT of the full-width baseline ialm_solve (reference pcp.py:118-197,
+ * svd_truncated linalg.py:102-125): with sv0 > 0 only the top-sv singular values
+ * of each iteration take part and sv adapts (pcp.py:160-165), capped at cap.
+ * Call before mlr_pcp_start; sv0 = 0 restores the full SVT. */
+int mlr_pcp_set_truncation(void* plan, int sv0, int cap);
 int mlr_pcp_set_timing(void* plan, int enable);
 int mlr_pcp_timing(void* plan, double* ms8, int* counts8);
 

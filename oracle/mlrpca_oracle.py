@@ -32,6 +32,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 import scipy.linalg
+import scipy.sparse.linalg
 import scipy.sparse as sp
 
 # --------------------------------------------------------------------------
@@ -352,6 +353,93 @@ def ml_ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500,
             break
     return PcpResult(l_mat, s_mat, y, mu, k, hist, mus, done,
                      chain.n_coarse, float(sigma1))
+
+
+DENSE_SVD_LIMIT = 256   # linalg.py:16
+
+
+def svd_truncated(x, r):
+    """linalg.py:102-125: leading r triplets; dense LAPACK when
+    min(m, n) <= 256 or r >= min(m, n), else ARPACK (svds, v0 = ones)."""
+    x = as_matrix(x)
+    k = min(x.shape)
+    r = int(r)
+    if not 1 <= r <= k:
+        raise ValueError(f"rank must satisfy 1 <= r <= {k}, got {r}")
+    if k <= DENSE_SVD_LIMIT or r >= k:
+        u, s, v = svd_full(x)
+        return u[:, :r], s[:r], v[:, :r]
+    u, s, vt = scipy.sparse.linalg.svds(x, k=r, v0=np.ones(min(x.shape)))
+    order = np.argsort(s)[::-1]
+    u, v = u[:, order], vt[order].T
+    if u.shape[1]:
+        peak = np.argmax(np.abs(u), axis=0)
+        sgn = np.sign(u[peak, np.arange(u.shape[1])])
+        sgn[sgn == 0] = 1.0
+        u, v = u * sgn, v * sgn
+    return u, s[order], v
+
+
+def ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500, rank_guess=5,
+         svd_budget=None, time_budget=None):
+    """pcp.py:118-197 (ialm_solve): inexact ALM with the adaptive truncated SVD."""
+    d = as_matrix(d, "d")
+    m, n = d.shape
+    if np.linalg.norm(d, "fro") == 0.0:
+        z = np.zeros_like(d)
+        return PcpResult(z, z.copy(), z.copy(), 0.0, 1, [Record(1, 0.0, 0.0, 0, 0.0, 0.0)], [], True)
+    lam = lam if lam is not None else 1.0 / np.sqrt(max(m, n))     # pcp.py:99
+    sigma1 = np.linalg.norm(d, 2)                                  # pcp.py:100
+    mu = mu0 if mu0 is not None else 1.25 / sigma1                 # pcp.py:101
+    kmax = min(m, n)
+    cap = min(svd_budget or kmax, kmax)                            # pcp.py:132-133
+    d_norm = np.linalg.norm(d, "fro")
+    s_mat = np.zeros_like(d)
+    y = d / max(np.linalg.norm(d, 2), np.max(np.abs(d)) / lam)     # pcp.py:112-115
+    sv = min(rank_guess + 1, cap)                                  # pcp.py:138
+    work = np.empty_like(d)
+    hist, mus = [], []
+    done = False
+    t0 = time.perf_counter()
+    k = 0
+    l_mat = np.zeros_like(d)
+    for k in range(1, max_iters + 1):                              # pcp.py:145
+        mus.append(mu)
+        inv = 1.0 / mu
+        np.multiply(y, inv, out=work)
+        work += d
+        work -= s_mat
+        u, sig, v = svd_truncated(work, sv)                        # pcp.py:153
+        rank = int(np.count_nonzero(sig > inv))
+        if rank == 0:
+            l_mat = np.zeros_like(d)
+            nuc = 0.0
+        else:
+            shrunk = sig[:rank] - inv
+            l_mat = (u[:, :rank] * shrunk) @ v[:, :rank].T
+            nuc = float(np.sum(shrunk))
+        if sig[-1] > inv:                                          # pcp.py:160-165
+            sv = min(sv + 5, cap)
+        else:
+            sv = max(min(rank + 1, cap), 1)
+        np.multiply(y, inv, out=work)
+        work += d
+        work -= l_mat
+        s_mat = soft_threshold(work, lam * inv)
+        np.subtract(d, l_mat, out=work)
+        work -= s_mat
+        gap = float(np.linalg.norm(work, "fro") / d_norm)
+        work *= mu
+        y += work
+        mu *= rho
+        hist.append(Record(k, gap, nuc + lam * float(np.sum(np.abs(s_mat))), rank,
+                           float(np.count_nonzero(s_mat)) / (m * n), time.perf_counter() - t0))
+        if gap <= tol:
+            done = True
+            break
+        if time_budget is not None and hist[-1].wall_seconds >= time_budget:
+            break
+    return PcpResult(l_mat, s_mat, y, mu, k, hist, mus, done, n, float(sigma1))
 
 
 # --------------------------------------------------------------------------

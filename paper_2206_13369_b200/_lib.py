@@ -55,6 +55,7 @@ _SIGS = {
                                 c_void_p]),
     "mlr_pcp_state": (c_int, [c_void_p, c_void_p, c_void_p]),
     "mlr_pcp_history": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "mlr_pcp_set_truncation": (c_int, [c_void_p, c_int, c_int]),
     "mlr_pcp_set_timing": (c_int, [c_void_p, c_int]),
     "mlr_pcp_timing": (c_int, [c_void_p, c_void_p, c_void_p]),
     # ML-CPCP

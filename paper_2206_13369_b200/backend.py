@@ -116,6 +116,10 @@ class CudaPcp:
         _lib.check(self.lib.mlr_pcp_history(self.h, int(count), out.ctypes.data, _stream()))
         return out[:count]
 
+    def set_truncation(self, sv0, cap):
+        """Truncated SVT of the full-width ialm_solve (0 restores the full SVT)."""
+        _lib.check(self.lib.mlr_pcp_set_truncation(self.h, int(sv0), int(cap)))
+
     PHASES = ("gram", "pre", "jacobi", "post", "recon", "update", "finalize", "lanczos")
 
     def set_timing(self, on):

@@ -1,11 +1,10 @@
 """Run the reference command line (``mlrpca pcp | cpcp | compare``,
 reference cli.py:218-236, 336-361) on the B200 solvers.
 
-The reference CLI calls ``ml_ialm_solve``, ``fwt_solve`` and ``ml_fwt_solve``
-through names bound in its ``cli`` module; ``install`` rebinds the ones this
-package implements, so solver selection, ``.lrml`` I/O and the metrics CSV
-stay the reference's own.  ``ialm_solve`` (the full-width PCP baseline with
-ARPACK truncation) keeps its CPU implementation.
+The reference CLI calls ``ialm_solve``, ``ml_ialm_solve``, ``fwt_solve`` and
+``ml_fwt_solve`` through names bound in its ``cli`` module (cli.py:22-25);
+``install`` rebinds them to this package's implementations, so solver
+selection, ``.lrml`` I/O and the metrics CSV stay the reference's own.
 
     import mlrpca.cli
     from paper_2206_13369_b200 import cli_bridge
@@ -20,6 +19,7 @@ from __future__ import annotations
 from . import cpcp, pcp
 
 GPU_SOLVERS = {
+    "ialm_solve": pcp.ialm_solve,
     "ml_ialm_solve": pcp.ml_ialm_solve,
     "fwt_solve": cpcp.fwt_solve,
     "ml_fwt_solve": cpcp.ml_fwt_solve,

@@ -474,6 +474,15 @@ int mlr_pcp_state(void* plan, double* out16, void* stream) {
   std::memcpy(out16, v, sizeof(v));
   return kOk;
 }
+int mlr_pcp_set_truncation(void* plan, int sv0, int cap) {
+  if (sv0 < 0 || (sv0 > 0 && cap < 1)) {
+    set_error("mlr_pcp_set_truncation: invalid arguments");
+    return kErrArg;
+  }
+  PLAN->trunc_sv0 = sv0 > 0 ? std::min(sv0, cap) : 0;
+  PLAN->trunc_cap = cap;
+  return kOk;
+}
 int mlr_pcp_set_timing(void* plan, int enable) {
   PLAN->timer.on = enable != 0;
   return kOk;

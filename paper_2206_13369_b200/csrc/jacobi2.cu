@@ -1077,8 +1077,9 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
 // taking pairs w, w+16, ... with FP64 DMMA.  B fragments come straight from
 // L2 (each one feeds both 8-row groups); 16 warps keep enough loads in
 // flight to cover the L2 latency.
-constexpr int VA_R = 16, VA_THREADS = 512, VA_WARPS = VA_THREADS / 32;
+constexpr int VA_THREADS = 512, VA_WARPS = VA_THREADS / 32;
 
+template <int VA_R>  // rows of V per CTA: 16, or 8 when a 16-row tile does not fit
 __global__ void __launch_bounds__(VA_THREADS)
 j2_vapply_kernel(double* __restrict__ V, int np, int nrows_v, const double* __restrict__ Qlog, int cap,
                  const int* __restrict__ qflag_log, int* __restrict__ result, const int* __restrict__ skip) {
@@ -1144,7 +1145,8 @@ j2_vapply_kernel(double* __restrict__ V, int np, int nrows_v, const double* __re
   }
 }
 
-static size_t vapply_smem(int np) { return (size_t)VA_R * (np + 2) * sizeof(double); }
+static int vapply_rows(int np) { return (size_t)16 * (np + 2) * sizeof(double) <= 200 * 1024 ? 16 : 8; }
+static size_t vapply_smem(int np) { return (size_t)vapply_rows(np) * (np + 2) * sizeof(double); }
 
 // Rotation-log capacity in steps: whole sweeps, up to 60, within ~128 MB.
 int jacobi2_log_steps(int np) {
@@ -1233,7 +1235,11 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
     attr[0].val.cooperative = 1;
   }
   const size_t vsm = vapply_smem(np);
-  if (vlog) MLR_CUDA(cudaFuncSetAttribute(j2_vapply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+  const int var = vapply_rows(np);
+  if (vlog) {
+    MLR_CUDA(cudaFuncSetAttribute(j2_vapply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+    MLR_CUDA(cudaFuncSetAttribute(j2_vapply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+  }
   // the log holds cap / nb sweeps: enough (jacobi, V) launch pairs for max_sweeps;
   // launches after convergence return immediately
   const int per_launch = vlog ? std::max(1, cap / nb) : max_sweeps;
@@ -1246,8 +1252,12 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
       MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<false>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
                                   Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow));
     if (vlog) {
-      j2_vapply_kernel<<<(nrows_v + VA_R - 1) / VA_R, VA_THREADS, vsm, st>>>(V, np, nrows_v, Qlog, cap, qflag_log,
-                                                                            result, skip);
+      if (var == 16)
+        j2_vapply_kernel<16><<<(nrows_v + 15) / 16, VA_THREADS, vsm, st>>>(V, np, nrows_v, Qlog, cap, qflag_log,
+                                                                          result, skip);
+      else
+        j2_vapply_kernel<8><<<(nrows_v + 7) / 8, VA_THREADS, vsm, st>>>(V, np, nrows_v, Qlog, cap, qflag_log,
+                                                                        result, skip);
       MLR_LAUNCH_CHECK("j2_vapply_kernel");
     }
   }

@@ -487,7 +487,11 @@ __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double
 // ------------------------------------------------------------ scalars
 __global__ void pcp_start_scalars(PcpDev* st, const LanczosDev* lz, const double* __restrict__ in_stats,
                                   double lam, double mu0, double rho, double tol, int max_iters,
-                                  double time_budget, double jac_tol, double m_global, double n) {
+                                  double time_budget, double jac_tol, double m_global, double n, int sv0,
+                                  int sv_cap) {
+  st->trunc = sv0 > 0;
+  st->sv = sv0;
+  st->sv_cap = sv_cap;
   st->m_global = m_global;
   st->n = n;
   const double sumsq = in_stats[0], maxabs = in_stats[1];
@@ -794,7 +798,7 @@ int pcp_start(PcpPlan* p, const void* D, int64_t ldd, void* Y0, int64_t ldy, con
   // itself is only accurate to ~eps * |B| (FP64 accumulation of T-precision A)
   p->jac_floor_rel = p->f32 ? 1e-13 : 1e-17;
   pcp_start_scalars<<<1, 1, 0, st>>>(p->dev, p->lz, in_stats, lam, mu0, rho, tol, max_iters, time_budget, jac_tol,
-                                     (double)p->m_global, (double)p->ch.n);
+                                     (double)p->m_global, (double)p->ch.n, p->trunc_sv0, p->trunc_cap);
   MLR_LAUNCH_CHECK("pcp_start_scalars");
   MLR_CUDA(cudaMemsetAsync(p->hist, 0, sizeof(double) * kHistCols * p->max_iters, st));
   return p->f32 ? row_pass<float>(kStart, p, D, ldd, nullptr, Y0, ldy, nullptr, nullptr, 0, st)
@@ -843,6 +847,62 @@ int pcp_finalize(PcpPlan* p, const double* red, cudaStream_t st) {
   return kOk;
 }
 
+// Truncated SVT of ialm_solve (reference pcp.py:152-165): only the top-sv
+// singular values take part (svd_truncated returns sv triplets); rank counts
+// those above tau; sv adapts for the next iteration.  The sv-th largest
+// sigma is found exactly by a radix select over the bit patterns
+// (non-negative doubles order like their bits).
+__global__ void __launch_bounds__(1024) svt_weights_trunc_kernel(PcpDev* __restrict__ st, int np, int nh,
+                                                                  const double* __restrict__ Bd,
+                                                                  double* __restrict__ sig_out,
+                                                                  double* __restrict__ f_out) {
+  if (st->done) return;
+  __shared__ double scratch[2 * 32];
+  __shared__ unsigned long long key_s;
+  __shared__ int cnt_s;
+  const double tau = st->tau;
+  const int sv = min(st->sv, nh);
+  // sigma_i = sqrt(lambda_i) (i < nh), as bit patterns
+  unsigned long long prefix = 0ull;
+  for (int bit = 63; bit >= 0; --bit) {
+    const unsigned long long cand = prefix | (1ull << bit);
+    int c = 0;
+    for (int i = threadIdx.x; i < nh; i += blockDim.x) {
+      const double s = sqrt(fmax(Bd[(int64_t)i * (np + 1)], 0.0));
+      c += (unsigned long long)__double_as_longlong(s) >= cand ? 1 : 0;
+    }
+    double v[2] = {(double)c, 0.0};
+    block_sum<2>(v, scratch);
+    if (threadIdx.x == 0) cnt_s = (int)(v[0] + 0.5);
+    __syncthreads();
+    if (cnt_s >= sv) prefix = cand;  // at least sv values >= cand: the sv-th largest has this bit
+    __syncthreads();
+  }
+  const double s_sv = __longlong_as_double((long long)prefix);  // the sv-th largest sigma
+  double nuc = 0.0, rk = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    double f = 0.0, s = 0.0;
+    if (i < nh) {
+      s = sqrt(fmax(Bd[(int64_t)i * (np + 1)], 0.0));
+      if (s >= s_sv && s > tau) {
+        f = (s - tau) / s;
+        nuc += s - tau;
+        rk += 1.0;
+      }
+    }
+    if (sig_out) sig_out[i] = s;
+    f_out[i] = f;
+  }
+  double v[2] = {nuc, rk};
+  block_sum<2>(v, scratch);
+  if (threadIdx.x == 0) {
+    st->nuclear = v[0];
+    st->rank = (int)(v[1] + 0.5);
+    // widen when the truncation clipped values above the threshold (pcp.py:160-163)
+    st->sv = s_sv > tau ? min(st->sv + 5, st->sv_cap) : max(min(st->rank + 1, st->sv_cap), 1);
+  }
+}
+
 // Coarse SVT from the (all-reduced) Gram in red: B = G^-1 K G^-1; Jacobi
 // on X = B V (warm start V); W~ = G^-1 V diag(f) V^T; Z = A W~.
 int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
@@ -874,9 +934,13 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   pcp_after_jacobi<<<1, 1, 0, st>>>(p->dev, p->jac_result);
   MLR_LAUNCH_CHECK("pcp_after_jacobi");
   // lambda_i = diag(B~) after convergence; f_i = (sigma_i - tau)+ / sigma_i
-  if ((rc = svt_weights(skip, np, p->ch.nh, false, p->Bm, &p->dev->tau, p->sig, p->fw, &p->dev->rank,
-                        &p->dev->nuclear, st)))
+  if (p->trunc_sv0 > 0) {
+    svt_weights_trunc_kernel<<<1, 1024, 0, st>>>(p->dev, np, p->ch.nh, p->Bm, p->sig, p->fw);
+    MLR_LAUNCH_CHECK("svt_weights_trunc_kernel");
+  } else if ((rc = svt_weights(skip, np, p->ch.nh, false, p->Bm, &p->dev->tau, p->sig, p->fw, &p->dev->rank,
+                               &p->dev->nuclear, st))) {
     return rc;
+  }
   // W~ = G^-1 V diag(f) V^T = U' diag(f) V^T with U' = G^-1 V
   if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;
   if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw))) return rc;

@@ -27,6 +27,7 @@ struct PcpDev {
   int rank;
   int max_iters;
   int jac_sweeps;
+  int trunc, sv, sv_cap;  // ialm_solve: keep only the top-sv triplets, adapt sv (pcp.py:157-165)
 };
 
 struct LanczosDev {
@@ -46,6 +47,7 @@ struct PcpPlan {
   double jac_tol_host;
   double jac_floor_rel;
   int jac_max_sweeps;
+  int trunc_sv0, trunc_cap;  // > 0: truncated SVT (full-width ialm_solve)
   // device buffers (carved from the caller's workspace)
   PcpDev* dev;
   LanczosDev* lz;

@@ -1,4 +1,5 @@
-"""ML-PCP drop-in: ``ml_ialm_solve`` (reference pcp.py:213-309) on B200.
+"""ML-PCP drop-in: ``ml_ialm_solve`` (reference pcp.py:213-309) and the
+full-width ``ialm_solve`` (pcp.py:118-197) on B200.
 
 The host loop mirrors the reference's structure and stopping rules; every
 arithmetic step runs in the CUDA library.  Per iteration the host enqueues
@@ -135,6 +136,54 @@ def ml_ialm_solve(d, opts=None):
             be.close()
     if out is None:
         return _zero_state(tuple(D.shape), kind, D)
+    return _state_from(*out, kind)
+
+
+def ialm_solve(d, opts=None):
+    """Full-width inexact ALM (drop-in for mlrpca.ialm_solve, reference
+    pcp.py:118-197).
+
+    Runs the ML-PCP device loop on the identity chain (n_H = n, so the
+    restriction is exact) with the truncated SVT enabled: only the top ``sv``
+    singular values take part, and ``sv`` adapts each iteration exactly as
+    the reference's svd_truncated bookkeeping does (pcp.py:132-138,
+    160-165).  PCP is transpose-symmetric (lam, mu0, the dual start and both
+    shrinkages are), so a wide ``d`` is solved as its transpose and the
+    Gram stays min(m, n) square.
+    """
+    D, kind = as_device_matrix(d, "d")
+    m, n = D.shape
+    opts = opts if opts is not None else PcpOptions()
+    lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m, n))
+    wide = n > m
+    if wide:
+        D = D.t().contiguous()
+        m, n = n, m
+    kmax = n
+    cap = min(opts.svd_budget or kmax, kmax)
+    sv0 = min(opts.rank_guess + 1, cap)
+    with torch.cuda.device(D.device):
+        chain = build_chain(n, n)
+        be = CudaPcp(chain, m, m, D.dtype == torch.float32, opts.max_iters, D.device)
+        be.set_truncation(sv0, cap)
+        if TIMING_SINK is not None:
+            be.set_timing(True)
+        try:
+            out = run_ialm(be, SINGLE, D, m, n, opts, lam, _check_every(opts))
+            if TIMING_SINK is not None:
+                t = be.timing()
+                t["iters"] = out[3]["k"] if out is not None else 0
+                t["jac_sweeps"] = [int(x) for x in out[4][:, 6]] if out is not None else []
+                t["lanczos_steps"] = be.lanczos_state()["k"] + 1
+                TIMING_SINK.append(t)
+        finally:
+            be.close()
+    if out is None:
+        shape = (n, m) if wide else (m, n)
+        return _zero_state(shape, kind, D)
+    if wide:
+        L, S, Yk, st, hist = out
+        out = (L.t().contiguous(), S.t().contiguous(), Yk.t().contiguous(), st, hist)
     return _state_from(*out, kind)
 
 

@@ -106,6 +106,33 @@ def pcp_c1_summary():
         rows=rows, sigma1=np.array(np.linalg.norm(d, 2)), **hist_arrays(st.history))
 
 
+def ialm_cases():
+    """Full-width inexact ALM (mlrpca.ialm_solve, pcp.py:118-197): dense SVD
+    below min(m, n) = 256, ARPACK above it, a wide input and a clipped
+    svd_budget."""
+    cases = {
+        # name: (m, n, rank, eta, seed, tol, svd_budget, dtype, full arrays)
+        "ialm_f64_dense": (120, 100, 5, 0.10, 21, 1e-7, None, np.float64, True),
+        "ialm_f32_dense": (150, 128, 6, 0.10, 22, 1e-6, None, np.float32, True),
+        "ialm_f64_wide": (80, 110, 4, 0.10, 23, 1e-7, None, np.float64, True),
+        "ialm_f64_budget": (100, 90, 8, 0.10, 24, 1e-7, 6, np.float64, True),
+        "ialm_f64_arpack": (300, 280, 6, 0.10, 25, 1e-7, None, np.float64, False),
+    }
+    for name, (m, n, r, eta, seed, tol, budget, dt, full) in cases.items():
+        d, _ = O.gaussian_rpca(m, n, r, eta, seed)
+        d = d.astype(dt).astype(np.float64)
+        st = mlrpca.ialm_solve(d, mlrpca.PcpOptions(tol_feasibility=tol, svd_budget=budget))
+        rows = np.arange(0, m, 17)
+        arrays = dict(l=st.l, s=st.s, y=st.y) if full else dict(l_rows=st.l[rows], s_rows=st.s[rows], rows=rows)
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), d=d if full else np.zeros(0), seed=np.array(seed),
+            shape=np.array([m, n, r]), eta=np.array(eta), mu=np.array(st.mu), iter=np.array(st.iter),
+            tol=np.array(tol), svd_budget=np.array(budget or 0), converged=np.array(st.converged),
+            l_fro=np.array(np.linalg.norm(st.l)), s_fro=np.array(np.linalg.norm(st.s)),
+            y_fro=np.array(np.linalg.norm(st.y)), mu_history=np.array(st.mu_history),
+            **arrays, **hist_arrays(st.history))
+
+
 def fwt_cases():
     cases = {
         # name: (m, n, rank, eta, observe, seed, n_H, tol, max_iters, dtype)
@@ -169,6 +196,7 @@ if __name__ == "__main__":
     linalg_kats()
     pcp_cases()
     pcp_c1_summary()
+    ialm_cases()
     fwt_cases()
     fwt_full_cases()
     print("golden vectors written to", HERE)

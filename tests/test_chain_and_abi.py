@@ -119,6 +119,6 @@ def test_cli_bridge_rebinds_and_restores():
     prev = cli_bridge.install(mod)
     assert mod.ml_ialm_solve is pcp.ml_ialm_solve
     assert mod.fwt_solve is cpcp.fwt_solve and mod.ml_fwt_solve is cpcp.ml_fwt_solve
-    assert mod.ialm_solve is cpu  # full-width PCP stays on the CPU
+    assert mod.ialm_solve is pcp.ialm_solve
     cli_bridge.uninstall(mod, prev)
-    assert mod.ml_ialm_solve is cpu and mod.fwt_solve is cpu and mod.ml_fwt_solve is cpu
+    assert mod.ialm_solve is cpu and mod.ml_ialm_solve is cpu and mod.fwt_solve is cpu and mod.ml_fwt_solve is cpu

@@ -116,6 +116,50 @@ def test_ml_ialm_identity_chain_and_select_levels():
     assert st.iter == ref.iter and relf(st.l, ref.l) <= 1e-10
 
 
+# ------------------------------------------------------------------ full-width PCP
+@pytest.mark.parametrize("name,tolrel", [("ialm_f64_dense", 1e-10), ("ialm_f32_dense", 1e-4),
+                                          ("ialm_f64_wide", 1e-10), ("ialm_f64_budget", 1e-10),
+                                          ("ialm_f64_arpack", 1e-10)])
+def test_ialm_golden(golden, name, tolrel):
+    """ialm_solve (reference pcp.py:118-197) against the reference's own output;
+    the arpack case (min(m, n) > 256) checks fingerprints plus the oracle."""
+    g = golden(name)
+    if g["d"].size:
+        d = g["d"]
+    else:
+        m, n, r = (int(x) for x in g["shape"])
+        d = O.gaussian_rpca(m, n, r, float(g["eta"]), int(g["seed"]))[0]
+    if "f32" in name:
+        d = d.astype(np.float32)
+    budget = int(g["svd_budget"]) or None
+    st = pkg.ialm_solve(d, pkg.PcpOptions(tol_feasibility=float(g["tol"]), svd_budget=budget))
+    assert abs(st.iter - int(g["iter"])) <= 1
+    assert st.converged == bool(g["converged"])
+    if "l" in g:
+        assert relf(st.l, g["l"]) <= tolrel
+        assert relf(st.s, g["s"]) <= tolrel
+    else:
+        assert relf(st.l[g["rows"]], g["l_rows"]) <= tolrel
+        ref = O.ialm(d, tol=float(g["tol"]))
+        assert relf(st.l, ref.l) <= tolrel and relf(st.s, ref.s) <= tolrel
+    if st.iter == int(g["iter"]):
+        assert [h.rank_l for h in st.history] == list(g["h_rank"])
+        assert np.isclose(st.mu, float(g["mu"]), rtol=1e-12)
+
+
+def test_ialm_edge_cases():
+    z = pkg.ialm_solve(np.zeros((12, 20)))
+    assert z.converged and z.iter == 1 and z.l.shape == (12, 20) and np.all(z.l == 0)
+    with pytest.raises(ValueError, match="non-finite"):
+        pkg.ialm_solve(np.full((10, 10), np.nan))
+    d, _ = O.gaussian_rpca(40, 64, 3, 0.1, 31)
+    st = pkg.ialm_solve(d, pkg.PcpOptions(max_iters=3, tol_feasibility=1e-14, rank_guess=1, svd_budget=2))
+    ref = O.ialm(d, max_iters=3, tol=1e-14, rank_guess=1, svd_budget=2)
+    assert st.iter == 3 and not st.converged and st.l.shape == (40, 64)
+    assert [h.rank_l for h in st.history] == [h.rank_l for h in ref.history]
+    assert relf(st.l, ref.l) <= 1e-10 and relf(st.y, ref.y) <= 1e-10
+
+
 # ------------------------------------------------------------------ ML-CPCP
 @pytest.mark.parametrize("name", ["fwt_f64_small", "fwt_f32_small", "fwt_f64_full"])
 def test_ml_fwt_golden_envelope(golden, name):

@@ -142,6 +142,33 @@ def test_golden_fwt_full(golden, name):
     assert_allclose(st.objective_history[:k], g["h_obj"][:k], rtol=1e-6)
 
 
+IALM_CASES = ["ialm_f64_dense", "ialm_f32_dense", "ialm_f64_wide", "ialm_f64_budget", "ialm_f64_arpack"]
+
+
+def _ialm_input(g):
+    if g["d"].size:
+        return g["d"]
+    m, n, r = (int(x) for x in g["shape"])
+    return O.gaussian_rpca(m, n, r, float(g["eta"]), int(g["seed"]))[0]
+
+
+@pytest.mark.parametrize("name", IALM_CASES)
+def test_golden_ialm(golden, name):
+    """Full-width IALM (reference ialm_solve, pcp.py:118-197): dense SVD at
+    min(m, n) <= 256, ARPACK above, wide input, clipped svd_budget."""
+    g = golden(name)
+    st = O.ialm(_ialm_input(g), tol=float(g["tol"]), svd_budget=int(g["svd_budget"]) or None)
+    assert st.iter == int(g["iter"])
+    assert [h.rank_l for h in st.history] == list(g["h_rank"])
+    assert_allclose([h.feasibility_gap for h in st.history], g["h_gap"], rtol=1e-8)
+    if "l" in g:
+        assert_allclose(st.l, g["l"], rtol=0, atol=1e-11 * np.abs(g["l"]).max())
+        assert_allclose(st.s, g["s"], rtol=0, atol=1e-11 * np.abs(g["s"]).max())
+    else:
+        assert_allclose(st.l[g["rows"]], g["l_rows"], rtol=0, atol=1e-10 * np.abs(g["l_rows"]).max())
+        assert_allclose(np.linalg.norm(st.l), float(g["l_fro"]), rtol=1e-11)
+
+
 def test_golden_c1_summary(golden):
     g = golden("pcp_c1_summary")
     d, _ = O.make_config("C1", 0)
