@@ -101,15 +101,15 @@ int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, 
 /* out16: k, done, status, rank, mu, mu_final, mu_last, nuclear, sigma1, d_norm, jac_sweeps, tau, scale, lam, 0, 0 */
 int mlr_pcp_state(void* plan, double* out16, void* stream);
 int mlr_pcp_history(void* plan, int count, double* out, void* stream); /* count x 8 */
-/* Per-phase CUDA-event timing: phases gram, pre (B, X=BV), jacobi, post
- * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize,
- * lanczos (sigma_1 estimate).  mlr_pcp_timing synchronises, returns total ms
- * and launch counts per phase (8 entries each) and resets the accumulators. */
 /* Truncated SVT of the full-width baseline ialm_solve (reference pcp.py:118-197,
  * svd_truncated linalg.py:102-125): with sv0 > 0 only the top-sv singular values
  * of each iteration take part and sv adapts (pcp.py:160-165), capped at cap.
  * Call before mlr_pcp_start; sv0 = 0 restores the full SVT. */
 int mlr_pcp_set_truncation(void* plan, int sv0, int cap);
+/* Per-phase CUDA-event timing: phases gram, pre (B, X=BV), jacobi, post
+ * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize,
+ * lanczos (sigma_1 estimate).  mlr_pcp_timing synchronises, returns total ms
+ * and launch counts per phase (8 entries each) and resets the accumulators. */
 int mlr_pcp_set_timing(void* plan, int enable);
 int mlr_pcp_timing(void* plan, double* ms8, int* counts8);
 
@@ -137,6 +137,52 @@ int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, voi
 /* Per-phase CUDA-event timing (8 slots: gram, power, dots, qp, -, update, finalize, -). */
 int mlr_cpcp_set_timing(void* plan, int enable);
 int mlr_cpcp_timing(void* plan, double* ms8, int* counts8);
+
+/* ---------------------------------------------------------------- telemetry
+ * Numerical-rank telemetry of the reference (collect_rank, cpcp.py:434-439;
+ * collect_diagnostics, pcp.py:298-306 with epsilon_bound multilevel.py:248-265).
+ *
+ * Spectrum plan: singular values of a row-sharded X (m_local x n, T = f32 ? float
+ * : double), or of X C for a fixed n x n double factor C (NULL = identity), in two
+ * passes accurate to ~eps * sigma_1 (one Gram eigensolve resolves only
+ * ~sqrt(eps) * sigma_1, far above the reference's max(m, n) * eps threshold):
+ *   gram   red  = X^T X (this rank's rows)              [allreduce red]
+ *   rotate V1 = eig(C^T red C) (warm-started); B = X C V1; red2 = B^T B  [allreduce red2]
+ *   finish sigma = sqrt(eig(red2)) sorted descending; rank = #{sigma > sigma_1 * rel};
+ *          wsum = sum_{k < rank} sigma_k * pair_w[k] (pair_w may be NULL)
+ * skip: optional device int; every step is a no-op while it is nonzero.
+ * red / red2 hold mlr_spec_red_doubles(plan) doubles; outputs are device pointers. */
+int64_t mlr_spec_workspace_bytes(int64_t m_local, int n);
+int mlr_spec_create(int64_t m_local, int n, int f32, const double* C, int64_t ldc, const int* skip, void* workspace,
+                    void** plan_out, void* stream);
+int mlr_spec_destroy(void* plan);
+int64_t mlr_spec_red_doubles(void* plan);
+int mlr_spec_gram(void* plan, const void* X, int64_t ldx, double* red, void* stream);
+int mlr_spec_rotate(void* plan, const void* X, int64_t ldx, const double* red, double* red2, void* stream);
+int mlr_spec_finish(void* plan, const double* red2, double rel, double* sig_out, double* rank_out,
+                    const double* pair_w, double* wsum_out, void* stream);
+/* Dense lower Cholesky factor C of G_R = R^T R (n_H x n_H, C C^T = G_R): sigma(L_H R^T) = sigma(L_H C). */
+int mlr_chain_cholesky(void* chain, double* C, int64_t ldc, void* stream);
+/* ML-PCP coarse iterate L_H = Z (m_local x n_H, the plan's dtype) of the latest SVT step. */
+int mlr_pcp_coarse_copy(void* plan, void* out, int64_t ldo, void* stream);
+/* delta = <Z_k (G_R - I), Z_k - Z_f G_R> over this rank's rows (pcp.py:300-302);
+ * work holds mlr_pcp_delta_work_doubles() doubles; out is one device double. */
+int64_t mlr_pcp_delta_work_doubles(void);
+int mlr_pcp_delta(void* plan, const void* Zk, const void* Zf, int64_t ldz, double* out, double* work, void* stream);
+/* ML-CPCP rank binding: the coarse iterate L_H (m_local x n_p, ld n_p), the plan's
+ * device stop flag (use as the spectrum plan's skip) and the device slot the
+ * finalize step records as the iteration's rank_l (-1 unless written). */
+int mlr_cpcp_rank_binding(void* plan, const void** lh, int64_t* ld, const int** done, double** rank_slot);
+/* FP32 plans: apply this iteration's rank-1 update (cpcp.py:399-402) to an FP64
+ * shadow L64 (m_local x n_H, ld >= n_H, zeroed before the first iteration) so the
+ * rank is taken of the unrounded iterate, like the reference's float64 run.
+ * Call after mlr_cpcp_update. */
+int mlr_cpcp_rank_shadow(void* plan, double* L64, int64_t ld, void* stream);
+/* track_oracle_atoms (cpcp.py:355-360): after mlr_cpcp_lmo, copy the iteration's
+ * LMO factors (u: m_local doubles, v: n_H doubles); later expand one saved pair
+ * into the dense atom M_L = -radius u (R v)^T (m_local x n float64, ld ldo). */
+int mlr_cpcp_atom_copy(void* plan, double* u_out, double* v_out, void* stream);
+int mlr_cpcp_atom_dense(void* plan, const double* u, const double* v, double* out, int64_t ldo, void* stream);
 
 #ifdef __cplusplus
 }

@@ -265,6 +265,17 @@ class PcpResult:
     converged: bool
     n_coarse: int = 0
     sigma1: float = 0.0
+    diagnostics: tuple = None   # (epsilon, delta_history) with collect_diagnostics
+
+
+def epsilon_bound(l_h, chain):
+    """multilevel.py:248-265: sum_k sigma_k(L_H) (1 - sigma_{n_H-k+1}(R)), k <= rank(L_H)."""
+    s_l = svd_full(as_matrix(l_h))[1]
+    r_h = int(np.count_nonzero(s_l > s_l[0] * max(l_h.shape) * np.finfo(float).eps))
+    if r_h == 0:
+        return 0.0
+    s_r = chain.composite_sigmas()
+    return float(np.sum(s_l[:r_h] * (1.0 - s_r[::-1][:r_h])))
 
 
 def _coarse_width(n, m, levels, rank_guess):
@@ -279,7 +290,7 @@ def _coarse_width(n, m, levels, rank_guess):
 
 
 def ml_ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500,
-            rank_guess=5, levels=None, time_budget=None):
+            rank_guess=5, levels=None, time_budget=None, collect_diagnostics=False):
     """pcp.py:213-309 (ml_ialm_solve) with pcp.py:95-115 inlined.
 
     Returns PcpResult.  Option validation follows pcp.py:42-54.
@@ -312,11 +323,12 @@ def ml_ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500,
     s_mat = np.zeros_like(d)
     y = d / max(np.linalg.norm(d, 2), np.max(np.abs(d)) / lam)     # pcp.py:112-115
     buf = np.empty_like(d)
-    hist, mus = [], []
+    hist, mus, iterates = [], [], []
     done = False
     t0 = time.perf_counter()
     k = 0
     l_mat = np.zeros_like(d)
+    l_h = np.zeros((m, chain.n_coarse))
     for k in range(1, max_iters + 1):                              # pcp.py:248
         mus.append(mu)
         inv = 1.0 / mu
@@ -327,12 +339,16 @@ def ml_ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500,
         u_h, sig, v_h = svd_full(m_h)                              # pcp.py:257
         rank = int(np.count_nonzero(sig > inv))                    # pcp.py:258
         if rank == 0:
+            l_h = np.zeros((m, chain.n_coarse))
             l_mat = np.zeros_like(d)
             nuc = 0.0
         else:
             kept = sig[:rank] - inv
-            l_mat = ((u_h[:, :rank] * kept) @ v_h[:, :rank].T) @ rd.T
+            l_h = (u_h[:, :rank] * kept) @ v_h[:, :rank].T
+            l_mat = l_h @ rd.T
             nuc = float(np.sum(kept))
+        if collect_diagnostics:                                    # pcp.py:268-269
+            iterates.append(l_h)
         np.multiply(y, inv, out=buf)                               # pcp.py:272-275
         buf += d
         buf -= l_mat
@@ -351,8 +367,14 @@ def ml_ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500,
             break
         if time_budget is not None and hist[-1].wall_seconds >= time_budget:
             break
+    diag = None
+    if collect_diagnostics:                                        # pcp.py:298-306
+        ref = restrict(l_mat, chain)
+        drift = (chain.composite.T @ chain.composite).toarray() - np.eye(chain.n_coarse)
+        deltas = [float(np.sum((lh @ drift) * (lh - ref))) for lh in iterates]
+        diag = (epsilon_bound(l_h, chain) if np.any(l_h) else 0.0, deltas)
     return PcpResult(l_mat, s_mat, y, mu, k, hist, mus, done,
-                     chain.n_coarse, float(sigma1))
+                     chain.n_coarse, float(sigma1), diag)
 
 
 DENSE_SVD_LIMIT = 256   # linalg.py:16
@@ -543,6 +565,7 @@ class CpcpResult:
     converged: bool
     n_coarse: int = 0
     power_passes: list | None = None
+    oracle_atoms: list | None = None
 
 
 def _converged(objs, tol, window=5):
@@ -554,7 +577,7 @@ def _converged(objs, tol, window=5):
 
 
 def ml_fwt(d, observed, lambda_l, lambda_s, tol=1e-3, max_iters=2000,
-           rank_guess=5, levels=None, time_budget=None, collect_rank=True):
+           rank_guess=5, levels=None, time_budget=None, collect_rank=True, track_oracle_atoms=False):
     """cpcp.py:480-515 (ml_fwt_solve) driving cpcp.py:326-456 (_run_fwt).
 
     ``observed`` is a boolean m x n array or None (fully observed).
@@ -605,8 +628,11 @@ def ml_fwt(d, observed, lambda_l, lambda_s, tol=1e-3, max_iters=2000,
     np.negative(r, out=r)
     done = False
     k = 0
+    atoms = [] if track_oracle_atoms else None                   # cpcp.py:355
     for k in range(1, max_iters + 1):                             # cpcp.py:357
         m_l, val_l = lmo(r)
+        if atoms is not None:                                     # cpcp.py:359-360
+            atoms.append(m_l.copy())
         i_s, j_s = l1_argmax(r)
         val_s = -abs(float(r[i_s, j_s]))
         cl = lambda_l < -val_l                                    # cpcp.py:365-368
@@ -679,7 +705,7 @@ def ml_fwt(d, observed, lambda_l, lambda_s, tol=1e-3, max_iters=2000,
         if time_budget is not None and hist[-1].wall_seconds >= time_budget:
             break
     return CpcpResult(l, s, t_l, t_s, u_l, u_s, k, hist, objs, done, nh,
-                      triple.passes)
+                      triple.passes, atoms)
 
 
 # --------------------------------------------------------------------------

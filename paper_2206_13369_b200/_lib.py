@@ -77,6 +77,23 @@ _SIGS = {
     "mlr_cpcp_history": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "mlr_cpcp_set_timing": (c_int, [c_void_p, c_int]),
     "mlr_cpcp_timing": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mlr_spec_workspace_bytes": (c_int64, [c_int64, c_int]),
+    "mlr_spec_create": (c_int, [c_int64, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p, POINTER(c_void_p),
+                                c_void_p]),
+    "mlr_spec_destroy": (c_int, [c_void_p]),
+    "mlr_spec_red_doubles": (c_int64, [c_void_p]),
+    "mlr_spec_gram": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "mlr_spec_rotate": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "mlr_spec_finish": (c_int, [c_void_p, c_void_p, c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mlr_chain_cholesky": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "mlr_pcp_coarse_copy": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "mlr_pcp_delta_work_doubles": (c_int64, []),
+    "mlr_pcp_delta": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "mlr_cpcp_rank_shadow": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "mlr_cpcp_atom_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mlr_cpcp_atom_dense": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+    "mlr_cpcp_rank_binding": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_int64), POINTER(c_void_p),
+                                      POINTER(c_void_p)]),
 }
 
 EXPORTED = tuple(_SIGS)

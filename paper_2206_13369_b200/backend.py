@@ -31,6 +31,7 @@ class CudaPcp:
         self.device = torch.device(device)
         self.f32 = bool(f32)
         self.n = chain.n_fine
+        self.nh = chain.n_coarse
         self.m_local = int(m_local)
         self.max_iters = int(max_iters)
         self.chain_h = chain.device_handle(self.device.index)
@@ -116,6 +117,15 @@ class CudaPcp:
         _lib.check(self.lib.mlr_pcp_history(self.h, int(count), out.ctypes.data, _stream()))
         return out[:count]
 
+    def coarse_copy(self, out):
+        """out (m_local x n_H) <- the latest coarse iterate L_H = Z."""
+        _lib.check(self.lib.mlr_pcp_coarse_copy(self.h, _ptr(out), out.stride(0), _stream()))
+
+    def delta(self, Zk, Zf, out, work):
+        """out (one device double) <- <Z_k (G - I), Z_k - Z_f G> over this rank's rows."""
+        _lib.check(self.lib.mlr_pcp_delta(self.h, _ptr(Zk), _ptr(Zf), Zk.stride(0), _ptr(out), _ptr(work),
+                                          _stream()))
+
     def set_truncation(self, sv0, cap):
         """Truncated SVT of the full-width ialm_solve (0 restores the full SVT)."""
         _lib.check(self.lib.mlr_pcp_set_truncation(self.h, int(sv0), int(cap)))
@@ -144,6 +154,7 @@ class CudaCpcp:
         self.device = torch.device(device)
         self.f32 = bool(f32)
         self.n = chain.n_fine
+        self.nh = chain.n_coarse
         self.m_local = int(m_local)
         self.max_iters = int(max_iters)
         self.chain_h = chain.device_handle(self.device.index)
@@ -226,6 +237,23 @@ class CudaCpcp:
         _lib.check(self.lib.mlr_cpcp_timing(self.h, ms.ctypes.data, cnt.ctypes.data))
         return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES) if not p.startswith("unused")}
 
+    def rank_binding(self):
+        """(L_H pointer, its leading dimension, device stop flag, rank slot)."""
+        lh, done, slot = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        ld = ctypes.c_int64()
+        _lib.check(self.lib.mlr_cpcp_rank_binding(self.h, ctypes.byref(lh), ctypes.byref(ld), ctypes.byref(done),
+                                                  ctypes.byref(slot)))
+        return lh.value, ld.value, done.value, slot.value
+
+    def atom_copy(self, u, v):
+        _lib.check(self.lib.mlr_cpcp_atom_copy(self.h, _ptr(u), _ptr(v), _stream()))
+
+    def atom_dense(self, u, v, out):
+        _lib.check(self.lib.mlr_cpcp_atom_dense(self.h, _ptr(u), _ptr(v), _ptr(out), out.stride(0), _stream()))
+
+    def rank_shadow(self, L64):
+        _lib.check(self.lib.mlr_cpcp_rank_shadow(self.h, _ptr(L64), L64.stride(0), _stream()))
+
     def history(self, count):
         out = np.zeros((max(count, 1), 8))
         objs = np.zeros(max(count, 1))
@@ -234,3 +262,54 @@ class CudaCpcp:
 
     def empty(self, shape, dtype):
         return torch.empty(shape, dtype=dtype, device=self.device)
+
+
+class CudaSpectrum:
+    """Two-pass singular values of a row-sharded tall X (or X C) for the
+    reference's numerical-rank telemetry (spectrum plan of the C ABI)."""
+
+    def __init__(self, m_local, n, f32, device, C=None, skip_ptr=None):
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        lib = self.lib
+        nbytes = lib.mlr_spec_workspace_bytes(int(m_local), int(n))
+        if nbytes < 0:
+            raise _lib.MlrError("mlr_spec_workspace_bytes failed")
+        self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p()
+        _lib.check(lib.mlr_spec_create(int(m_local), int(n), int(bool(f32)), _ptr(C), C.stride(0) if C is not None else 0,
+                                       ctypes.c_void_p(skip_ptr or 0), _ptr(self.ws), ctypes.byref(h), _stream()))
+        self.h = h
+        nn = int(lib.mlr_spec_red_doubles(h))
+        self.np_ = int(round(nn ** 0.5))
+        self.red = torch.zeros(nn, dtype=torch.float64, device=self.device)
+        self.red2 = torch.zeros(nn, dtype=torch.float64, device=self.device)
+        self.C = C  # keep alive until spec_init's copy has run
+
+    def close(self):
+        if self.h is not None:
+            self.lib.mlr_spec_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def gram(self, x_ptr, ldx):
+        _lib.check(self.lib.mlr_spec_gram(self.h, ctypes.c_void_p(x_ptr), int(ldx), _ptr(self.red), _stream()))
+
+    def rotate(self, x_ptr, ldx):
+        _lib.check(self.lib.mlr_spec_rotate(self.h, ctypes.c_void_p(x_ptr), int(ldx), _ptr(self.red),
+                                            _ptr(self.red2), _stream()))
+
+    def finish(self, rel, sig_out=None, rank_ptr=None, pair_w=None, wsum_out=None):
+        _lib.check(self.lib.mlr_spec_finish(self.h, _ptr(self.red2), float(rel), _ptr(sig_out),
+                                            ctypes.c_void_p(rank_ptr or 0), _ptr(pair_w), _ptr(wsum_out),
+                                            _stream()))
+
+
+def chain_cholesky(chain, device):
+    """Dense lower Cholesky factor of R^T R on the device (n_H x n_H, float64)."""
+    lib = _lib.load()
+    h = chain.device_handle(torch.device(device).index)
+    C = torch.empty((chain.n_coarse, chain.n_coarse), dtype=torch.float64, device=device)
+    _lib.check(lib.mlr_chain_cholesky(h, _ptr(C), C.stride(0), _stream()))
+    return C

@@ -126,6 +126,15 @@ class Chain:
         g = np.diag(self.g_diag) + np.diag(self.g_off, 1) + np.diag(self.g_off, -1)
         return float(np.sqrt(max(np.linalg.eigvalsh(g)[-1], 0.0)))
 
+    def composite_sigmas(self):
+        """All singular values of R, descending (multilevel.py:90-95); from the
+        tridiagonal R^T R (host-side chain setup, like sigma_max)."""
+        if self.n_coarse == self.n_fine and not np.any(self.g_off) and np.all(self.g_diag == 1.0):
+            return np.ones(self.n_coarse)
+        from scipy.linalg import eigvalsh_tridiagonal
+        lam = eigvalsh_tridiagonal(self.g_diag, self.g_off) if self.n_coarse > 1 else self.g_diag.copy()
+        return np.sqrt(np.maximum(lam, 0.0))[::-1].copy()
+
     def device_handle(self, device_index):
         """Chain tables on the given CUDA device (uploaded once, cached)."""
         h = self._dev.get(device_index)

@@ -10,13 +10,12 @@ and the 5-iteration convergence window all run on the device.
 from __future__ import annotations
 
 import dataclasses
-import warnings
 
 import numpy as np
 import torch
 
 from .api_types import CpcpOptions, CpcpState, IterationRecord, ObservationMask
-from .backend import CudaCpcp
+from .backend import CudaCpcp, CudaSpectrum, chain_cholesky
 from .chain import build_chain, resolve_coarse_width
 from .runtime import SINGLE, Comm, as_device_matrix, give_back
 
@@ -25,7 +24,48 @@ from .runtime import SINGLE, Comm, as_device_matrix, give_back
 TIMING_SINK = None
 
 
-def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every):
+class RankProbe:
+    """collect_rank (reference cpcp.py:434-439): the numerical rank of the
+    fine iterate L = L_H R^T after each update, i.e. #{sigma_i(L) >
+    sigma_1(L) max(m, n) eps}.  sigma(L) = sigma(L_H C) with C C^T = R^T R,
+    computed on the device by the two-pass spectrum plan (warm-started across
+    iterations) and recorded by the finalize step as the iteration's rank_l.
+    FP32 plans keep an FP64 shadow of L_H (same rank-1 updates, unrounded):
+    the reference runs in float64, and FP32 rounding noise would otherwise
+    count as rank."""
+
+    def __init__(self, be, chain, comm, m_global, f32, device):
+        self.comm = comm
+        self.be = be
+        lh, ld, done, self.slot = be.rank_binding()
+        self.shadow = None
+        if f32:
+            self.shadow = torch.zeros((be.m_local, chain.n_coarse), dtype=torch.float64, device=device)
+            lh, ld = self.shadow.data_ptr(), self.shadow.stride(0)
+        self.lh, self.ld = lh, ld
+        identity = chain.n_coarse == chain.n_fine and chain.n_factors == 0
+        C = None if identity else chain_cholesky(chain, device)
+        self.spec = CudaSpectrum(be.m_local, chain.n_coarse, False, device, C=C, skip_ptr=done)
+        self.rel = max(m_global, chain.n_fine) * np.finfo(np.float64).eps
+
+    def step(self):
+        sp = self.spec
+        if self.shadow is not None:
+            self.be.rank_shadow(self.shadow)
+        sp.gram(self.lh, self.ld)
+        self.comm.sum(sp.red)
+        sp.rotate(self.lh, self.ld)
+        self.comm.sum(sp.red2)
+        sp.finish(self.rel, rank_ptr=self.slot)
+
+    def close(self):
+        self.spec.close()
+
+
+def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every, probe=None, atoms=None):
+    """Row-block host loop shared by the single-GPU and sharded entry points.
+    ``probe`` records collect_rank; ``atoms`` (a list) receives the LMO factors
+    (u, v) of every iteration for track_oracle_atoms."""
     st = be.input_stats(D)
     comm.sum(st[2:3])
     if st[2].item() > 0:
@@ -41,8 +81,14 @@ def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every):
     while True:
         for _ in range(check_every):
             be.lmo()
+            if atoms is not None:
+                uv = (be.empty((be.m_local,), torch.float64), be.empty((be.nh,), torch.float64))
+                be.atom_copy(*uv)
+                atoms.append(uv)
             comm.sum(be.dots)
             be.update(D, maskbits, S)
+            if probe is not None:
+                probe.step()
             be.gram()
             comm.sum(be.red[:ns])
             comm.gather(be.amax_all, be.amax)
@@ -63,20 +109,30 @@ def _check_every(opts):
     return 1 if opts.time_budget is not None else 8
 
 
-def _warn_unsupported(opts):
-    if opts.track_oracle_atoms:
-        raise NotImplementedError("track_oracle_atoms is not available on the GPU path")
-    if opts.collect_rank:
-        warnings.warn("collect_rank is not computed on the GPU path; rank_l is reported as -1",
-                      RuntimeWarning, stacklevel=3)
+def _oracle_atoms(be, atoms, out, kind):
+    """track_oracle_atoms (cpcp.py:355-360): the dense LMO atom of every
+    iteration (this rank's rows), expanded on the device from the saved
+    factors; None on the P[D] = 0 early exit, like the reference."""
+    if atoms is None:
+        return None
+    st = out[2]
+    k = st["k"]
+    if st["done"] == 1 and k == 1 and out[4][0] == 0.0 and out[3][0][0] == 0.0:
+        return None
+    res = []
+    for u, v in atoms[:k]:
+        a = be.empty((be.m_local, be.n), torch.float64)
+        be.atom_dense(u, v, a)
+        res.append(give_back(a, kind))
+    return res
 
 
-def _state_from(L, S, st, hist, objs, kind):
+def _state_from(L, S, st, hist, objs, kind, atoms=None):
     history = [IterationRecord(i + 1, float(h[0]), float(h[1]), int(round(h[2])), float(h[3]), float(h[4]))
                for i, h in enumerate(hist)]
     return CpcpState(l=give_back(L, kind), s=give_back(S, kind), t_l=float(st["t_l"]), t_s=float(st["t_s"]),
                      u_l=float(st["u_l"]), u_s=float(st["u_s"]), iter=int(st["k"]), history=history,
-                     objective_history=[float(x) for x in objs], converged=st["done"] == 1)
+                     objective_history=[float(x) for x in objs], converged=st["done"] == 1, oracle_atoms=atoms)
 
 
 def _mask_bits(mask, shape, device, rows=None):
@@ -97,7 +153,6 @@ def ml_fwt_solve(d, mask=None, opts=None):
         raise ValueError("CpcpOptions with penalty weights is required")
     D, kind = as_device_matrix(d, "d")
     m, n = D.shape
-    _warn_unsupported(opts)
     with torch.cuda.device(D.device):
         nh = resolve_coarse_width(n, m, opts.levels, opts.rank_guess)
         chain = build_chain(n, nh)
@@ -106,15 +161,20 @@ def ml_fwt_solve(d, mask=None, opts=None):
         be = CudaCpcp(chain, m, m, 0, D.dtype == torch.float32, opts.max_iters, 1, D.device)
         if TIMING_SINK is not None:
             be.set_timing(True)
+        probe = RankProbe(be, chain, SINGLE, m, D.dtype == torch.float32, D.device) if opts.collect_rank else None
+        atoms = [] if opts.track_oracle_atoms else None
         try:
-            out = run_fwt(be, SINGLE, D, bits, m, opts, radius, _check_every(opts))
+            out = run_fwt(be, SINGLE, D, bits, m, opts, radius, _check_every(opts), probe, atoms)
+            atoms = _oracle_atoms(be, atoms, out, kind)
             if TIMING_SINK is not None:
                 t = be.timing()
                 t["iters"] = out[2]["k"]
                 TIMING_SINK.append(t)
         finally:
+            if probe is not None:
+                probe.close()
             be.close()
-    return _state_from(*out, kind)
+    return _state_from(*out, kind, atoms)
 
 
 def fwt_solve(d, mask=None, opts=None):
@@ -140,17 +200,21 @@ def ml_fwt_solve_rows(d_local, mask_local, opts, m_global, row0, group=None):
     D, kind = as_device_matrix(d_local, "d")
     m, n = D.shape
     comm = Comm(group)
-    _warn_unsupported(opts)
     with torch.cuda.device(D.device):
         chain = build_chain(n, resolve_coarse_width(n, m_global, opts.levels, opts.rank_guess))
         radius = 1.0 / chain.sigma_max()
         bits = _mask_bits(mask_local, (m, n), D.device)
         be = CudaCpcp(chain, m, m_global, row0, D.dtype == torch.float32, opts.max_iters, comm.world, D.device)
+        probe = RankProbe(be, chain, comm, m_global, D.dtype == torch.float32, D.device) if opts.collect_rank else None
+        atoms = [] if opts.track_oracle_atoms else None
         try:
-            out = run_fwt(be, comm, D, bits, m_global, opts, radius, _check_every(opts))
+            out = run_fwt(be, comm, D, bits, m_global, opts, radius, _check_every(opts), probe, atoms)
+            atoms = _oracle_atoms(be, atoms, out, kind)
         finally:
+            if probe is not None:
+                probe.close()
             be.close()
-    return _state_from(*out, kind)
+    return _state_from(*out, kind, atoms)
 
 
 __all__ = ["ml_fwt_solve", "fwt_solve", "ml_fwt_solve_rows", "CpcpOptions"]

@@ -12,6 +12,7 @@
 #include "cpcp.h"
 #include "kernels.h"
 #include "pcp.h"
+#include "spectrum.h"
 
 namespace mlr {
 
@@ -31,6 +32,12 @@ static int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n > 0 ? n : 148;
+}
+static int spec_splits(int64_t m_local, int n) {
+  const int64_t t = round_up(n, 64) / 64;
+  int64_t splits = ceil_div(2 * sm_count(), t * (t + 1) / 2);
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
+  return (int)std::max<int64_t>(1, splits);
 }
 
 // ------------------------------------------------------------ restrict / prolong
@@ -580,6 +587,113 @@ int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, voi
   if (objectives)
     MLR_CUDA(cudaMemcpyAsync(objectives, PLAN->obj, sizeof(double) * count, cudaMemcpyDeviceToHost, STREAM));
   MLR_CUDA(cudaStreamSynchronize(STREAM));
+  return kOk;
+}
+
+// ------------------------------------------------------------ spectrum / telemetry
+int64_t mlr_spec_workspace_bytes(int64_t m_local, int n) {
+  if (m_local < 0 || n < 1) return -1;
+  return spec_workspace_bytes(m_local, n, spec_splits(m_local, n));
+}
+int mlr_spec_create(int64_t m_local, int n, int f32, const double* C, int64_t ldc, const int* skip, void* workspace,
+                    void** plan_out, void* stream) {
+  if (m_local < 0 || n < 1 || !workspace || !plan_out || (C && ldc < n)) {
+    set_error("mlr_spec_create: invalid arguments");
+    return kErrArg;
+  }
+  SpecPlan* p = new SpecPlan();
+  p->m_local = m_local;
+  p->n = n;
+  p->np = (int)round_up(n, 64);
+  p->splits = spec_splits(m_local, n);
+  p->f32 = f32 != 0;
+  p->skip = skip;
+  spec_carve(*p, workspace);
+  int rc = spec_init(p, C, ldc, (cudaStream_t)stream);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  *plan_out = p;
+  return kOk;
+}
+int mlr_spec_destroy(void* plan) {
+  delete (SpecPlan*)plan;
+  return kOk;
+}
+int64_t mlr_spec_red_doubles(void* plan) { return (int64_t)((SpecPlan*)plan)->np * ((SpecPlan*)plan)->np; }
+int mlr_spec_gram(void* plan, const void* X, int64_t ldx, double* red, void* stream) {
+  return spec_gram((SpecPlan*)plan, X, ldx, red, (cudaStream_t)stream);
+}
+int mlr_spec_rotate(void* plan, const void* X, int64_t ldx, const double* red, double* red2, void* stream) {
+  return spec_rotate((SpecPlan*)plan, X, ldx, red, red2, (cudaStream_t)stream);
+}
+int mlr_spec_finish(void* plan, const double* red2, double rel, double* sig_out, double* rank_out,
+                    const double* pair_w, double* wsum_out, void* stream) {
+  return spec_finish((SpecPlan*)plan, red2, rel, sig_out, rank_out, pair_w, wsum_out, (cudaStream_t)stream);
+}
+int mlr_chain_cholesky(void* chain, double* C, int64_t ldc, void* stream) {
+  if (!chain || !C || ldc < ((Chain*)chain)->d.nh) {
+    set_error("mlr_chain_cholesky: invalid arguments");
+    return kErrArg;
+  }
+  return chain_cholesky(((Chain*)chain)->d, C, ldc, (cudaStream_t)stream);
+}
+int mlr_pcp_coarse_copy(void* plan, void* out, int64_t ldo, void* stream) {
+  PcpPlan* p = (PcpPlan*)plan;
+  if (!out || ldo < p->ch.nh) {
+    set_error("mlr_pcp_coarse_copy: invalid arguments");
+    return kErrArg;
+  }
+  if (p->m_local == 0) return kOk;
+  const size_t tb = p->f32 ? 4 : 8;
+  MLR_CUDA(cudaMemcpy2DAsync(out, tb * ldo, p->Z, tb * p->ch.np, tb * p->ch.nh, p->m_local, cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+  return kOk;
+}
+int64_t mlr_pcp_delta_work_doubles(void) { return 148 * 8 + 8; }
+int mlr_pcp_delta(void* plan, const void* Zk, const void* Zf, int64_t ldz, double* out, double* work, void* stream) {
+  PcpPlan* p = (PcpPlan*)plan;
+  if (!Zk || !Zf || !out || !work || ldz < p->ch.nh) {
+    set_error("mlr_pcp_delta: invalid arguments");
+    return kErrArg;
+  }
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p->m_local, 8), 148 * 8));
+  return pcp_delta(p->ch, p->f32, p->m_local, Zk, Zf, ldz, out, work, blocks, (cudaStream_t)stream);
+}
+int mlr_cpcp_rank_shadow(void* plan, double* L64, int64_t ld, void* stream) {
+  CpcpPlan* p = (CpcpPlan*)plan;
+  if (!L64 || ld < p->ch.nh) {
+    set_error("mlr_cpcp_rank_shadow: invalid arguments");
+    return kErrArg;
+  }
+  return cpcp_rank_shadow(p, L64, ld, (cudaStream_t)stream);
+}
+int mlr_cpcp_atom_copy(void* plan, double* u_out, double* v_out, void* stream) {
+  if (!u_out || !v_out) {
+    set_error("mlr_cpcp_atom_copy: invalid arguments");
+    return kErrArg;
+  }
+  return cpcp_atom_copy((CpcpPlan*)plan, u_out, v_out, (cudaStream_t)stream);
+}
+int mlr_cpcp_atom_dense(void* plan, const double* u, const double* v, double* out, int64_t ldo, void* stream) {
+  CpcpPlan* p = (CpcpPlan*)plan;
+  if (!u || !v || !out || ldo < p->ch.n) {
+    set_error("mlr_cpcp_atom_dense: invalid arguments");
+    return kErrArg;
+  }
+  return cpcp_atom_dense(p, u, v, out, ldo, (cudaStream_t)stream);
+}
+int mlr_cpcp_rank_binding(void* plan, const void** lh, int64_t* ld, const int** done, double** rank_slot) {
+  CpcpPlan* p = (CpcpPlan*)plan;
+  if (!lh || !ld || !done || !rank_slot) {
+    set_error("mlr_cpcp_rank_binding: invalid arguments");
+    return kErrArg;
+  }
+  *lh = p->LH;
+  *ld = p->ch.np;
+  *done = &p->dev->done;
+  *rank_slot = &p->dev->rank_l;
   return kOk;
 }
 

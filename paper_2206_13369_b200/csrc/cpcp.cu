@@ -253,6 +253,7 @@ __global__ void cp_start_scalars(CpcpDev* st, double lam_l, double lam_s, double
   st->k = 0;
   st->done = 0;
   st->status = 0;
+  st->rank_l = -1.0;
   st->t0_ns = cp_now_ns();
 }
 
@@ -693,7 +694,7 @@ __global__ void cp_finalize_kernel(CpcpDev* st, const double* __restrict__ stats
   double* h = hist + (int64_t)(k - 1) * kCpHistCols;
   h[0] = sqrt(st->sq) / st->pd_norm;
   h[1] = obj;
-  h[2] = -1.0;
+  h[2] = st->rank_l;
   h[3] = st->nnz / (st->m_global * st->n);
   h[4] = wall;
   h[5] = st->ga;
@@ -711,6 +712,65 @@ __global__ void cp_finalize_kernel(CpcpDev* st, const double* __restrict__ stats
   } else {
     st->k = k + 1;
   }
+}
+
+// FP64 shadow of the coarse iterate for collect_rank on FP32 data: the same
+// rank-1 update as the fused row pass (L_H <- (1-ga) L_H + ga coef u v^T,
+// cpcp.py:399-402) without rounding to FP32, so the numerical rank sees the
+// iterate the reference's float64 run holds rather than FP32 rounding noise.
+__global__ void __launch_bounds__(256) cp_shadow_kernel(const CpcpDev* __restrict__ st, int64_t m, int nh,
+                                                        const double* __restrict__ u, const double* __restrict__ v,
+                                                        double* __restrict__ L64, int64_t ld) {
+  if (st->done) return;
+  const double ga = st->ga, one_ga = 1.0 - ga, gc = ga * st->coef;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * nh; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nh;
+    const int k = (int)(e % nh);
+    double* p = L64 + i * ld + k;
+    *p = one_ga * *p + (gc * u[i]) * v[k];
+  }
+}
+
+// track_oracle_atoms (cpcp.py:355-360): the LMO atom of one iteration,
+// M_L = -radius * u (R v)^T (cpcp.py:506-513; fwt_solve: -u v^T), from the
+// factors saved after that iteration's LMO step.  Dense m_local x n, float64.
+__global__ void __launch_bounds__(256) cp_atom_kernel(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m,
+                                                      const double* __restrict__ u, const double* __restrict__ v,
+                                                      double* __restrict__ out, int64_t ldo) {
+  const double nr = -st->radius;
+  const int n = ch.n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n;
+    const int j = (int)(e % n);
+    const int c = ch.c0[j];
+    // m_h[i][c] = (-radius) * (u_i v_c), then m_h @ R^T (two taps)
+    double a = nr * (u[i] * v[c]) * ch.w0[j];
+    if (ch.w1[j] != 0.0) a += nr * (u[i] * v[c + 1]) * ch.w1[j];
+    out[i * ldo + j] = a;
+  }
+}
+
+int cpcp_atom_copy(CpcpPlan* p, double* u_out, double* v_out, cudaStream_t st) {
+  if (p->m_local > 0)
+    MLR_CUDA(cudaMemcpyAsync(u_out, p->u, sizeof(double) * p->m_local, cudaMemcpyDeviceToDevice, st));
+  MLR_CUDA(cudaMemcpyAsync(v_out, p->v, sizeof(double) * p->ch.nh, cudaMemcpyDeviceToDevice, st));
+  return kOk;
+}
+
+int cpcp_atom_dense(CpcpPlan* p, const double* u, const double* v, double* out, int64_t ldo, cudaStream_t st) {
+  if (p->m_local == 0) return kOk;
+  const int blocks = (int)std::min<int64_t>(ceil_div(p->m_local * p->ch.n, 256), 148 * 16);
+  cp_atom_kernel<<<blocks, 256, 0, st>>>(p->dev, p->ch, p->m_local, u, v, out, ldo);
+  MLR_LAUNCH_CHECK("cp_atom_kernel");
+  return kOk;
+}
+
+int cpcp_rank_shadow(CpcpPlan* p, double* L64, int64_t ld, cudaStream_t st) {
+  if (p->m_local == 0) return kOk;
+  const int blocks = (int)std::min<int64_t>(ceil_div(p->m_local * p->ch.nh, 256), 148 * 8);
+  cp_shadow_kernel<<<blocks, 256, 0, st>>>(p->dev, p->m_local, p->ch.nh, p->u, p->v, L64, ld);
+  MLR_LAUNCH_CHECK("cp_shadow_kernel");
+  return kOk;
 }
 
 // ------------------------------------------------------------ host drivers

@@ -21,6 +21,7 @@ struct CpcpDev {
   int j_s;
   double ga, gb;
   int k, done, status, max_iters, max_passes;
+  double rank_l;            // numerical rank of L (collect_rank), -1 when not collected
 };
 
 struct CpcpPlan {
@@ -64,5 +65,8 @@ int cpcp_update(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, i
                 const double* dots, cudaStream_t st);
 int cpcp_finalize(CpcpPlan* p, const double* red, cudaStream_t st);
 int cpcp_outputs(CpcpPlan* p, void* L, int64_t ldl, cudaStream_t st);
+int cpcp_rank_shadow(CpcpPlan* p, double* L64, int64_t ld, cudaStream_t st);
+int cpcp_atom_copy(CpcpPlan* p, double* u_out, double* v_out, cudaStream_t st);
+int cpcp_atom_dense(CpcpPlan* p, const double* u, const double* v, double* out, int64_t ldo, cudaStream_t st);
 
 }  // namespace mlr

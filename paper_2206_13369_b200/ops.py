@@ -2,7 +2,9 @@
 restriction operators on device data).
 
 ``restrict`` / ``prolong`` mirror multilevel.restrict / multilevel.prolong
-(multilevel.py:212-245); ``eigh_psd`` exposes the coarse Jacobi eigensolver.
+(multilevel.py:212-245); ``eigh_psd`` exposes the coarse Jacobi eigensolver;
+``singular_values`` / ``matrix_rank`` expose the two-pass spectrum plan used
+by the rank telemetry (collect_rank, collect_diagnostics).
 """
 
 from __future__ import annotations
@@ -13,6 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .backend import CudaSpectrum
 from .chain import Chain
 from .runtime import as_device_matrix, give_back
 
@@ -77,3 +80,38 @@ def eigh_psd(b, tol=None, max_sweeps=60):
     order = torch.argsort(lam[:n], descending=True)
     return (give_back(lam[:n][order].contiguous(), kind), give_back(V[:n, :n][:, order].contiguous(), kind),
             int(info[0]))
+
+
+def _spectrum(x, rel):
+    X, kind = as_device_matrix(x, "x")
+    if X.shape[1] > X.shape[0]:
+        X = X.t().contiguous()
+    m, n = X.shape
+    f32 = X.dtype == torch.float32
+    with torch.cuda.device(X.device):
+        sp = CudaSpectrum(m, n, f32, X.device)
+        try:
+            sig = torch.zeros(sp.np_, dtype=torch.float64, device=X.device)
+            rank = torch.zeros(1, dtype=torch.float64, device=X.device)
+            sp.gram(X.data_ptr(), X.stride(0))
+            sp.rotate(X.data_ptr(), X.stride(0))
+            sp.finish(rel, sig_out=sig, rank_ptr=rank.data_ptr())
+            torch.cuda.current_stream().synchronize()
+        finally:
+            sp.close()
+    return sig[:n], int(rank.item()), kind
+
+
+def singular_values(x):
+    """All min(m, n) singular values of x, descending, accurate to ~eps * sigma_1
+    (Gram + Jacobi, then Jacobi on the Gram of the rotated columns)."""
+    sig, _, kind = _spectrum(x, 0.0)
+    return give_back(sig.contiguous(), kind)
+
+
+def matrix_rank(x):
+    """#{sigma_i > sigma_1 * max(m, n) * eps(dtype)} (numpy.linalg.matrix_rank's
+    default tolerance; the reference's rank_l column, cpcp.py:434-439)."""
+    X, _ = as_device_matrix(x, "x")
+    eps = np.finfo(np.float32 if X.dtype == torch.float32 else np.float64).eps
+    return _spectrum(X, max(X.shape) * eps)[1]

@@ -13,8 +13,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .api_types import IterationRecord, PcpOptions, PcpState, SvdError
-from .backend import CudaPcp
+from .api_types import IterationRecord, MultilevelDiagnostics, PcpOptions, PcpState, SvdError
+from .backend import CudaPcp, CudaSpectrum
 from .chain import build_chain, resolve_coarse_width
 from .runtime import SINGLE, Comm, as_device_matrix, give_back
 
@@ -38,10 +38,12 @@ def _jacobi_tol(opts, f32):
     return 1e-9 if f32 else 64 * np.finfo(np.float64).eps
 
 
-def run_ialm(be, comm, D, m_global, n, opts, lam, check_every):
+def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
     """Row-block host loop shared by the single-GPU and sharded entry points.
 
-    Returns (L, S, Y, state dict, history array) or None for a zero D."""
+    ``coarse`` (a list) receives a copy of the coarse iterate L_H after every
+    SVT step (collect_diagnostics).  Returns (L, S, Y, state dict, history
+    array) or None for a zero D."""
     st3 = be.input_stats(D)
     comm.sum(st3[0:1])
     comm.max(st3[1:2])
@@ -78,6 +80,10 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every):
     while True:
         for _ in range(check_every):
             be.svt()
+            if coarse is not None:
+                z = be.empty((D.shape[0], be.nh), D.dtype)
+                be.coarse_copy(z)
+                coarse.append(z)
             be.update(D, Y[calls % 2], Y[(calls + 1) % 2])
             calls += 1
             be.gram(1)
@@ -94,6 +100,41 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every):
     be.outputs(D, Y[(k - 1) % 2], L, S)
     hist = be.history(k)
     return L, S, Y[k % 2], st, hist
+
+
+def diagnostics(be, comm, chain, coarse, k, m_global):
+    """collect_diagnostics (reference pcp.py:298-306): epsilon_bound of the
+    final coarse iterate (multilevel.py:248-265) and the alignment errors
+    delta_j = <L_H^j (R^T R - I), L_H^j - restrict(L_final)>, with
+    restrict(L_final) = L_H^final R^T R.  All on the device: one streaming
+    pass per delta, and the two-pass spectrum plan for sigma(L_H^final)."""
+    zs = coarse[:k]
+    zf = zs[-1]
+    dev = zf.device
+    deltas = torch.zeros(k, dtype=torch.float64, device=dev)
+    work = torch.zeros(int(be.lib.mlr_pcp_delta_work_doubles()), dtype=torch.float64, device=dev)
+    for j, z in enumerate(zs):
+        be.delta(z, zf, deltas[j:j + 1], work)
+    comm.sum(deltas)
+    f32 = zf.dtype == torch.float32
+    nh = chain.n_coarse
+    spec = CudaSpectrum(zf.shape[0], nh, f32, dev)
+    try:
+        spec.gram(zf.data_ptr(), zf.stride(0))
+        comm.sum(spec.red)
+        spec.rotate(zf.data_ptr(), zf.stride(0))
+        comm.sum(spec.red2)
+        # k-th largest sigma(L_H) pairs with the k-th smallest sigma(R)
+        pair = torch.zeros(spec.np_, dtype=torch.float64)
+        pair[:nh] = torch.from_numpy(1.0 - chain.composite_sigmas()[::-1].copy())
+        pair = pair.to(dev)
+        out = torch.zeros(2, dtype=torch.float64, device=dev)
+        eps = np.finfo(np.float32 if f32 else np.float64).eps
+        spec.finish(max(m_global, nh) * eps, rank_ptr=out[1:].data_ptr(), pair_w=pair, wsum_out=out[:1])
+        epsilon = float(out[0].item())
+    finally:
+        spec.close()
+    return MultilevelDiagnostics(epsilon=epsilon, delta_history=[float(x) for x in deltas.tolist()])
 
 
 def _state_from(L, S, Yk, st, hist, kind):
@@ -115,17 +156,19 @@ def ml_ialm_solve(d, opts=None):
     D, kind = as_device_matrix(d, "d")
     m, n = D.shape
     opts = opts if opts is not None else PcpOptions()
-    if opts.collect_diagnostics:
-        raise NotImplementedError("collect_diagnostics is not available on the GPU path yet")
     lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m, n))
+    diag = None
     with torch.cuda.device(D.device):
         opts_checked = _checked_width(n, m, opts)
         chain = build_chain(n, opts_checked)
         be = CudaPcp(chain, m, m, D.dtype == torch.float32, opts.max_iters, D.device)
         if TIMING_SINK is not None:
             be.set_timing(True)
+        coarse = [] if opts.collect_diagnostics else None
         try:
-            out = run_ialm(be, SINGLE, D, m, n, opts, lam, _check_every(opts))
+            out = run_ialm(be, SINGLE, D, m, n, opts, lam, _check_every(opts), coarse)
+            if coarse is not None and out is not None:
+                diag = diagnostics(be, SINGLE, chain, coarse, out[3]["k"], m)
             if TIMING_SINK is not None:
                 t = be.timing()
                 t["iters"] = out[3]["k"] if out is not None else 0
@@ -136,7 +179,9 @@ def ml_ialm_solve(d, opts=None):
             be.close()
     if out is None:
         return _zero_state(tuple(D.shape), kind, D)
-    return _state_from(*out, kind)
+    state = _state_from(*out, kind)
+    state.diagnostics = diag
+    return state
 
 
 def ialm_solve(d, opts=None):
@@ -205,13 +250,17 @@ def ml_ialm_solve_rows(d_local, opts, m_global, group=None):
     m, n = D.shape
     comm = Comm(group)
     lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m_global, n))
+    diag = None
     with torch.cuda.device(D.device):
         chain = build_chain(n, _checked_width(n, m_global, opts))
         be = CudaPcp(chain, m, m_global, D.dtype == torch.float32, opts.max_iters, D.device)
         if TIMING_SINK is not None:
             be.set_timing(True)
+        coarse = [] if opts.collect_diagnostics else None
         try:
-            out = run_ialm(be, comm, D, m_global, n, opts, lam, _check_every(opts))
+            out = run_ialm(be, comm, D, m_global, n, opts, lam, _check_every(opts), coarse)
+            if coarse is not None and out is not None:
+                diag = diagnostics(be, comm, chain, coarse, out[3]["k"], m_global)
             if TIMING_SINK is not None:
                 t = be.timing()
                 t["iters"] = out[3]["k"] if out is not None else 0
@@ -222,4 +271,6 @@ def ml_ialm_solve_rows(d_local, opts, m_global, group=None):
             be.close()
     if out is None:
         return _zero_state(tuple(D.shape), kind, D)
-    return _state_from(*out, kind)
+    state = _state_from(*out, kind)
+    state.diagnostics = diag
+    return state

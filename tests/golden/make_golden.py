@@ -133,6 +133,58 @@ def ialm_cases():
             **arrays, **hist_arrays(st.history))
 
 
+def telemetry_cases():
+    """collect_diagnostics (pcp.py:298-306) and collect_rank (cpcp.py:434-439)."""
+    d, _ = O.gaussian_rpca(120, 96, 6, 0.10, 3)
+    st = mlrpca.ml_ialm_solve(d, mlrpca.PcpOptions(levels=24, collect_diagnostics=True))
+    np.savez_compressed(os.path.join(HERE, "diag_pcp_f64.npz"), d=d, n_coarse=np.array(24), iter=np.array(st.iter),
+                        epsilon=np.array(st.diagnostics.epsilon), deltas=np.array(st.diagnostics.delta_history))
+    d32, _ = O.gaussian_rpca(200, 160, 8, 0.10, 4)
+    d32 = d32.astype(np.float32).astype(np.float64)
+    st = mlrpca.ml_ialm_solve(d32, mlrpca.PcpOptions(levels=40, tol_feasibility=1e-6, collect_diagnostics=True))
+    np.savez_compressed(os.path.join(HERE, "diag_pcp_f32.npz"), d=d32, n_coarse=np.array(40), iter=np.array(st.iter),
+                        tol=np.array(1e-6), epsilon=np.array(st.diagnostics.epsilon),
+                        deltas=np.array(st.diagnostics.delta_history))
+    cases = {
+        # name: (m, n, rank, eta, observe, seed, n_H (None = full width), tol, max_iters, dtype)
+        "rank_ml_f64": (100, 80, 4, 0.10, 0.8, 5, 20, 1e-6, 120, np.float64),
+        "rank_full_f64": (90, 70, 4, 0.10, 0.8, 11, None, 1e-6, 120, np.float64),
+        "rank_ml_f32": (160, 128, 4, 0.10, 0.7, 6, 16, 1e-5, 80, np.float32),
+    }
+    for name, (m, n, r, eta, obs, seed, nh, tol, iters, dt) in cases.items():
+        d, mask = O.gaussian_rpca(m, n, r, eta, seed, observe=obs)
+        d = d.astype(dt).astype(np.float64)
+        lam = 1 / np.sqrt(max(m, n))
+        opts = mlrpca.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=tol, max_iters=iters,
+                                  levels=nh, collect_rank=True)
+        om = mlrpca.ObservationMask(mask)
+        st = mlrpca.fwt_solve(d, om, opts) if nh is None else mlrpca.ml_fwt_solve(d, om, opts)
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), d=d, mask=mask, n_coarse=np.array(nh or 0), tol=np.array(tol),
+            max_iters=np.array(iters), lam_l=np.array(lam), lam_s=np.array(lam / np.sqrt(max(m, n))),
+            iter=np.array(st.iter), l_rank=np.array(np.linalg.matrix_rank(st.l)), **hist_arrays(st.history))
+
+
+def atom_cases():
+    """track_oracle_atoms (cpcp.py:355-360): every iteration's dense LMO atom."""
+    cases = {
+        # name: (m, n, rank, observe, seed, n_H (None = full width), max_iters)
+        "atoms_ml_f64": (40, 32, 3, 0.8, 31, 8, 12),
+        "atoms_full_f64": (30, 24, 3, 0.8, 32, None, 10),
+    }
+    for name, (m, n, r, obs, seed, nh, iters) in cases.items():
+        d, mask = O.gaussian_rpca(m, n, r, 0.1, seed, observe=obs)
+        lam = 1 / np.sqrt(max(m, n))
+        opts = mlrpca.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=1e-9, max_iters=iters,
+                                  levels=nh, collect_rank=False, track_oracle_atoms=True)
+        om = mlrpca.ObservationMask(mask)
+        st = mlrpca.fwt_solve(d, om, opts) if nh is None else mlrpca.ml_fwt_solve(d, om, opts)
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), d=d, mask=mask, n_coarse=np.array(nh or 0), max_iters=np.array(iters),
+            lam_l=np.array(lam), lam_s=np.array(lam / np.sqrt(max(m, n))), iter=np.array(st.iter),
+            atoms=np.array(st.oracle_atoms), **hist_arrays(st.history))
+
+
 def fwt_cases():
     cases = {
         # name: (m, n, rank, eta, observe, seed, n_H, tol, max_iters, dtype)
@@ -197,6 +249,8 @@ if __name__ == "__main__":
     pcp_cases()
     pcp_c1_summary()
     ialm_cases()
+    telemetry_cases()
+    atom_cases()
     fwt_cases()
     fwt_full_cases()
     print("golden vectors written to", HERE)

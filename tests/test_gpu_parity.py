@@ -160,6 +160,89 @@ def test_ialm_edge_cases():
     assert relf(st.l, ref.l) <= 1e-10 and relf(st.y, ref.y) <= 1e-10
 
 
+# ------------------------------------------------------------------ telemetry
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_singular_values_graded(dtype):
+    """The two-pass spectrum resolves singular values far below sqrt(eps) of
+    the largest (one Gram eigensolve would not): absolute error ~eps sigma_1."""
+    rng = np.random.default_rng(7)
+
+    def graded(m, n, s):
+        u, _ = np.linalg.qr(rng.standard_normal((m, len(s))))
+        v, _ = np.linalg.qr(rng.standard_normal((n, len(s))))
+        return ((u * s) @ v.T).astype(dtype)
+
+    x = graded(250, 100, np.logspace(0, -15, 100))
+    ref = np.linalg.svd(x.astype(np.float64), compute_uv=False)
+    got = pkg.singular_values(x)
+    eps = np.finfo(dtype).eps
+    assert got.shape == (100,) and np.all(np.diff(got) <= 0)
+    assert np.abs(got - ref).max() <= 50 * eps * ref[0]
+    # rank at numpy's default tolerance (no singular value near the threshold)
+    assert pkg.matrix_rank(x) == np.linalg.matrix_rank(x)
+    w = graded(160, 60, np.concatenate([np.logspace(0, -10, 30), np.zeros(30)])).T.copy()  # wide, rank 30
+    assert pkg.matrix_rank(w) == np.linalg.matrix_rank(w) == (30 if dtype == np.float64 else 14)
+
+
+@pytest.mark.parametrize("name", ["rank_ml_f64", "rank_full_f64", "rank_ml_f32"])
+def test_collect_rank_golden(golden, name):
+    """collect_rank (cpcp.py:434-439) against the reference's own rank column;
+    FW-T is chaotic, so the gate is the first 30 iterations plus the final
+    rank of the GPU's own L."""
+    g = golden(name)
+    d = g["d"].astype(np.float32) if "f32" in name else g["d"]
+    opts = pkg.CpcpOptions(lambda_l=float(g["lam_l"]), lambda_s=float(g["lam_s"]), tol=float(g["tol"]),
+                           max_iters=int(g["max_iters"]), levels=int(g["n_coarse"]) or None, collect_rank=True)
+    fn = pkg.fwt_solve if "full" in name else pkg.ml_fwt_solve
+    st = fn(d, pkg.ObservationMask(g["mask"]), opts)
+    ranks = [h.rank_l for h in st.history]
+    k = min(len(ranks), len(g["h_rank"]), 30)
+    assert ranks[:k] == list(g["h_rank"][:k])
+    tol = np.abs(np.linalg.svd(st.l.astype(np.float64), compute_uv=False)).max() * max(st.l.shape) * np.finfo(st.l.dtype).eps
+    assert ranks[-1] == np.linalg.matrix_rank(st.l.astype(np.float64), tol=tol)
+
+
+@pytest.mark.parametrize("name,tolrel", [("diag_pcp_f64", 1e-8), ("diag_pcp_f32", 1e-3)])
+def test_collect_diagnostics_golden(golden, name, tolrel):
+    """collect_diagnostics (pcp.py:298-306) against the reference's epsilon and
+    delta history."""
+    g = golden(name)
+    d = g["d"].astype(np.float32) if "f32" in name else g["d"]
+    tol = float(g["tol"]) if "tol" in g else 1e-7
+    st = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=int(g["n_coarse"]), tol_feasibility=tol,
+                                             collect_diagnostics=True))
+    assert st.iter == int(g["iter"])
+    dg = st.diagnostics
+    assert abs(dg.epsilon - float(g["epsilon"])) <= tolrel * abs(float(g["epsilon"]))
+    ref = g["deltas"]
+    assert len(dg.delta_history) == len(ref)
+    assert np.abs(np.array(dg.delta_history) - ref).max() <= tolrel * np.abs(ref).max()
+    assert dg.delta_max == max(0.0, max(ref)) or abs(dg.delta_max - max(0.0, max(ref))) <= tolrel * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["atoms_ml_f64", "atoms_full_f64"])
+def test_oracle_atoms_golden(golden, name):
+    """track_oracle_atoms (cpcp.py:355-360): one dense atom per iteration,
+    equal to the reference's while the FW-T trajectories agree."""
+    g = golden(name)
+    nh = int(g["n_coarse"]) or None
+    opts = pkg.CpcpOptions(lambda_l=float(g["lam_l"]), lambda_s=float(g["lam_s"]), tol=1e-9,
+                           max_iters=int(g["max_iters"]), levels=nh, collect_rank=False, track_oracle_atoms=True)
+    fn = pkg.fwt_solve if nh is None else pkg.ml_fwt_solve
+    st = fn(g["d"], pkg.ObservationMask(g["mask"]), opts)
+    assert st.iter == int(g["iter"]) and len(st.oracle_atoms) == st.iter
+    assert all(a.shape == g["d"].shape and a.dtype == np.float64 for a in st.oracle_atoms)
+    # the first two atoms agree to rounding; after that FW-T is chaotic (the
+    # oracle itself moves atoms 3-5 by ~1e-3 under 1-ulp input perturbations)
+    for a, ref in list(zip(st.oracle_atoms, g["atoms"]))[:2]:
+        assert relf(a, ref) <= 1e-9
+    for a in st.oracle_atoms:  # every atom is -radius u (R v)^T: rank one, inside the unit nuclear ball
+        assert np.linalg.matrix_rank(a) <= 1 and np.linalg.norm(a) <= 1 + 1e-12
+    z = fn(np.zeros((8, 6)), None, pkg.CpcpOptions(lambda_l=0.1, lambda_s=0.1, levels=None if nh is None else 3,
+                                                    collect_rank=False, track_oracle_atoms=True))
+    assert z.oracle_atoms is None  # P[D] = 0 early exit (cpcp.py:348-350)
+
+
 # ------------------------------------------------------------------ ML-CPCP
 @pytest.mark.parametrize("name", ["fwt_f64_small", "fwt_f32_small", "fwt_f64_full"])
 def test_ml_fwt_golden_envelope(golden, name):

@@ -169,6 +169,38 @@ def test_golden_ialm(golden, name):
         assert_allclose(np.linalg.norm(st.l), float(g["l_fro"]), rtol=1e-11)
 
 
+def test_golden_diagnostics(golden):
+    """collect_diagnostics (pcp.py:298-306): epsilon_bound and delta history."""
+    g = golden("diag_pcp_f64")
+    st = O.ml_ialm(g["d"], levels=int(g["n_coarse"]), collect_diagnostics=True)
+    assert st.iter == int(g["iter"])
+    eps, deltas = st.diagnostics
+    assert_allclose(eps, float(g["epsilon"]), rtol=1e-12)
+    assert_allclose(deltas, g["deltas"], rtol=1e-10, atol=1e-12 * np.abs(g["deltas"]).max())
+
+
+@pytest.mark.parametrize("name", ["rank_ml_f64", "rank_full_f64", "rank_ml_f32"])
+def test_golden_collect_rank(golden, name):
+    """collect_rank (cpcp.py:434-439): numerical rank of L per iteration."""
+    g = golden(name)
+    nh = int(g["n_coarse"]) or g["d"].shape[1]
+    st = O.ml_fwt(g["d"], g["mask"], float(g["lam_l"]), float(g["lam_s"]), tol=float(g["tol"]),
+                  max_iters=int(g["max_iters"]), levels=nh, collect_rank=True)
+    k = min(len(st.history), len(g["h_rank"]), 30)
+    assert [h.rank_l for h in st.history[:k]] == list(g["h_rank"][:k])
+
+
+@pytest.mark.parametrize("name", ["atoms_ml_f64", "atoms_full_f64"])
+def test_golden_oracle_atoms(golden, name):
+    """track_oracle_atoms (cpcp.py:355-360)."""
+    g = golden(name)
+    nh = int(g["n_coarse"]) or g["d"].shape[1]
+    st = O.ml_fwt(g["d"], g["mask"], float(g["lam_l"]), float(g["lam_s"]), tol=1e-9,
+                  max_iters=int(g["max_iters"]), levels=nh, collect_rank=False, track_oracle_atoms=True)
+    assert st.iter == int(g["iter"]) == len(st.oracle_atoms)
+    assert_allclose(np.array(st.oracle_atoms), g["atoms"], rtol=0, atol=1e-12 * np.abs(g["atoms"]).max())
+
+
 def test_golden_c1_summary(golden):
     g = golden("pcp_c1_summary")
     d, _ = O.make_config("C1", 0)
