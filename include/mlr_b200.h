@@ -184,6 +184,18 @@ int mlr_cpcp_rank_shadow(void* plan, double* L64, int64_t ld, void* stream);
 int mlr_cpcp_atom_copy(void* plan, double* u_out, double* v_out, void* stream);
 int mlr_cpcp_atom_dense(void* plan, const double* u, const double* v, double* out, int64_t ldo, void* stream);
 
+/* ---------------------------------------------------------------- frame stacks
+ * Video pipeline layout (reference io.py:131-182).  frames: count 8-bit rasters
+ * (height x width, row-major, frame j at frames + j*height*width), device memory.
+ * x: the (height*width) x count solver matrix (row-major, ld ldx >= count), pixel
+ * (row, col) of frame j at entry (row + col*height, j) (io.py:33-36).
+ * to_matrix: x = u8 / 255.0 (float64, then rounded to float when f32) - ingest_frames.
+ * to_frames: clamp to [0, 1] and floor(v * 255 + 0.5) - emit_frames' _quantize. */
+int mlr_frames_to_matrix(const uint8_t* frames, int count, int height, int width, int f32, void* x, int64_t ldx,
+                         void* stream);
+int mlr_matrix_to_frames(const void* x, int64_t ldx, int f32, int count, int height, int width, uint8_t* frames,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,5 +21,6 @@ from .api_types import (  # noqa: F401
 )
 from .chain import LevelError, build_chain, coarse_sizes, select_levels  # noqa: F401
 from .cpcp import fwt_solve, ml_fwt_solve, ml_fwt_solve_rows  # noqa: F401
+from . import frames  # noqa: F401
 from .ops import eigh_psd, matrix_rank, prolong, restrict, singular_values  # noqa: F401
 from .pcp import ialm_solve, ml_ialm_solve, ml_ialm_solve_rows  # noqa: F401

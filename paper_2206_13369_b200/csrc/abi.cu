@@ -632,6 +632,22 @@ int mlr_spec_finish(void* plan, const double* red2, double rel, double* sig_out,
                     const double* pair_w, double* wsum_out, void* stream) {
   return spec_finish((SpecPlan*)plan, red2, rel, sig_out, rank_out, pair_w, wsum_out, (cudaStream_t)stream);
 }
+int mlr_frames_to_matrix(const uint8_t* frames, int count, int height, int width, int f32, void* x, int64_t ldx,
+                         void* stream) {
+  if (!frames || !x || count < 1 || height < 1 || width < 1 || ldx < count || height > 65535 || count > 65535 * 32) {
+    set_error("mlr_frames_to_matrix: invalid arguments");
+    return kErrArg;
+  }
+  return frames_to_matrix(frames, count, height, width, f32 != 0, x, ldx, (cudaStream_t)stream);
+}
+int mlr_matrix_to_frames(const void* x, int64_t ldx, int f32, int count, int height, int width, uint8_t* frames,
+                         void* stream) {
+  if (!frames || !x || count < 1 || height < 1 || width < 1 || ldx < count || height > 65535 || count > 65535 * 32) {
+    set_error("mlr_matrix_to_frames: invalid arguments");
+    return kErrArg;
+  }
+  return matrix_to_frames(x, ldx, f32 != 0, count, height, width, frames, (cudaStream_t)stream);
+}
 int mlr_chain_cholesky(void* chain, double* C, int64_t ldc, void* stream) {
   if (!chain || !C || ldc < ((Chain*)chain)->d.nh) {
     set_error("mlr_chain_cholesky: invalid arguments");

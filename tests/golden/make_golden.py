@@ -185,6 +185,43 @@ def atom_cases():
             atoms=np.array(st.oracle_atoms), **hist_arrays(st.history))
 
 
+def frame_cases():
+    """Frame-stack I/O (io.py:100-182): raw PGM bytes, the reference's ingested
+    matrix and the bytes its emit_frames writes for given L / S."""
+    import tempfile
+    from mlrpca import io as rio
+    rng = np.random.default_rng(41)
+    h, w, count = 6, 5, 3
+    raster = rng.integers(0, 256, (count, h, w), dtype=np.uint8)
+    raster[0, 0, :] = [0, 1, 127, 254, 255]
+    with tempfile.TemporaryDirectory() as tmp:
+        paths = []
+        for j in range(count):
+            p = os.path.join(tmp, f"f{j}.pgm")
+            if j == 1:  # header with a comment and odd whitespace
+                with open(p, "wb") as fh:
+                    fh.write(b"P5 # frame one\n%d\t%d\n# max\n255\n" % (w, h) + raster[j].tobytes())
+            else:
+                rio.write_pgm(raster[j], p)
+            paths.append(p)
+        files = [open(p, "rb").read() for p in paths]
+        stack = rio.ingest_frames(paths)
+        m = h * w
+        l = rng.uniform(-0.2, 1.2, (m, count))
+        s = rng.uniform(-0.5, 0.5, (m, count))
+        l[:4, 0] = [0.5 / 255, 1.5 / 255, 254.5 / 255, 1.0]  # round-half-up boundaries
+        out = os.path.join(tmp, "out")
+        written = rio.emit_frames(stack, l, s, out)
+        emitted = [open(p, "rb").read() for p in written]
+        names = [os.path.basename(p) for p in written]
+    blob = np.frombuffer(b"".join(files), dtype=np.uint8)
+    eblob = np.frombuffer(b"".join(emitted), dtype=np.uint8)
+    np.savez_compressed(
+        os.path.join(HERE, "frames.npz"), raster=raster, files=blob, file_sizes=np.array([len(f) for f in files]),
+        matrix=stack.matrix, height=np.array(h), width=np.array(w), l=l, s=s, emitted=eblob,
+        emitted_sizes=np.array([len(e) for e in emitted]), names=np.array(names))
+
+
 def fwt_cases():
     cases = {
         # name: (m, n, rank, eta, observe, seed, n_H, tol, max_iters, dtype)
@@ -251,6 +288,7 @@ if __name__ == "__main__":
     ialm_cases()
     telemetry_cases()
     atom_cases()
+    frame_cases()
     fwt_cases()
     fwt_full_cases()
     print("golden vectors written to", HERE)

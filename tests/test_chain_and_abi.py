@@ -115,10 +115,14 @@ def test_cli_bridge_rebinds_and_restores():
     import types
     from paper_2206_13369_b200 import cli_bridge, cpcp, pcp
     cpu = object()
-    mod = types.SimpleNamespace(ialm_solve=cpu, ml_ialm_solve=cpu, fwt_solve=cpu, ml_fwt_solve=cpu)
+    io = types.SimpleNamespace(ingest_frames=cpu, emit_frames=cpu, save_matrix=cpu)
+    mod = types.SimpleNamespace(ialm_solve=cpu, ml_ialm_solve=cpu, fwt_solve=cpu, ml_fwt_solve=cpu,
+                                _numerical_rank=cpu, io=io)
     prev = cli_bridge.install(mod)
     assert mod.ml_ialm_solve is pcp.ml_ialm_solve
     assert mod.fwt_solve is cpcp.fwt_solve and mod.ml_fwt_solve is cpcp.ml_fwt_solve
-    assert mod.ialm_solve is pcp.ialm_solve
+    assert mod.ialm_solve is pcp.ialm_solve and mod._numerical_rank is pkg.matrix_rank
+    assert mod.io.save_matrix is cpu and mod.io.ingest_frames is not cpu  # frame I/O on the GPU, rest forwarded
     cli_bridge.uninstall(mod, prev)
     assert mod.ialm_solve is cpu and mod.ml_ialm_solve is cpu and mod.fwt_solve is cpu and mod.ml_fwt_solve is cpu
+    assert mod._numerical_rank is cpu and mod.io is io

@@ -9,6 +9,8 @@ Gates:
            SURVEY.md fact 7); iteration 1 must agree to rounding.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -241,6 +243,65 @@ def test_oracle_atoms_golden(golden, name):
     z = fn(np.zeros((8, 6)), None, pkg.CpcpOptions(lambda_l=0.1, lambda_s=0.1, levels=None if nh is None else 3,
                                                     collect_rank=False, track_oracle_atoms=True))
     assert z.oracle_atoms is None  # P[D] = 0 early exit (cpcp.py:348-350)
+
+
+# ------------------------------------------------------------------ frame stacks
+def _frame_files(g, tmp_path):
+    blob, paths, o = g["files"].tobytes(), [], 0
+    for j, n in enumerate(g["file_sizes"]):
+        p = tmp_path / f"f{j}.pgm"
+        p.write_bytes(blob[o:o + int(n)])
+        o += int(n)
+        paths.append(str(p))
+    return paths
+
+
+def test_ingest_emit_golden(golden, tmp_path):
+    """ingest_frames / emit_frames (io.py:128-182) against the reference: the
+    device-built matrix is bit-identical, the emitted PGM bytes identical."""
+    g = golden("frames")
+    paths = _frame_files(g, tmp_path)
+    st = pkg.frames.ingest_frames(paths)
+    assert (st.frame_height, st.frame_width, st.count) == (int(g["height"]), int(g["width"]), 3)
+    assert np.array_equal(st.matrix, g["matrix"])
+    st32 = pkg.frames.ingest_frames(paths, dtype=np.float32)
+    assert np.array_equal(st32.matrix, g["matrix"].astype(np.float32))
+    written = pkg.frames.emit_frames(st, g["l"], g["s"], str(tmp_path / "out"))
+    assert [os.path.basename(p) for p in written] == list(g["names"])
+    blob = b"".join(open(p, "rb").read() for p in written)
+    assert blob == g["emitted"].tobytes()
+    # ingest -> emit reproduces the input bytes exactly (io.py:164-166)
+    back = pkg.frames.matrix_to_frames(st32.matrix, st.frame_height, st.frame_width)
+    assert np.array_equal(back, g["raster"])
+
+
+def test_video_pipeline_end_to_end(tmp_path):
+    """cli.py:311-334 on the GPU: synthetic moving squares over a low-rank
+    background, ingested on the device, solved by ML-FWT, emitted as PGM."""
+    rng = np.random.default_rng(5)
+    h, w, count = 24, 32, 40
+    bg = (rng.uniform(0.2, 0.8, (h, w, 1)) * rng.uniform(0.8, 1.0, (1, 1, count)))
+    stack = np.repeat(bg, 1, axis=2)
+    for j in range(count):
+        r0, c0 = (j // 2) % (h - 6), j % (w - 6)
+        stack[r0:r0 + 6, c0:c0 + 6, j] = 1.0
+    raster = np.floor(np.clip(stack, 0, 1) * 255 + 0.5).astype(np.uint8).transpose(2, 0, 1)
+    paths = []
+    for j in range(count):
+        p = tmp_path / f"in_{j:03d}.pgm"
+        pkg.frames.write_pgm(raster[j], str(p))
+        paths.append(str(p))
+    state, st, written = pkg.frames.video(paths, str(tmp_path / "out"), solver="ml-fwt")
+    assert len(written) == 2 * count and state.iter >= 1
+    m = st.matrix.cpu().numpy()
+    assert m.shape == (h * w, count)
+    lam = 1.0 / np.sqrt(h * w)  # the CLI defaults, computed the same way (cli.py:192-198)
+    ref = pkg.ml_fwt_solve(m, None, pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(h * w), tol=1e-3,
+                                                      max_iters=2000, collect_rank=False))
+    assert ref.iter == state.iter
+    assert np.array_equal(np.asarray(ref.l), state.l.cpu().numpy())
+    first = pkg.frames.read_pgm(written[0])
+    assert first.shape == (h, w)
 
 
 # ------------------------------------------------------------------ ML-CPCP
