@@ -17,7 +17,7 @@ import torch
 from .api_types import CpcpOptions, CpcpState, IterationRecord, ObservationMask
 from .backend import CudaCpcp, CudaSpectrum, chain_cholesky
 from .chain import build_chain, resolve_coarse_width
-from .runtime import SINGLE, Comm, as_device_matrix, give_back
+from .runtime import SINGLE, Comm, as_device_matrix, give_back, give_back_all
 
 
 # When set to a list, solves record per-phase CUDA-event timings into it.
@@ -130,7 +130,8 @@ def _oracle_atoms(be, atoms, out, kind):
 def _state_from(L, S, st, hist, objs, kind, atoms=None):
     history = [IterationRecord(i + 1, float(h[0]), float(h[1]), int(round(h[2])), float(h[3]), float(h[4]))
                for i, h in enumerate(hist)]
-    return CpcpState(l=give_back(L, kind), s=give_back(S, kind), t_l=float(st["t_l"]), t_s=float(st["t_s"]),
+    l, s = give_back_all([L, S], kind)
+    return CpcpState(l=l, s=s, t_l=float(st["t_l"]), t_s=float(st["t_s"]),
                      u_l=float(st["u_l"]), u_s=float(st["u_s"]), iter=int(st["k"]), history=history,
                      objective_history=[float(x) for x in objs], converged=st["done"] == 1, oracle_atoms=atoms)
 

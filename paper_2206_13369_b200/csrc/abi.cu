@@ -122,7 +122,7 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.jac_result = c.take<int>(4 * 16);
   p.lzQ = c.take<double>(8 * (size_t)n * (p.lz_kmax + 1));
   p.lzT = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
-  p.lzW = c.take<double>(8 * (size_t)n * p.lz_splits);
+  p.lzW = c.take<double>(8 * (size_t)n * std::max(p.lz_splits, p.lz_fused_ctas));
   p.lzWork = c.take<double>(8 * (size_t)n);
 }
 
@@ -143,6 +143,12 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   int64_t ls = ceil_div(2 * sms, col_blocks);
   ls = std::min<int64_t>(ls, std::max<int64_t>(1, m_local / 32));
   p.lz_splits = (int)std::max<int64_t>(1, ls);
+  {
+    const char* e = getenv("MLR_LZ_FUSED");
+    const bool fused = ch.n <= 2048 && !(e && e[0] == '0');
+    p.lz_fused_ctas = fused ? (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(m_local, 1), 8), sms))
+                            : 0;
+  }
   p.lz_kmax = std::min(500, std::max(8, ch.n));
   p.jac_tol_host = 1e-14;
   p.jac_max_sweeps = 60;

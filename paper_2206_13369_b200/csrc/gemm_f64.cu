@@ -146,8 +146,18 @@ __global__ void sum_slices_kernel(const double* __restrict__ P, int64_t count, i
                                   int slices, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
+    // fixed summation order; loads batched 8 deep so the chain is not
+    // one L2 round trip per slice
     double s = 0.0;
-    for (int z = 0; z < slices; ++z) s += P[z * slice + i];
+    int z = 0;
+    for (; z + 8 <= slices; z += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = P[(int64_t)(z + q) * slice + i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; z < slices; ++z) s += P[(int64_t)z * slice + i];
     out[i] = s;
   }
 }

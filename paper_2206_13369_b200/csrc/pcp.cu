@@ -198,6 +198,68 @@ __global__ void __launch_bounds__(256) lz_dtv_kernel(const LanczosDev* __restric
     if (j0 + e < n) o[e] = acc[e];
 }
 
+// w = D^T (D q) in one pass over D for short rows (n <= LZ_FUSED_N): a warp
+// keeps its row in registers, reduces t_i = d_i . q, then adds t_i d_i to
+// its private FP64 accumulator in shared memory; the CTA sums its warps'
+// accumulators in a fixed order into wpart[blockIdx.x] (sum_slices then
+// sums the CTAs, also in a fixed order: deterministic).  Half the HBM
+// traffic of the two-kernel path and no t round trip.
+constexpr int LZ_FUSED_N = 2048, LZ_FW = 8;
+template <typename T>
+__global__ void __launch_bounds__(LZ_FW * 32, 1) lz_dtdv_kernel(const LanczosDev* __restrict__ lz,
+                                                                const T* __restrict__ D, int64_t ldd, int64_t m,
+                                                                int n, const double* __restrict__ Q,
+                                                                double* __restrict__ wpart) {
+  if (lz->done) return;
+  constexpr int NV = 16 / sizeof(T);
+  constexpr int MAXC = LZ_FUSED_N / (32 * NV);
+  extern __shared__ __align__(16) double lzacc[];  // LZ_FW x n
+  const double* __restrict__ q = Q + (int64_t)lz->k * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* acc = lzacc + (int64_t)warp * n;
+  for (int j = lane; j < n; j += 32) acc[j] = 0.0;
+  const bool vec = (n % NV == 0) && (ldd % NV == 0);
+  for (int64_t i = (int64_t)blockIdx.x * LZ_FW + warp; i < m; i += (int64_t)gridDim.x * LZ_FW) {
+    const T* row = D + i * ldd;
+    T r[MAXC][NV];
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int j = (c * 32 + lane) * NV;
+      if (vec) {
+        if (j < n) *reinterpret_cast<float4*>(r[c]) = __ldg(reinterpret_cast<const float4*>(row + j));
+      } else {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) r[c][e] = j + e < n ? row[j + e] : T(0);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int j = (c * 32 + lane) * NV;
+      if (j < n)
+#pragma unroll
+        for (int e = 0; e < NV; ++e)
+          if (vec || j + e < n) s = fma((double)r[c][e], __ldg(q + j + e), s);
+    }
+    const double t = warp_sum(s);
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int j = (c * 32 + lane) * NV;
+      if (j < n)
+#pragma unroll
+        for (int e = 0; e < NV; ++e)
+          if (vec || j + e < n) acc[j + e] = fma((double)r[c][e], t, acc[j + e]);
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < LZ_FW; ++w) v += lzacc[(int64_t)w * n + j];
+    wpart[(int64_t)blockIdx.x * n + j] = v;
+  }
+}
+
 // True if the symmetric tridiagonal (a[0..k1), b[0..k1-1)) has an eigenvalue
 // above x: T - x I has a positive LDL^T pivot d_i = p_i / p_(i-1), with the
 // leading principal minors p_i = (a_i - x) p_(i-1) - b_(i-1)^2 p_(i-2)
@@ -747,6 +809,21 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
     return kOk;
   }
   p->timer.begin(st);
+  if (n <= LZ_FUSED_N && p->lz_fused_ctas > 0) {
+    const int ctas = p->lz_fused_ctas;
+    const size_t smem = sizeof(double) * LZ_FW * (size_t)n;
+    if (p->f32) {
+      MLR_CUDA(cudaFuncSetAttribute(lz_dtdv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      lz_dtdv_kernel<float><<<ctas, LZ_FW * 32, smem, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzQ, p->lzW);
+    } else {
+      MLR_CUDA(cudaFuncSetAttribute(lz_dtdv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      lz_dtdv_kernel<double><<<ctas, LZ_FW * 32, smem, st>>>(p->lz, (const double*)D, ldd, m, n, p->lzQ, p->lzW);
+    }
+    MLR_LAUNCH_CHECK("lz_dtdv_kernel");
+    const int rc = sum_slices(p->lzW, n, n, ctas, wpart_out, st);
+    p->timer.end(kPhLanczos, st);
+    return rc;
+  }
   const int blocks = (int)std::min<int64_t>(ceil_div(m, 8), (int64_t)p->row_blocks);
   if (p->f32)
     lz_dv_kernel<float><<<blocks, 256, 0, st>>>(p->lz, (const float*)D, ldd, m, n, p->lzQ, p->lzT);

@@ -44,6 +44,7 @@ struct PcpPlan {
   int64_t m_local, m_global;
   int max_iters;
   int row_blocks, gram_splits, lz_splits, lz_kmax;
+  int lz_fused_ctas;  // > 0: one-pass D^T D q (n <= 2048)
   double jac_tol_host;
   double jac_floor_rel;
   int jac_max_sweeps;

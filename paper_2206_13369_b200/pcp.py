@@ -16,7 +16,7 @@ import torch
 from .api_types import IterationRecord, MultilevelDiagnostics, PcpOptions, PcpState, SvdError
 from .backend import CudaPcp, CudaSpectrum
 from .chain import build_chain, resolve_coarse_width
-from .runtime import SINGLE, Comm, as_device_matrix, give_back
+from .runtime import SINGLE, Comm, as_device_matrix, give_back, give_back_all
 
 LANCZOS_TOL = 1e-15
 
@@ -35,7 +35,10 @@ def _zero_state(shape, kind, like):
 def _jacobi_tol(opts, f32):
     if opts.jacobi_tol is not None:
         return float(opts.jacobi_tol)
-    return 1e-9 if f32 else 64 * np.finfo(np.float64).eps
+    # FP32 data carries ~6e-8 relative noise; a 1e-6 relative off-diagonal
+    # test leaves relF(L) vs the FP64 oracle unchanged on C2 (4.8e-6 vs 4.7e-6
+    # at 1e-9) and saves ~10% of the sweeps (tools/gpu/jacobi_tol_sweep.py)
+    return 1e-6 if f32 else 64 * np.finfo(np.float64).eps
 
 
 def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
@@ -140,7 +143,8 @@ def diagnostics(be, comm, chain, coarse, k, m_global):
 def _state_from(L, S, Yk, st, hist, kind):
     history = [IterationRecord(i + 1, float(h[0]), float(h[1]), int(round(h[2])), float(h[3]), float(h[4]))
                for i, h in enumerate(hist)]
-    return PcpState(l=give_back(L, kind), s=give_back(S, kind), y=give_back(Yk, kind), mu=float(st["mu_final"]),
+    l, s, y = give_back_all([L, S, Yk], kind)
+    return PcpState(l=l, s=s, y=y, mu=float(st["mu_final"]),
                     iter=int(st["k"]), history=history, mu_history=[float(x) for x in hist[:, 5]],
                     converged=st["done"] == 1)
 
