@@ -36,7 +36,7 @@ def _jacobi_tol(opts, f32):
     if opts.jacobi_tol is not None:
         return float(opts.jacobi_tol)
     # FP32 data carries ~6e-8 relative noise; a 1e-6 relative off-diagonal
-    # test leaves relF(L) vs the FP64 oracle unchanged on C2 (4.8e-6 vs 4.7e-6
+    # test leaves relF(L) vs the FP64 reference unchanged on C2 (4.8e-6 vs 4.7e-6
     # at 1e-9) and saves ~10% of the sweeps (tools/gpu/jacobi_tol_sweep.py)
     return 1e-6 if f32 else 64 * np.finfo(np.float64).eps
 
