@@ -285,6 +285,22 @@ int mlr_chain_create(int n, int nh, const int32_t* c0, const double* w0, const d
       best = std::max(best, run);
     }
     d.max_run = best;
+    // regular chain (repeated halving, n = n_H * 2^L): c0[j] = max(0, (j+1)/P - 1)
+    // and no w1 weight on the first fine column of a run; the row kernels then
+    // restrict with fixed lane groups instead of the general segmented scan
+    d.reg_lgp = 0;
+    const char* env = getenv("MLR_REG_CHAIN");
+    if (nh >= 2 && n % nh == 0 && !(env && env[0] == '0')) {
+      const int P = n / nh;
+      int lg = 0;
+      while ((1 << lg) < P) ++lg;
+      bool reg = (1 << lg) == P && P >= 2 && P <= 64;
+      for (int j = 0; j < n && reg; ++j) {
+        reg = c0[j] == std::max(0, (j + 1) / P - 1);
+        if ((j + 1) % P == 0 || j < P - 1) reg = reg && w1[j] == 0.0;
+      }
+      if (reg) d.reg_lgp = lg;
+    }
   }
   auto up = [&](void** dst, const void* src, size_t bytes) -> int {
     void* p = nullptr;

@@ -132,6 +132,21 @@ template <typename T, int NV>
 struct StencilVec {
   int key[NV];
   T w0[NV], w1[NV];
+  // weights only (regular chains compute the keys): zero past n
+  __device__ __forceinline__ void loadw(const T* __restrict__ w0p, const T* __restrict__ w1p, int n, int j) {
+    using VT = Vec<T>;
+    if (j + NV <= n) {
+      VT::unpack(__ldg(reinterpret_cast<const typename VT::V*>(w0p + j)), w0);
+      VT::unpack(__ldg(reinterpret_cast<const typename VT::V*>(w1p + j)), w1);
+    } else {
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const bool in = j + e < n;
+        w0[e] = in ? __ldg(w0p + j + e) : T(0);
+        w1[e] = in ? __ldg(w1p + j + e) : T(0);
+      }
+    }
+  }
   __device__ __forceinline__ void load(const int* __restrict__ c0, const T* __restrict__ w0p,
                                        const T* __restrict__ w1p, int n, int j) {
     using VT = Vec<T>;
@@ -311,6 +326,66 @@ struct SegRestrict {
   }
 };
 
+// Restriction for regular chains (repeated halving, n = n_H * P, P = 2^lgp,
+// c0[j] = max(0, (j+1)/P - 1)).  Fine columns [pP, pP + P) are one group of
+// L = P/NV lanes: their w1 parts and the w0 part of the group's last column
+// (the first column of run p, whose w1 is zero) belong to coarse key p ("B"),
+// the other w0 parts to key p - 1 ("A"; key 0 for the row's first group).
+// Key p = B_p + A_{p+1}: a butterfly over the group, one shuffle from the
+// next group, and a carry across chunks.  No keys, ballots or staging;
+// fixed summation order (deterministic).
+template <typename T, int NB, int NV>
+struct RegRestrict {
+  T carry[NB];
+  bool have;
+  __device__ __forceinline__ void begin() { have = false; }
+
+  __device__ __forceinline__ void chunk(const T (&w0)[NV], const T (&w1)[NV], const T (&x)[NB][NV], int cbase,
+                                        T* const (&out)[NB], int lane, int lgp) {
+    constexpr int CH = 32 * NV;
+    const int L = (1 << lgp) / NV;  // lanes per group (1..32)
+    const bool last_lane = (lane & (L - 1)) == L - 1;
+    const bool first_group = cbase == 0 && lane < L;
+    const int pbase = cbase >> lgp;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      T a = T(0), bb = T(0);
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const T p0 = w0[e] * x[b][e];
+        if (e == NV - 1 && last_lane) bb += p0; else a += p0;
+        bb = fma(w1[e], x[b][e], bb);
+      }
+      if (first_group) {
+        bb += a;
+        a = T(0);
+      }
+#pragma unroll
+      for (int st = 0; st < 5; ++st) {
+        const int o = 1 << st;
+        if (o >= L) break;
+        a += __shfl_xor_sync(kFull, a, o);
+        bb += __shfl_xor_sync(kFull, bb, o);
+      }
+      const T an = L < 32 ? __shfl_down_sync(kFull, a, L) : T(0);
+      if ((lane & (L - 1)) == 0 && lane + L < 32) out[b][pbase + (lane >> (lgp - (NV == 4 ? 2 : 1)))] = bb + an;
+      if (lane == 0 && have) out[b][pbase - 1] = carry[b] + a;
+      carry[b] = __shfl_sync(kFull, bb, 31);
+    }
+    have = true;
+    (void)CH;
+  }
+
+  // the last group of the row's last chunk has no successor; zero the rest of [.., np)
+  __device__ __forceinline__ void finish(T* const (&out)[NB], int n, int np, int lane, int lgp) {
+    constexpr int CH = 32 * NV;
+    const int plast = (((n + CH - 1) / CH) * CH >> lgp) - 1;
+    for (int k = plast + lane; k < np; k += 32)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) out[b][k] = k == plast ? carry[b] : T(0);
+  }
+};
+
 __host__ __device__ __forceinline__ int seg_scan_steps(int max_run, int nv) {
   const int lanes = min(32, (max_run + 2 * nv - 2) / nv);  // lanes one run can touch
   int s = 0;
@@ -321,7 +396,7 @@ __host__ __device__ __forceinline__ int seg_scan_steps(int max_run, int nv) {
 // -------------------------------------------------------------------- ML-PCP
 enum RowModeW { kWStart = 0, kWUpdate = 1, kWOutput = 2 };
 
-template <typename T, int MODE, bool RING>
+template <typename T, int MODE, bool RING, bool REG>
 __global__ void __launch_bounds__(RW_THREADS, 3)
 pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __restrict__ D, int64_t ldd,
               const T* __restrict__ Yin, T* __restrict__ Yout, int64_t ldy, const T* __restrict__ Z,
@@ -337,10 +412,12 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   const int steps = seg_scan_steps(ch.max_run, NV);
   const int zlen = round_up_dev(np + 2, 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES + (RING ? RING_BYTES : 0));
+  constexpr int STAGE = REG ? 0 : SR::STAGE_BYTES;
+  const int lgp = ch.reg_lgp;
+  unsigned char* wbase = smem_raw + (size_t)warp * (zlen * sizeof(T) + STAGE + (RING ? RING_BYTES : 0));
   T* zrow = reinterpret_cast<T*>(wbase);
   unsigned char* stage = wbase + zlen * sizeof(T);
-  const LaneRing ring{stage + SR::STAGE_BYTES};
+  const LaneRing ring{stage + STAGE};
 
   const double mu_d = st->mu;
   const T inv = (T)(1.0 / mu_d);
@@ -352,6 +429,7 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   const bool vec = (ldd % NV == 0) && (ldy % NV == 0) && (MODE != kWOutput || ldo % NV == 0);
   const bool pipe = RING && vec;
   SR sr;
+  RegRestrict<T, 1, NV> rr;
   const int nc = (n + CH - 1) / CH;
   const int64_t first = (int64_t)blockIdx.x * RW_WARPS + warp, stride = (int64_t)gridDim.x * RW_WARPS;
   // prefetch cursor: (row, chunk, ring slot) of the next chunk to stage
@@ -382,7 +460,7 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
     }
     const T* drow = D + i * ldd;
     const T* yrow = Yin + i * ldy;
-    sr.begin(stage);
+    if (REG) rr.begin(); else sr.begin(stage);
     T* const outp[1] = {A + i * np};
     T dn[NV], yn[NV];  // register path: one chunk in flight
     if (!pipe) {
@@ -416,7 +494,7 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
         }
       }
       StencilVec<T, NV> sv;
-      sv.load(c0p, w0p, w1p, n, j);
+      if (REG) sv.loadw(w0p, w1p, n, j); else sv.load(c0p, w0p, w1p, n, j);
       T x[1][NV], yo[NV], lo_v[NV], so_v[NV];
       T c_res = T(0), c_l1 = T(0);
       int c_nnz = 0;
@@ -429,7 +507,7 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
           yo[e] = y;
           x[0][e] = y * inv + d;
         } else {
-          const int c = min(sv.key[e], np);
+          const int c = REG ? max(0, ((j + e + 1) >> lgp) - 1) : min(sv.key[e], np);
           const T l = sv.w0[e] * zrow[c] + sv.w1[e] * zrow[c + 1];
           const T y = yv[e];
           const T w = y * inv + d - l;
@@ -458,9 +536,14 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
         continue;
       }
       store_vec<T, NV>(Yout + i * ldy, j, n, vec, yo);
-      sr.chunk(sv, x, cbase + CH < n ? __ldg(c0p + cbase + CH) : INT_MAX, outp, lane, steps);
+      if (REG)
+        rr.chunk(sv.w0, sv.w1, x, cbase, outp, lane, lgp);
+      else
+        sr.chunk(sv, x, cbase + CH < n ? __ldg(c0p + cbase + CH) : INT_MAX, outp, lane, steps);
     }
-    if (MODE != kWOutput) sr.finish(outp, nh, np, lane);
+    if (MODE != kWOutput) {
+      if (REG) rr.finish(outp, n, np, lane, lgp); else sr.finish(outp, nh, np, lane);
+    }
     __syncwarp();
   }
   cp_wait<0>();
@@ -477,11 +560,17 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
 }
 
 bool rows_warp_ok(const ChainDev& ch, bool) { return ch.keys_dense != 0; }
+// regular chains whose groups are whole lanes and fit a chunk
+static bool rows_reg_ok(const ChainDev& ch, bool f32) {
+  const int nv = f32 ? 4 : 2, P = 1 << ch.reg_lgp;
+  return ch.reg_lgp > 0 && P >= nv && P <= 32 * nv;
+}
 
 int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy, void* Lout,
              void* Sout, int64_t ldo, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
-  const size_t stage = p->f32 ? SegRestrict<float, 1, 4>::STAGE_BYTES : SegRestrict<double, 1, 2>::STAGE_BYTES;
+  const bool reg = rows_reg_ok(p->ch, p->f32);
+  const size_t stage = reg ? 0 : (p->f32 ? SegRestrict<float, 1, 4>::STAGE_BYTES : SegRestrict<double, 1, 2>::STAGE_BYTES);
   // the cp.async ring only while 3 CTAs per SM still fit (occupancy first)
   const size_t base = RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
   const bool ring = base + RW_WARPS * RING_BYTES <= 80 * 1024;
@@ -489,7 +578,8 @@ int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, 
   const int blocks = p->row_blocks;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
-    auto kern = ring ? pcp_rows_warp<T, MODE, true> : pcp_rows_warp<T, MODE, false>;                                                                         \
+    auto kern = reg ? (ring ? pcp_rows_warp<T, MODE, true, true> : pcp_rows_warp<T, MODE, false, true>)          \
+                    : (ring ? pcp_rows_warp<T, MODE, true, false> : pcp_rows_warp<T, MODE, false, false>);       \
     MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
     kern<<<blocks, RW_THREADS, smem, st>>>(p->dev, p->ch, p->m_local, (const T*)D, ldd, (const T*)Yin, (T*)Yout, \
                                            ldy, (const T*)p->Z, (T*)p->A, (T*)Lout, (T*)Sout, ldo, p->row_part); \
@@ -515,7 +605,7 @@ __device__ __forceinline__ void am_merge_w(AmRecW& a, const AmRecW& b) {
 
 enum CpModeW { kCWInit = 0, kCWUpdate = 1, kCWOutput = 2 };
 
-template <typename T, int MODE, bool RING>
+template <typename T, int MODE, bool RING, bool REG>
 __global__ void __launch_bounds__(RW_THREADS, 3)
 cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row0, int64_t m_global,
              const T* __restrict__ D, int64_t ldd, const uint32_t* __restrict__ mask, int64_t ldm, T* __restrict__ S,
@@ -533,11 +623,13 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   const int zlen = round_up_dev(np + 2, 4);
   double* vs = reinterpret_cast<double*>(smem_raw);  // v (np), CTA-shared
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int STAGE = REG ? 0 : SR::STAGE_BYTES;
+  const int lgp = ch.reg_lgp;
   unsigned char* wbase =
-      smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * (zlen * sizeof(T) + SR::STAGE_BYTES + (RING ? RING_BYTES : 0));
+      smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * (zlen * sizeof(T) + STAGE + (RING ? RING_BYTES : 0));
   T* lrow = reinterpret_cast<T*>(wbase);
   unsigned char* stage = wbase + zlen * sizeof(T);
-  const LaneRing ring{stage + SR::STAGE_BYTES};
+  const LaneRing ring{stage + STAGE};
   if (MODE == kCWUpdate)
     for (int k = threadIdx.x; k < np; k += blockDim.x) vs[k] = vg[k];
   __syncthreads();
@@ -557,6 +649,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   long long bidx = -1;
   const bool vec = (ldd % NV == 0) && (lds % NV == 0) && (MODE != kCWOutput || ldl % NV == 0);
   SR sr;
+  RegRestrict<T, 2, NV> rr;
   const int nc = (n + CH - 1) / CH;
   const int64_t first = (int64_t)blockIdx.x * RW_WARPS + warp, stride = (int64_t)gridDim.x * RW_WARPS;
   const bool pipe = RING && vec && MODE != kCWOutput;
@@ -600,7 +693,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
     const uint32_t* mrow = mask ? mask + i * ldm : nullptr;
     const long long gi = row0 + i;
     const bool spike_row = spike_on && gi == i_s;
-    sr.begin(stage);
+    if (REG) rr.begin(); else sr.begin(stage);
     T* const outs[2] = {GH + i * np, SH + i * np};
     T dn[NV], sn_[NV];  // register path: one chunk in flight
     uint32_t bitn = 0xffffffffu;
@@ -613,12 +706,12 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
       const int cbase = c * CH;
       const int j = cbase + lane * NV;
       StencilVec<T, NV> sv;
-      sv.load(c0p, w0p, w1p, n, j);
+      if (REG) sv.loadw(w0p, w1p, n, j); else sv.load(c0p, w0p, w1p, n, j);
       if (MODE == kCWOutput) {
         T lv[NV];
 #pragma unroll
         for (int e = 0; e < NV; ++e) {
-          const int c = min(sv.key[e], np);
+          const int c = REG ? max(0, ((j + e + 1) >> lgp) - 1) : min(sv.key[e], np);
           lv[e] = sv.w0[e] * lrow[c] + sv.w1[e] * lrow[c + 1];
         }
         store_vec<T, NV>(Lout + i * ldl, j, n, vec, lv);
@@ -669,7 +762,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
         }
 #pragma unroll
         for (int e = 0; e < NV; ++e) {
-          const int c = min(sv.key[e], np);
+          const int c = REG ? max(0, ((j + e + 1) >> lgp) - 1) : min(sv.key[e], np);
           const T l = sv.w0[e] * lrow[c] + sv.w1[e] * lrow[c + 1];
           const T d = dv[e];
           const bool obs = (bits >> e) & 1u;
@@ -707,9 +800,14 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
       a_ss += (double)c_ss;
       a_sr += (double)c_sr;
       if (MODE == kCWUpdate) store_vec<T, NV>(sro, j, n, vec, x[1]);
-      sr.chunk(sv, x, cbase + CH < n ? __ldg(c0p + cbase + CH) : INT_MAX, outs, lane, steps);
+      if (REG)
+        rr.chunk(sv.w0, sv.w1, x, cbase, outs, lane, lgp);
+      else
+        sr.chunk(sv, x, cbase + CH < n ? __ldg(c0p + cbase + CH) : INT_MAX, outs, lane, steps);
     }
-    if (MODE != kCWOutput) sr.finish(outs, nh, np, lane);
+    if (MODE != kCWOutput) {
+      if (REG) rr.finish(outs, n, np, lane, lgp); else sr.finish(outs, nh, np, lane);
+    }
     __syncwarp();
   }
   cp_wait<0>();
@@ -745,14 +843,16 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
 int cp_rows(CpcpPlan* p, int mode, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S,
             int64_t lds, void* Lout, int64_t ldl, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
-  const size_t stage = p->f32 ? SegRestrict<float, 2, 4>::STAGE_BYTES : SegRestrict<double, 2, 2>::STAGE_BYTES;
+  const bool reg = rows_reg_ok(p->ch, p->f32);
+  const size_t stage = reg ? 0 : (p->f32 ? SegRestrict<float, 2, 4>::STAGE_BYTES : SegRestrict<double, 2, 2>::STAGE_BYTES);
   const size_t base = (size_t)round_up(p->ch.np * 8, 16) + RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
   const bool ring = base + RW_WARPS * RING_BYTES <= 80 * 1024;
   const size_t smem = base + (ring ? RW_WARPS * RING_BYTES : 0);
   const int blocks = p->row_blocks;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
-    auto kern = ring ? cp_rows_warp<T, MODE, true> : cp_rows_warp<T, MODE, false>;                                                                          \
+    auto kern = reg ? (ring ? cp_rows_warp<T, MODE, true, true> : cp_rows_warp<T, MODE, false, true>)            \
+                    : (ring ? cp_rows_warp<T, MODE, true, false> : cp_rows_warp<T, MODE, false, false>);         \
     MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
     kern<<<blocks, RW_THREADS, smem, st>>>(p->dev, p->ch, p->m_local, p->row0, p->m_global, (const T*)D, ldd,    \
                                            mask, ldm, (T*)S, lds, (T*)p->LH, (T*)p->GH, (T*)p->SH, p->u, p->v, \
