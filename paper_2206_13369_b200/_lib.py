@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_double, c_int, c_int64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmlr_b200.so")
+LIB_PATH = os.environ.get("MLR_LIB_PATH") or os.path.join(_HERE, "libmlr_b200.so")  # override: A/B builds
 
 _lib = None
 

@@ -396,12 +396,13 @@ __host__ __device__ __forceinline__ int seg_scan_steps(int max_run, int nv) {
 // -------------------------------------------------------------------- ML-PCP
 enum RowModeW { kWStart = 0, kWUpdate = 1, kWOutput = 2 };
 
-template <typename T, int MODE, bool RING, bool REG>
+template <typename T, int MODE, bool RING, int RG>
 __global__ void __launch_bounds__(RW_THREADS, 3)
 pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __restrict__ D, int64_t ldd,
               const T* __restrict__ Yin, T* __restrict__ Yout, int64_t ldy, const T* __restrict__ Z,
               T* __restrict__ A, T* __restrict__ Lout, T* __restrict__ Sout, int64_t ldo, double* __restrict__ part) {
   if (MODE == kWUpdate && st->done) return;
+  constexpr bool REG = RG > 0;  // regular chain; RG == 2: stencil weights held in registers (long rows)
   using SR = SegRestrict<T, 1, Vec<T>::N>;
   constexpr int NV = Vec<T>::N, CH = 32 * NV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -430,6 +431,18 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   const bool pipe = RING && vec;
   SR sr;
   RegRestrict<T, 1, NV> rr;
+  // regular chains: a lane's stencil weights depend only on its position in
+  // the chunk (the phase (j+1) mod P) except in chunk 0, so they are loaded
+  // once per kernel instead of once per chunk
+  T rw0[NV], rw1[NV];
+  constexpr bool wreg = RG == 2;
+  if (wreg) {
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      rw0[e] = __ldg(w0p + CH + lane * NV + e);
+      rw1[e] = __ldg(w1p + CH + lane * NV + e);
+    }
+  }
   const int nc = (n + CH - 1) / CH;
   const int64_t first = (int64_t)blockIdx.x * RW_WARPS + warp, stride = (int64_t)gridDim.x * RW_WARPS;
   // prefetch cursor: (row, chunk, ring slot) of the next chunk to stage
@@ -494,7 +507,17 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
         }
       }
       StencilVec<T, NV> sv;
-      if (REG) sv.loadw(w0p, w1p, n, j); else sv.load(c0p, w0p, w1p, n, j);
+      if (wreg && cbase > 0) {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          sv.w0[e] = j + e < n ? rw0[e] : T(0);
+          sv.w1[e] = j + e < n ? rw1[e] : T(0);
+        }
+      } else if (REG) {
+        sv.loadw(w0p, w1p, n, j);
+      } else {
+        sv.load(c0p, w0p, w1p, n, j);
+      }
       T x[1][NV], yo[NV], lo_v[NV], so_v[NV];
       T c_res = T(0), c_l1 = T(0);
       int c_nnz = 0;
@@ -576,10 +599,13 @@ int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, 
   const bool ring = base + RW_WARPS * RING_BYTES <= 80 * 1024;
   const size_t smem = base + (ring ? RW_WARPS * RING_BYTES : 0);
   const int blocks = p->row_blocks;
+  // weights in registers pay off on long rows only (measured: C5 -13%, C2 +7%)
+  const int rg = reg ? (p->ch.n >= 16 * 32 * (p->f32 ? 4 : 2) ? 2 : 1) : 0;
 #define MLR_LAUNCH(T, MODE)                                                                                     \
   {                                                                                                             \
-    auto kern = reg ? (ring ? pcp_rows_warp<T, MODE, true, true> : pcp_rows_warp<T, MODE, false, true>)          \
-                    : (ring ? pcp_rows_warp<T, MODE, true, false> : pcp_rows_warp<T, MODE, false, false>);       \
+    auto kern = rg == 2 ? (ring ? pcp_rows_warp<T, MODE, true, 2> : pcp_rows_warp<T, MODE, false, 2>)            \
+              : rg == 1 ? (ring ? pcp_rows_warp<T, MODE, true, 1> : pcp_rows_warp<T, MODE, false, 1>)            \
+                        : (ring ? pcp_rows_warp<T, MODE, true, 0> : pcp_rows_warp<T, MODE, false, 0>);           \
     MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
     kern<<<blocks, RW_THREADS, smem, st>>>(p->dev, p->ch, p->m_local, (const T*)D, ldd, (const T*)Yin, (T*)Yout, \
                                            ldy, (const T*)p->Z, (T*)p->A, (T*)Lout, (T*)Sout, ldo, p->row_part); \
@@ -706,6 +732,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
       const int cbase = c * CH;
       const int j = cbase + lane * NV;
       StencilVec<T, NV> sv;
+      // (per-lane weights in registers, as in pcp_rows_warp, spill here)
       if (REG) sv.loadw(w0p, w1p, n, j); else sv.load(c0p, w0p, w1p, n, j);
       if (MODE == kCWOutput) {
         T lv[NV];
