@@ -139,6 +139,14 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   int64_t splits = ceil_div(2 * sms, tiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
+  {
+    // coarse n_p^3 products: about one CTA per SM, K chunks of >= 32
+    const int64_t t2 = (int64_t)(ch.np / 64) * (ch.np / 64);
+    int64_t ks = std::min<int64_t>(ceil_div(sms, t2), ch.np / 32);
+    const char* e = getenv("MLR_COARSE_KSPLIT");
+    if (e) ks = atoi(e);
+    p.coarse_ksplit = (int)std::max<int64_t>(1, std::min<int64_t>(ks, p.gram_splits));
+  }
   const int64_t col_blocks = ceil_div(ch.n, 2048);  // lz_dtv_kernel tiles: row blocks x 2048 columns
   int64_t ls = ceil_div(2 * sms, col_blocks);
   ls = std::min<int64_t>(ls, std::max<int64_t>(1, m_local / 32));

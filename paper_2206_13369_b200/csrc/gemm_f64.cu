@@ -143,7 +143,8 @@ gemm_f64_kernel(int M, int N, int K, const TA* __restrict__ A, int64_t lda,
 
 // Deterministic sum of `slices` partial matrices (contiguous, stride `slice`).
 __global__ void sum_slices_kernel(const double* __restrict__ P, int64_t count, int64_t slice,
-                                  int slices, double* __restrict__ out) {
+                                  int slices, double* __restrict__ out, const int* __restrict__ skip) {
+  if (skip && *skip) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
     // fixed summation order; loads batched 8 deep so the chain is not
@@ -202,10 +203,10 @@ int gemm_f64(GemmSpec g, cudaStream_t st) {
 }
 
 int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out,
-               cudaStream_t st) {
+               cudaStream_t st, const int* skip) {
   int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 148 * 8);
   if (blocks < 1) blocks = 1;
-  sum_slices_kernel<<<blocks, 256, 0, st>>>(P, count, slice, slices, out);
+  sum_slices_kernel<<<blocks, 256, 0, st>>>(P, count, slice, slices, out, skip);
   MLR_LAUNCH_CHECK("sum_slices_kernel");
   return kOk;
 }

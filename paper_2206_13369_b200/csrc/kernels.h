@@ -32,7 +32,8 @@ int gemm_f64(GemmSpec g, cudaStream_t st);
 int frames_to_matrix(const uint8_t* frames, int count, int H, int W, bool f32, void* x, int64_t ldx, cudaStream_t st);
 int matrix_to_frames(const void* x, int64_t ldx, bool f32, int count, int H, int W, uint8_t* frames,
                      cudaStream_t st);
-int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st);
+int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st,
+               const int* skip = nullptr);
 
 // ---------------------------------------------------------------- jacobi
 

@@ -989,14 +989,21 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   // Warm start: with V the previous eigenvectors and U = G^-1 V,
   //   B~ = V^T (G^-1 K G^-1) V = U^T K U       (M_H = A G^-1, B = M_H^T M_H)
   p->timer.begin(st);
+  // n_p^3 products: (n_p/64)^2 output tiles are too few CTAs for small n_p,
+  // so K is split (slices in gram_part, free between Gram passes) and the
+  // slices summed in a fixed order
+  const int ksplit = p->coarse_ksplit;
   auto mm = [&](const double* A, bool ta, const double* Bp, bool tb, double* C, const double* ks) {
     GemmSpec g{};
     g.M = np; g.N = np; g.K = np;
     g.A = A; g.lda = np; g.a_f32 = false; g.trans_a = ta;
     g.B = Bp; g.ldb = np; g.b_f32 = false; g.trans_b = tb;
-    g.C = C; g.ldc = np; g.c_f32 = false; g.c_slice = 0; g.splits = 1; g.alpha = 1.0;
+    g.C = ksplit > 1 ? p->gram_part : C; g.ldc = np; g.c_f32 = false;
+    g.c_slice = ksplit > 1 ? (int64_t)np * np : 0; g.splits = ksplit; g.alpha = 1.0;
     g.kscale = ks; g.skip = skip;
-    return gemm_f64(g, st);
+    int rc = gemm_f64(g, st);
+    if (rc || ksplit <= 1) return rc;
+    return sum_slices(p->gram_part, (int64_t)np * np, (int64_t)np * np, ksplit, C, st, skip);
   };
   if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;   // U = G^-1 V
   if ((rc = mm(red, false, p->T1, false, p->Xm, nullptr))) return rc;        // T = K U

@@ -45,6 +45,7 @@ struct PcpPlan {
   int max_iters;
   int row_blocks, gram_splits, lz_splits, lz_kmax;
   int lz_fused_ctas;  // > 0: one-pass D^T D q (n <= 2048)
+  int coarse_ksplit;  // split-K of the n_p^3 coarse products (<= gram_splits)
   double jac_tol_host;
   double jac_floor_rel;
   int jac_max_sweeps;
