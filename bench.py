@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -297,10 +298,12 @@ def main():
                "sample": f"1 full C2 solve ({it} iterations, oracle port of mlrpca.ml_ialm_solve, numpy/OpenBLAS FP64)"}
 
     lz = statistics.mean(s.get("lanczos_steps", 0) for s in sink) if sink else 0
-    # launches per solve (see profiles/r01_bench_launches_c2.md): 15 per iteration
-    # (gram 2, pre 3, jacobi 2, after/weights 2, post 2, recon 1, update 2, finalize 1),
-    # 4 per Lanczos step, ~12 fixed (stats, start, outputs)
-    per_solve_launches = (15 * (iters / args.steps) + 4 * lz + 12)
+    # launches per solve (counted in profiles/r01_bench_launches_c2.csv: 787 per C2 solve):
+    # 20 per loop call (gram 3, pre 6 incl. split-K sums, jacobi + V update 2,
+    # after/weights 2, post 4, recon 1, update 1, finalize 1; the host polls every
+    # 4 calls), 3 per Lanczos step (D^T D q, slice sum, update), 11 fixed
+    calls = 4 * math.ceil((iters / args.steps) / 4)
+    per_solve_launches = 20 * calls + 3 * lz + 11
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

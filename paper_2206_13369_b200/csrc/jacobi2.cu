@@ -1145,7 +1145,13 @@ j2_vapply_kernel(double* __restrict__ V, int np, int nrows_v, const double* __re
   }
 }
 
-static int vapply_rows(int np) { return (size_t)16 * (np + 2) * sizeof(double) <= 200 * 1024 ? 16 : 8; }
+// 16-row tiles while that still gives ~32+ CTAs; 8-row tiles otherwise (more
+// CTAs for small n_p, or a 16-row tile no longer fits shared memory)
+static int vapply_rows(int np) {
+  const char* e = getenv("MLR_VA_ROWS");
+  if (e) return atoi(e) == 16 ? 16 : 8;
+  return (size_t)16 * (np + 2) * sizeof(double) <= 200 * 1024 && np / 16 >= 32 ? 16 : 8;
+}
 static size_t vapply_smem(int np) { return (size_t)vapply_rows(np) * (np + 2) * sizeof(double); }
 
 // Rotation-log capacity in steps: whole sweeps, up to 60, within ~128 MB.
