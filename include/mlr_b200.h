@@ -100,6 +100,15 @@ int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, 
                     int64_t ldo, void* stream);
 /* out16: k, done, status, rank, mu, mu_final, mu_last, nuclear, sigma1, d_norm, jac_sweeps, tau, scale, lam, 0, 0 */
 int mlr_pcp_state(void* plan, double* out16, void* stream);
+/* Pipelined polling: mlr_pcp_snapshot enqueues an asynchronous copy of the
+ * plan's device state (solver + Lanczos) into `host` (pinned, at least
+ * mlr_pcp_snapshot_bytes()) and returns at once; after the caller has waited on
+ * an event recorded behind it, mlr_pcp_snapshot_read decodes it into the
+ * mlr_pcp_state / mlr_pcp_lanczos_state layouts (either output may be NULL).
+ * The host can keep the next batch of steps queued while it waits. */
+int64_t mlr_pcp_snapshot_bytes(void);
+int mlr_pcp_snapshot(void* plan, void* host, void* stream);
+int mlr_pcp_snapshot_read(const void* host, double* out16, double* lz4);
 int mlr_pcp_history(void* plan, int count, double* out, void* stream); /* count x 8 */
 /* Truncated SVT of the full-width baseline ialm_solve (reference pcp.py:118-197,
  * svd_truncated linalg.py:102-125): with sv0 > 0 only the top-sv singular values
@@ -133,6 +142,10 @@ int mlr_cpcp_finalize(void* plan, const double* red, void* stream);
 int mlr_cpcp_outputs(void* plan, void* L, int64_t ldl, void* stream);
 /* out32: k, done, status, t_l, t_s, u_l, u_s, sigma, passes, ga, gb, corner_l, corner_s, i_s, j_s, s2, ... */
 int mlr_cpcp_state(void* plan, double* out32, void* stream);
+/* pipelined polling, as mlr_pcp_snapshot / mlr_pcp_snapshot_read */
+int64_t mlr_cpcp_snapshot_bytes(void);
+int mlr_cpcp_snapshot(void* plan, void* host, void* stream);
+int mlr_cpcp_snapshot_read(const void* host, double* out32);
 int mlr_cpcp_history(void* plan, int count, double* out, double* objectives, void* stream); /* count x 8, count */
 /* Per-phase CUDA-event timing (8 slots: gram, power, dots, qp, -, update, finalize, -). */
 int mlr_cpcp_set_timing(void* plan, int enable);

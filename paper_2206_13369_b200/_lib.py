@@ -54,6 +54,9 @@ _SIGS = {
     "mlr_pcp_outputs": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
                                 c_void_p]),
     "mlr_pcp_state": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mlr_pcp_snapshot_bytes": (c_int64, []),
+    "mlr_pcp_snapshot": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mlr_pcp_snapshot_read": (c_int, [c_void_p, c_void_p, c_void_p]),
     "mlr_pcp_history": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "mlr_pcp_set_truncation": (c_int, [c_void_p, c_int, c_int]),
     "mlr_pcp_set_timing": (c_int, [c_void_p, c_int]),
@@ -74,6 +77,9 @@ _SIGS = {
     "mlr_cpcp_finalize": (c_int, [c_void_p, c_void_p, c_void_p]),
     "mlr_cpcp_outputs": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "mlr_cpcp_state": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mlr_cpcp_snapshot_bytes": (c_int64, []),
+    "mlr_cpcp_snapshot": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mlr_cpcp_snapshot_read": (c_int, [c_void_p, c_void_p]),
     "mlr_cpcp_history": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "mlr_cpcp_set_timing": (c_int, [c_void_p, c_int]),
     "mlr_cpcp_timing": (c_int, [c_void_p, c_void_p, c_void_p]),

@@ -8,6 +8,7 @@ stream; all arithmetic runs in libmlr_b200.so.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -21,6 +22,50 @@ def _ptr(t):
 
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _Snapshots:
+    """Double-buffered pinned host copies of a plan's device state, each
+    followed by an event: the host reads batch j's state while batch j + 1
+    is already queued, so the GPU never idles on a poll.  Instances are
+    pooled (pinned allocation is slow and can stall behind other host work),
+    so a solve allocates nothing on the host once warm."""
+
+    _pool: dict = {}
+    _lock = threading.Lock()
+
+    def __init__(self, nbytes):
+        self.nbytes = int(nbytes)
+        self.buf = [torch.empty(self.nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self.next = 0
+
+    @classmethod
+    def get(cls, nbytes):
+        with cls._lock:
+            free = cls._pool.get(int(nbytes))
+            if free:
+                snap = free.pop()
+                snap.next = 0
+                return snap
+        return cls(nbytes)
+
+    def release(self):
+        for e in self.ev:
+            e.synchronize()  # no copy into these buffers is still in flight
+        with self._lock:
+            self._pool.setdefault(self.nbytes, []).append(self)
+
+    def take(self, copy_fn):
+        i = self.next
+        self.next ^= 1
+        copy_fn(ctypes.c_void_p(self.buf[i].data_ptr()))
+        self.ev[i].record()
+        return i
+
+    def wait(self, i):
+        self.ev[i].synchronize()
+        return ctypes.c_void_p(self.buf[i].data_ptr())
 
 
 class CudaPcp:
@@ -50,6 +95,9 @@ class CudaPcp:
         self.lz_w = torch.zeros(self.n, dtype=torch.float64, device=self.device)
 
     def close(self):
+        if getattr(self, "_snaps", None) is not None:
+            self._snaps.release()
+            self._snaps = None
         if self.h is not None:
             self.lib.mlr_pcp_destroy(self.h)
             self.h = None
@@ -105,6 +153,10 @@ class CudaPcp:
     def state(self):
         out = np.zeros(16)
         _lib.check(self.lib.mlr_pcp_state(self.h, out.ctypes.data, _stream()))
+        return self._state_dict(out)
+
+    @staticmethod
+    def _state_dict(out):
         keys = ("k", "done", "status", "rank", "mu", "mu_final", "mu_last", "nuclear", "sigma1", "d_norm",
                 "jac_sweeps", "tau", "scale", "lam")
         d = dict(zip(keys, out[:len(keys)].tolist()))
@@ -116,6 +168,20 @@ class CudaPcp:
         out = np.zeros((max(count, 1), 8))
         _lib.check(self.lib.mlr_pcp_history(self.h, int(count), out.ctypes.data, _stream()))
         return out[:count]
+
+    def snapshot(self):
+        """Queue a copy of the device state; returns a token for read_snapshot."""
+        if getattr(self, "_snaps", None) is None:
+            self._snaps = _Snapshots.get(self.lib.mlr_pcp_snapshot_bytes())
+        return self._snaps.take(lambda p: _lib.check(self.lib.mlr_pcp_snapshot(self.h, p, _stream())))
+
+    def read_snapshot(self, token):
+        """(state dict as state(), lanczos dict as lanczos_state()) of a snapshot."""
+        p = self._snaps.wait(token)
+        out, lz = np.zeros(16), np.zeros(4)
+        _lib.check(self.lib.mlr_pcp_snapshot_read(p, out.ctypes.data, lz.ctypes.data))
+        return self._state_dict(out), {"k": int(lz[0]), "done": int(lz[1]), "sigma1": float(lz[2]),
+                                       "theta": float(lz[3])}
 
     def coarse_copy(self, out):
         """out (m_local x n_H) <- the latest coarse iterate L_H = Z."""
@@ -174,6 +240,9 @@ class CudaCpcp:
         self.mwork = torch.zeros(int(lib.mlr_matrix_stats_work_doubles()), dtype=torch.float64, device=self.device)
 
     def close(self):
+        if getattr(self, "_snaps", None) is not None:
+            self._snaps.release()
+            self._snaps = None
         if self.h is not None:
             self.lib.mlr_cpcp_destroy(self.h)
             self.h = None
@@ -215,9 +284,24 @@ class CudaCpcp:
     def outputs(self, L):
         _lib.check(self.lib.mlr_cpcp_outputs(self.h, _ptr(L), L.stride(0), _stream()))
 
+    def snapshot(self):
+        if getattr(self, "_snaps", None) is None:
+            self._snaps = _Snapshots.get(self.lib.mlr_cpcp_snapshot_bytes())
+        return self._snaps.take(lambda p: _lib.check(self.lib.mlr_cpcp_snapshot(self.h, p, _stream())))
+
+    def read_snapshot(self, token):
+        p = self._snaps.wait(token)
+        out = np.zeros(32)
+        _lib.check(self.lib.mlr_cpcp_snapshot_read(p, out.ctypes.data))
+        return self._state_dict(out)
+
     def state(self):
         out = np.zeros(32)
         _lib.check(self.lib.mlr_cpcp_state(self.h, out.ctypes.data, _stream()))
+        return self._state_dict(out)
+
+    @staticmethod
+    def _state_dict(out):
         keys = ("k", "done", "status", "t_l", "t_s", "u_l", "u_s", "sigma", "passes", "ga", "gb", "corner_l",
                 "corner_s", "i_s", "j_s", "s2", "pd_norm", "sq", "l1", "nnz", "ss", "sr", "r_is", "s_is", "spike",
                 "none", "coef")

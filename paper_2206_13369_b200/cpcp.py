@@ -78,6 +78,7 @@ def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every, probe=No
     comm.sum(be.red[:ns])
     comm.gather(be.amax_all, be.amax)
     be.begin()
+    pending = None
     while True:
         for _ in range(check_every):
             be.lmo()
@@ -93,9 +94,13 @@ def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every, probe=No
             comm.sum(be.red[:ns])
             comm.gather(be.amax_all, be.amax)
             be.finalize()
-        state = be.state()
-        if state["done"]:
-            break
+        # pipelined polling (see pcp.run_ialm)
+        token = be.snapshot()
+        if pending is not None:
+            state = be.read_snapshot(pending)
+            if state["done"]:
+                break
+        pending = token
     k = state["k"]
     L = be.empty(tuple(D.shape), D.dtype)
     be.outputs(L)

@@ -502,13 +502,41 @@ int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, 
                     int64_t ldo, void* stream) {
   return pcp_outputs(PLAN, D, ldd, Y_prev, ldy, L, S, ldo, STREAM);
 }
+static void pcp_state_values(const PcpDev& h, double* out16) {
+  double v[16] = {(double)h.k, (double)h.done, (double)h.status, (double)h.rank, h.mu, h.mu_final, h.mu_last,
+                  h.nuclear, h.sigma1, h.d_norm, (double)h.jac_sweeps, h.tau, h.scale, h.lam, 0.0, 0.0};
+  std::memcpy(out16, v, sizeof(v));
+}
 int mlr_pcp_state(void* plan, double* out16, void* stream) {
   PcpDev h;
   MLR_CUDA(cudaMemcpyAsync(&h, PLAN->dev, sizeof(PcpDev), cudaMemcpyDeviceToHost, STREAM));
   MLR_CUDA(cudaStreamSynchronize(STREAM));
-  double v[16] = {(double)h.k, (double)h.done, (double)h.status, (double)h.rank, h.mu, h.mu_final, h.mu_last,
-                  h.nuclear, h.sigma1, h.d_norm, (double)h.jac_sweeps, h.tau, h.scale, h.lam, 0.0, 0.0};
-  std::memcpy(out16, v, sizeof(v));
+  pcp_state_values(h, out16);
+  return kOk;
+}
+int64_t mlr_pcp_snapshot_bytes(void) { return (int64_t)(sizeof(PcpDev) + sizeof(LanczosDev)); }
+int mlr_pcp_snapshot(void* plan, void* host, void* stream) {
+  if (!host) {
+    set_error("mlr_pcp_snapshot: null buffer");
+    return kErrArg;
+  }
+  MLR_CUDA(cudaMemcpyAsync(host, PLAN->dev, sizeof(PcpDev), cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaMemcpyAsync((char*)host + sizeof(PcpDev), PLAN->lz, sizeof(LanczosDev), cudaMemcpyDeviceToHost,
+                           STREAM));
+  return kOk;
+}
+int mlr_pcp_snapshot_read(const void* host, double* out16, double* lz4) {
+  PcpDev h;
+  LanczosDev z;
+  std::memcpy(&h, host, sizeof(PcpDev));
+  std::memcpy(&z, (const char*)host + sizeof(PcpDev), sizeof(LanczosDev));
+  if (out16) pcp_state_values(h, out16);
+  if (lz4) {
+    lz4[0] = z.k;
+    lz4[1] = z.done;
+    lz4[2] = z.sigma1;
+    lz4[3] = z.theta;
+  }
   return kOk;
 }
 int mlr_pcp_set_truncation(void* plan, int sv0, int cap) {
@@ -592,15 +620,33 @@ int mlr_cpcp_update(void* plan, const void* D, int64_t ldd, const uint32_t* mask
 }
 int mlr_cpcp_finalize(void* plan, const double* red, void* stream) { return cpcp_finalize(PLAN, red, STREAM); }
 int mlr_cpcp_outputs(void* plan, void* L, int64_t ldl, void* stream) { return cpcp_outputs(PLAN, L, ldl, STREAM); }
-int mlr_cpcp_state(void* plan, double* out32, void* stream) {
-  CpcpDev h;
-  MLR_CUDA(cudaMemcpyAsync(&h, PLAN->dev, sizeof(CpcpDev), cudaMemcpyDeviceToHost, STREAM));
-  MLR_CUDA(cudaStreamSynchronize(STREAM));
+static void cpcp_state_values(const CpcpDev& h, double* out32) {
   double v[32] = {(double)h.k, (double)h.done, (double)h.status, h.t_l, h.t_s, h.u_l, h.u_s, h.sigma,
                   (double)h.passes, h.ga, h.gb, (double)h.corner_l, (double)h.corner_s, (double)h.i_s,
                   (double)h.j_s, h.s2, h.pd_norm, h.sq, h.l1, h.nnz, h.ss, h.sr, h.r_is, h.s_is, h.spike,
                   (double)h.none, h.coef, 0, 0, 0, 0, 0};
   std::memcpy(out32, v, sizeof(v));
+}
+int mlr_cpcp_state(void* plan, double* out32, void* stream) {
+  CpcpDev h;
+  MLR_CUDA(cudaMemcpyAsync(&h, PLAN->dev, sizeof(CpcpDev), cudaMemcpyDeviceToHost, STREAM));
+  MLR_CUDA(cudaStreamSynchronize(STREAM));
+  cpcp_state_values(h, out32);
+  return kOk;
+}
+int64_t mlr_cpcp_snapshot_bytes(void) { return (int64_t)sizeof(CpcpDev); }
+int mlr_cpcp_snapshot(void* plan, void* host, void* stream) {
+  if (!host) {
+    set_error("mlr_cpcp_snapshot: null buffer");
+    return kErrArg;
+  }
+  MLR_CUDA(cudaMemcpyAsync(host, PLAN->dev, sizeof(CpcpDev), cudaMemcpyDeviceToHost, STREAM));
+  return kOk;
+}
+int mlr_cpcp_snapshot_read(const void* host, double* out32) {
+  CpcpDev h;
+  std::memcpy(&h, host, sizeof(CpcpDev));
+  cpcp_state_values(h, out32);
   return kOk;
 }
 int mlr_cpcp_set_timing(void* plan, int enable) {

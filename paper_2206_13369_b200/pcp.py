@@ -62,15 +62,20 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
     lz_tol = LANCZOS_TOL if D.dtype == torch.float64 else 1e-11
     be.lanczos_init()
     steps = 0
+    # pipelined polling: batch j + 1 is queued before batch j's state is read
+    # (steps after convergence are no-ops on the device)
+    pending = None
     while True:
         for _ in range(4):
             w = be.lanczos_matvec(D)
             comm.sum(w)
             be.lanczos_update(w, lz_tol)
             steps += 1
-        if be.lanczos_state()["done"]:
+        token = be.snapshot()
+        if pending is not None and be.read_snapshot(pending)[1]["done"]:
             break
-        if steps > 2 * n + 16:
+        pending = token
+        if steps > 2 * n + 24:
             raise SvdError("Lanczos estimate of sigma_1(D) did not converge", iterations=steps)
     f32 = D.dtype == torch.float32
     Y = [be.empty(tuple(D.shape), D.dtype), be.empty(tuple(D.shape), D.dtype)]
@@ -80,6 +85,7 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
     be.gram(0)
     comm.sum(be.red[:nn])
     calls = 0
+    pending = None
     while True:
         for _ in range(check_every):
             be.svt()
@@ -92,9 +98,14 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
             be.gram(1)
             comm.sum(be.red[:ns])
             be.finalize()
-        st = be.state()
-        if st["done"]:
-            break
+        # pipelined polling: the next batch is queued before this one's state
+        # is read; once done, every further step is a no-op on the device
+        token = be.snapshot()
+        if pending is not None:
+            st = be.read_snapshot(pending)[0]
+            if st["done"]:
+                break
+        pending = token
     if st["done"] == 3:
         raise SvdError("coarse Jacobi eigensolver did not converge", iterations=-st["jac_sweeps"])
     k = st["k"]

@@ -36,6 +36,16 @@ class _Base:
     def empty(self, shape, dtype):
         return torch.zeros(shape, dtype=dtype)
 
+    # pipelined polling: the emulation is synchronous, so a snapshot is the
+    # state at the time it is taken
+    def snapshot(self):
+        if hasattr(self, "lanczos_state"):
+            return (self.state() if hasattr(self, "st") else None, self.lanczos_state())
+        return self.state()
+
+    def read_snapshot(self, token):
+        return token
+
     def close(self):
         pass
 
