@@ -89,6 +89,11 @@ int mlr_pcp_lanczos_init(void* plan, void* stream);
 int mlr_pcp_lanczos_matvec(void* plan, const void* D, int64_t ldd, double* w_part, void* stream);
 int mlr_pcp_lanczos_update(void* plan, const double* w_reduced, double tol, void* stream);
 int mlr_pcp_lanczos_state(void* plan, double* out4, void* stream); /* k, done, sigma1, theta */
+/* One rank: the whole Lanczos run (init state from mlr_pcp_lanczos_init) in one
+ * cooperative launch, same steps and stopping rule as the matvec/update loop;
+ * available when mlr_pcp_lanczos_run_available(plan) (n <= 4096). */
+int mlr_pcp_lanczos_run(void* plan, const void* D, int64_t ldd, double tol, void* stream);
+int mlr_pcp_lanczos_run_available(void* plan);
 int mlr_pcp_start(void* plan, const void* D, int64_t ldd, void* Y0, int64_t ldy, const double* in_stats, double lam,
                   double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
                   int jac_max_sweeps, void* stream);

@@ -45,6 +45,8 @@ _SIGS = {
     "mlr_pcp_lanczos_matvec": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "mlr_pcp_lanczos_update": (c_int, [c_void_p, c_void_p, c_double, c_void_p]),
     "mlr_pcp_lanczos_state": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "mlr_pcp_lanczos_run": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_void_p]),
+    "mlr_pcp_lanczos_run_available": (c_int, [c_void_p]),
     "mlr_pcp_start": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_double, c_double,
                               c_double, c_double, c_int, c_double, c_double, c_int, c_void_p]),
     "mlr_pcp_gram": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),

@@ -118,6 +118,12 @@ class CudaPcp:
     def lanczos_update(self, w, tol):
         _lib.check(self.lib.mlr_pcp_lanczos_update(self.h, _ptr(w), float(tol), _stream()))
 
+    def lanczos_run_available(self):
+        return bool(self.lib.mlr_pcp_lanczos_run_available(self.h))
+
+    def lanczos_run(self, D, tol):
+        _lib.check(self.lib.mlr_pcp_lanczos_run(self.h, _ptr(D), D.stride(0), float(tol), _stream()))
+
     def lanczos_state(self):
         out = np.zeros(4)
         _lib.check(self.lib.mlr_pcp_lanczos_state(self.h, out.ctypes.data, _stream()))

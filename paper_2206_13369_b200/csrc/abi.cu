@@ -122,7 +122,8 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.jac_result = c.take<int>(4 * 16);
   p.lzQ = c.take<double>(8 * (size_t)n * (p.lz_kmax + 1));
   p.lzT = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
-  p.lzW = c.take<double>(8 * (size_t)n * std::max(p.lz_splits, p.lz_fused_ctas));
+  p.lzW = c.take<double>(8 * (size_t)n * std::max(std::max(p.lz_splits, p.lz_fused_ctas), p.lz_run_ctas));
+  p.lzRed = c.take<double>(8 * (size_t)std::max(p.lz_run_ctas, 1) * (2 * ((size_t)p.lz_kmax + 1) + 4));
   p.lzWork = c.take<double>(8 * (size_t)n);
 }
 
@@ -156,6 +157,8 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
     const bool fused = ch.n <= 2048 && !(e && e[0] == '0');
     p.lz_fused_ctas = fused ? (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(m_local, 1), 8), sms))
                             : 0;
+    const char* r = getenv("MLR_LZ_RUN");
+    p.lz_run_ctas = (ch.n <= 4096 && m_local > 0 && !(r && r[0] == '0')) ? sms : 0;
   }
   p.lz_kmax = std::min(500, std::max(8, ch.n));
   p.jac_tol_host = 1e-14;
@@ -470,6 +473,10 @@ int mlr_pcp_lanczos_matvec(void* plan, const void* D, int64_t ldd, double* w_par
 int mlr_pcp_lanczos_update(void* plan, const double* w, double tol, void* stream) {
   return pcp_lanczos_update(PLAN, w, tol, STREAM);
 }
+int mlr_pcp_lanczos_run(void* plan, const void* D, int64_t ldd, double tol, void* stream) {
+  return pcp_lanczos_run(PLAN, D, ldd, tol, STREAM);
+}
+int mlr_pcp_lanczos_run_available(void* plan) { return lanczos_run_ok(PLAN); }
 int mlr_pcp_lanczos_state(void* plan, double* out4, void* stream) {
   LanczosDev h;
   MLR_CUDA(cudaMemcpyAsync(&h, PLAN->lz, sizeof(LanczosDev), cudaMemcpyDeviceToHost, STREAM));

@@ -546,6 +546,191 @@ __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double
   }
 }
 
+// The whole Lanczos run in one cooperative kernel (one CTA per SM, one rank,
+// n <= LZ_RUN_MAXN): per step
+//   t = D q_k (CTA b owns a contiguous row block; warp per row)      | sync
+//   CTA partial of D^T t (thread-owned columns, rows re-read from L2)  | sync
+//   w = sum of the partials over CTA b's column slice; alpha partials | sync
+//   w -= alpha q_k + beta q_{k-1}; reorthogonalisation (twice) with
+//   dot partials per slice, every CTA summing them in the same order   | 2 syncs
+//   beta; q_{k+1}; the Ritz value (multisection, every CTA alike)      | sync
+// so the host launches once instead of ~3 kernels per step plus polls.
+// Every reduction has a fixed order: bit-identical to rerunning it.
+constexpr int LZ_RUN_MAXN = 4096, LZ_RUN_T = 256;
+
+// Sum of G per-CTA partials base[g * stride] by one warp: lane l takes
+// g = l, l + 32, ... (loads in flight together), then a fixed shuffle tree.
+__device__ __forceinline__ double warp_gsum(const double* base, int64_t stride, int G, int lane) {
+  double v = 0.0;
+  for (int g = lane; g < G; g += 32) v += base[(int64_t)g * stride];
+  return warp_sum(v);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LZ_RUN_T, 1) lz_run_kernel(LanczosDev* lz, double* __restrict__ Q,
+                                                              const T* __restrict__ D, int64_t ldd, int64_t m,
+                                                              int n, double tol, double* __restrict__ tbuf,
+                                                              double* __restrict__ wpart, double* __restrict__ w,
+                                                              double* __restrict__ red) {
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = LZ_RUN_T / 32, MAXC = LZ_RUN_MAXN / LZ_RUN_T;
+  const int64_t r0 = m * b / G, r1 = m * (b + 1) / G;  // this CTA's rows
+  const int S = (n + G - 1) / G, j0 = min(n, b * S), j1 = min(n, j0 + S);  // this CTA's column slice
+  const int K0 = lz->kmax + 1;                                             // stride of the partial arrays
+  __shared__ double scratch[2 * 32];
+  __shared__ double bc[4];
+  extern __shared__ __align__(16) double lzr[];
+  double* ts = lzr;                   // t of this CTA's rows
+  double* hfull = ts + (r1 - r0);     // h (K0)
+  double* ta = hfull + K0;            // tridiagonal alpha
+  double* tb = ta + K0;               // beta
+  int k = lz->k;
+  int stable = lz->stable;
+  double theta = lz->theta, theta_prev = lz->theta_prev;
+  bool stop = lz->done != 0;
+  while (!stop) {
+    const double* qk = Q + (int64_t)k * n;
+    // ---- t = D q_k over this CTA's rows
+    for (int64_t i = r0 + wid; i < r1; i += NW) {
+      const T* row = D + i * ldd;
+      double s = 0.0;
+#pragma unroll 8
+      for (int j = lane; j < n; j += 32) s = fma((double)row[j], qk[j], s);
+      s = warp_sum(s);
+      if (lane == 0) ts[i - r0] = s;
+    }
+    __syncthreads();
+    // ---- CTA partial of D^T t: thread owns columns tid, tid + 256, ...
+    {
+      double acc[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
+      for (int64_t i = r0; i < r1; ++i) {
+        const T* row = D + i * ldd;
+        const double ti = ts[i - r0];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+          const int j = c * LZ_RUN_T + tid;
+          if (j < n) acc[c] = fma((double)row[j], ti, acc[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int j = c * LZ_RUN_T + tid;
+        if (j < n) wpart[(int64_t)b * n + j] = acc[c];
+      }
+    }
+    grid.sync();
+    // ---- w over this CTA's slice (warp per column sums the G partials); alpha partial
+    for (int j = j0 + wid; j < j1; j += NW) {
+      const double v = warp_gsum(wpart + j, n, G, lane);
+      if (lane == 0) w[j] = v;
+    }
+    __syncthreads();
+    double sa = 0.0;
+    for (int j = j0 + tid; j < j1; j += LZ_RUN_T) sa = fma(w[j], qk[j], sa);
+    {
+      double v2[2] = {sa, 0.0};
+      block_sum<2>(v2, scratch);
+      if (tid == 0) red[(int64_t)b * (2 * K0 + 4)] = v2[0];
+    }
+    grid.sync();
+    if (wid == 0) {
+      const double a = warp_gsum(red, 2 * K0 + 4, G, lane);
+      if (lane == 0) bc[0] = a;
+    }
+    __syncthreads();
+    const double alpha = bc[0];
+    const double bprev = k > 0 ? lz->beta[k - 1] : 0.0;
+    for (int j = j0 + tid; j < j1; j += LZ_RUN_T) {
+      double v = w[j] - alpha * qk[j];
+      if (k > 0) v -= bprev * Q[(int64_t)(k - 1) * n + j];
+      w[j] = v;
+    }
+    __syncthreads();
+    const int K = k + 1;
+    // ---- full reorthogonalisation, twice (classical Gram-Schmidt)
+    for (int pass = 0; pass < 2; ++pass) {
+      double* ph = red + (int64_t)b * (2 * K0 + 4) + 2 + pass * K0;
+      for (int c = wid; c < K; c += NW) {
+        const double* qc = Q + (int64_t)c * n;
+        double d = 0.0;
+        for (int j = j0 + lane; j < j1; j += 32) d = fma(qc[j], w[j], d);
+        d = warp_sum(d);
+        if (lane == 0) ph[c] = d;
+      }
+      grid.sync();
+      for (int c = wid; c < K; c += NW) {
+        const double h = warp_gsum(red + 2 + pass * K0 + c, 2 * K0 + 4, G, lane);
+        if (lane == 0) hfull[c] = h;
+      }
+      __syncthreads();
+      for (int j = j0 + tid; j < j1; j += LZ_RUN_T) {
+        double acc = 0.0;
+        for (int c = 0; c < K; ++c) acc = fma(hfull[c], Q[(int64_t)c * n + j], acc);
+        w[j] -= acc;
+      }
+      __syncthreads();
+    }
+    // ---- beta
+    double nn = 0.0;
+    for (int j = j0 + tid; j < j1; j += LZ_RUN_T) nn = fma(w[j], w[j], nn);
+    {
+      double v2[2] = {nn, 0.0};
+      block_sum<2>(v2, scratch);
+      if (tid == 0) red[(int64_t)b * (2 * K0 + 4) + 1] = v2[0];
+    }
+    grid.sync();
+    if (wid == 0) {
+      const double b2 = warp_gsum(red + 1, 2 * K0 + 4, G, lane);
+      if (lane == 0) bc[1] = sqrt(b2);
+    }
+    for (int c = tid; c < k; c += LZ_RUN_T) {
+      ta[c] = lz->alpha[c];
+      tb[c] = lz->beta[c];
+    }
+    __syncthreads();
+    const double beta = bc[1];
+    if (tid == 0) {
+      ta[k] = alpha;
+      tb[k] = beta;
+    }
+    __syncthreads();
+    // ---- Ritz value: same adaptive schedule as lz_update_cluster
+    const bool close = theta > 0.0 && fabs(theta - theta_prev) <= 1e-6 * theta;
+    const bool eval = close || (k % 4 == 3) || k + 1 >= lz->kmax || beta <= 1e-300;
+    const double th = eval ? tridiag_max_eig_block(ta, tb, K) : theta;
+    const double rel = theta > 0.0 ? fabs(th - theta) / th : 1.0;
+    stable = !eval ? stable : ((rel <= tol) ? stable + 1 : 0);
+    stop = (eval && stable >= 2 && k >= 3) || beta <= 1e-300 * fmax(th, 1e-300) || k + 1 >= lz->kmax;
+    if (!stop) {
+      double* qn = Q + (int64_t)(k + 1) * n;
+      const double inv = 1.0 / beta;
+      for (int j = j0 + tid; j < j1; j += LZ_RUN_T) qn[j] = w[j] * inv;
+    }
+    if (eval) {
+      theta_prev = theta;
+      theta = th;
+    }
+    grid.sync();  // q_{k+1} complete; every CTA has read lz->alpha/beta of earlier steps
+    if (b == 0 && tid == 0) {
+      lz->alpha[k] = alpha;
+      lz->beta[k] = beta;
+      lz->theta_prev = theta_prev;
+      lz->theta = theta;
+      lz->stable = stable;
+      if (stop) {
+        lz->done = 1;
+        lz->sigma1 = sqrt(fmax(th, 0.0));
+      }
+      lz->k = stop ? k : k + 1;
+    }
+    grid.sync();  // lz->alpha/beta visible before the next step reads them
+    if (!stop) ++k;
+  }
+}
+
 // ------------------------------------------------------------ scalars
 __global__ void pcp_start_scalars(PcpDev* st, const LanczosDev* lz, const double* __restrict__ in_stats,
                                   double lam, double mu0, double rho, double tol, int max_iters,
@@ -841,6 +1026,32 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
   const int rc = sum_slices(p->lzW, n, n, splits, wpart_out, st);
   p->timer.end(kPhLanczos, st);
   return rc;
+}
+
+int lanczos_run_ok(const PcpPlan* p) { return p->lz_run_ctas > 0; }
+
+int pcp_lanczos_run(PcpPlan* p, const void* D, int64_t ldd, double tol, cudaStream_t st) {
+  if (p->lz_run_ctas <= 0) {
+    set_error("pcp_lanczos_run: not available for this plan (n too large)");
+    return kErrArg;
+  }
+  const int n = p->ch.n;
+  int64_t m = p->m_local;
+  const int G = p->lz_run_ctas;
+  const int K0 = p->lz_kmax + 1;
+  const size_t smem = sizeof(double) * ((size_t)ceil_div(std::max<int64_t>(m, 1), G) + 3 * (size_t)K0 + 8);
+  void* args[] = {(void*)&p->lz, (void*)&p->lzQ, (void*)&D, (void*)&ldd, (void*)&m, (void*)&n, (void*)&tol,
+                  (void*)&p->lzT, (void*)&p->lzW, (void*)&p->lzWork, (void*)&p->lzRed};
+  p->timer.begin(st);
+  if (p->f32) {
+    MLR_CUDA(cudaFuncSetAttribute(lz_run_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLR_CUDA(cudaLaunchCooperativeKernel((void*)lz_run_kernel<float>, dim3(G), dim3(LZ_RUN_T), args, smem, st));
+  } else {
+    MLR_CUDA(cudaFuncSetAttribute(lz_run_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLR_CUDA(cudaLaunchCooperativeKernel((void*)lz_run_kernel<double>, dim3(G), dim3(LZ_RUN_T), args, smem, st));
+  }
+  p->timer.end(kPhLanczos, st);
+  return kOk;
 }
 
 int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStream_t st) {

@@ -46,6 +46,8 @@ struct PcpPlan {
   int row_blocks, gram_splits, lz_splits, lz_kmax;
   int lz_fused_ctas;  // > 0: one-pass D^T D q (n <= 2048)
   int coarse_ksplit;  // split-K of the n_p^3 coarse products (<= gram_splits)
+  int lz_run_ctas;    // > 0: the whole Lanczos run in one cooperative kernel (one rank, n <= 4096)
+  double* lzRed;      // lz_run_ctas x (2 (kmax + 1) + 4) dot partials
   double jac_tol_host;
   double jac_floor_rel;
   int jac_max_sweeps;
@@ -73,6 +75,8 @@ int matrix_stats(int64_t m, int n, bool f32, const void* D, int64_t ldd, double*
 int pcp_lanczos_init(PcpPlan* p, cudaStream_t st);
 int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out, cudaStream_t st);
 int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStream_t st);
+int pcp_lanczos_run(PcpPlan* p, const void* D, int64_t ldd, double tol, cudaStream_t st);
+int lanczos_run_ok(const PcpPlan* p);
 int pcp_start(PcpPlan* p, const void* D, int64_t ldd, void* Y0, int64_t ldy, const double* in_stats, double lam,
               double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
               cudaStream_t st);

@@ -62,10 +62,15 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
     lz_tol = LANCZOS_TOL if D.dtype == torch.float64 else 1e-11
     be.lanczos_init()
     steps = 0
-    # pipelined polling: batch j + 1 is queued before batch j's state is read
-    # (steps after convergence are no-ops on the device)
+    # one rank: the whole run is one cooperative kernel; otherwise batches of
+    # steps with the all-reduce in between and pipelined polling (batch j + 1
+    # is queued before batch j's state is read; steps after convergence are
+    # no-ops on the device)
+    run_whole = comm.world == 1 and getattr(be, "lanczos_run_available", lambda: False)()
+    if run_whole:
+        be.lanczos_run(D, lz_tol)
     pending = None
-    while True:
+    while not run_whole:
         for _ in range(4):
             w = be.lanczos_matvec(D)
             comm.sum(w)
