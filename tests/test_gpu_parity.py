@@ -245,6 +245,24 @@ def test_oracle_atoms_golden(golden, name):
     assert z.oracle_atoms is None  # P[D] = 0 early exit (cpcp.py:348-350)
 
 
+# ------------------------------------------------------------------ determinism
+def test_solves_are_bitwise_reproducible():
+    """Every reduction has a fixed order (no atomics in the arithmetic): two
+    solves of the same input agree bit for bit, PCP and CPCP."""
+    d, _ = O.gaussian_rpca(300, 256, 8, 0.1, 41)
+    d32 = d.astype(np.float32)
+    a = pkg.ml_ialm_solve(d32, pkg.PcpOptions(levels=32, tol_feasibility=1e-6))
+    b = pkg.ml_ialm_solve(d32, pkg.PcpOptions(levels=32, tol_feasibility=1e-6))
+    assert a.iter == b.iter and np.array_equal(a.l, b.l) and np.array_equal(a.s, b.s) and np.array_equal(a.y, b.y)
+    d2, mask = O.gaussian_rpca(400, 256, 6, 0.1, 42, observe=0.8)
+    lam = 1 / np.sqrt(400)
+    opts = pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / 20, tol=1e-6, max_iters=200, levels=32, collect_rank=False)
+    c = pkg.ml_fwt_solve(d2, pkg.ObservationMask(mask), opts)
+    e = pkg.ml_fwt_solve(d2, pkg.ObservationMask(mask), opts)
+    assert c.iter == e.iter and np.array_equal(c.l, e.l) and np.array_equal(c.s, e.s)
+    assert c.objective_history == e.objective_history
+
+
 # ------------------------------------------------------------------ frame stacks
 def _frame_files(g, tmp_path):
     blob, paths, o = g["files"].tobytes(), [], 0
