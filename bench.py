@@ -43,6 +43,39 @@ def _ncu_traffic():
         return {}
 
 
+def cpcp_secondary(dev, seed):
+    """Side measurements (not the headline metric): ML-CPCP C3 to tolerance and
+    C4 for 300 iterations, device-resident input, CUDA events, L2 flushed."""
+    import torch
+
+    import paper_2206_13369_b200 as pkg
+    from paper_2206_13369_b200.datasets import CONFIGS, make_config
+    out = {}
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for name, cap in (("C3", 5000), ("C4", 300)):
+        c = CONFIGS[name]
+        d, mask = make_config(name, seed)
+        m, n = d.shape
+        D = torch.from_numpy(d).to(dev)
+        om = pkg.ObservationMask(mask)
+        lam = 1.0 / np.sqrt(max(m, n))
+        mk = lambda it: pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=c["tol"], max_iters=it,
+                                        levels=c["n_coarse"], collect_rank=False)
+        pkg.ml_fwt_solve(D, om, mk(20))
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = pkg.ml_fwt_solve(D, om, mk(cap))
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        out[name] = {"workload": f"{name} ML-CPCP {m}x{n}, n_H={c['n_coarse']}, tol {c['tol']}, max_iters {cap}",
+                     "iterations": st.iter, "converged": st.converged, "solve_ms": ms,
+                     "iterations_per_s": st.iter / (ms / 1e3), "dtype": "f32"}
+        del D
+    return out
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -141,6 +174,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the ML-CPCP C3/C4 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -309,8 +343,12 @@ def main():
     # update), 11 fixed.  Calls and steps are issued in batches of 4 and the polling
     # is pipelined one batch deep, so one batch of each runs (as no-ops) past the end.
     calls = 4 * math.ceil((iters / args.steps) / 4) + 4
-    lz_issued = 4 * math.ceil(lz / 4) + 4
-    per_solve_launches = 20 * calls + 3 * lz_issued + 11
+    if world == 1 and n <= 4096:
+        lz_launches = 2  # init + the single cooperative Lanczos kernel
+    else:
+        lz_launches = 3 * (4 * math.ceil(lz / 4) + 4)
+    per_solve_launches = 20 * calls + lz_launches + 11
+    secondary = cpcp_secondary(dev, args.seed) if (world == 1 and not args.no_secondary) else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -328,6 +366,7 @@ def main():
         "dominant_phase": dominant,
         "time_to_tol_ms": total_ms / args.steps,
         "cpu_baseline": cpu,
+        "cpcp_configs": secondary,
         "gpu_launches": int(per_solve_launches * args.steps),
         "clocks": clk.summary(),
     }
