@@ -1191,6 +1191,38 @@ __global__ void __launch_bounds__(1024) svt_weights_trunc_kernel(PcpDev* __restr
   }
 }
 
+// Eigenvalues of the converged B~ in descending order (real coarse indices
+// only; the zero padding [nh, np) never mixes with them): the next
+// iteration's warm start then has blocks of similar eigenvalues, so fewer
+// block-Jacobi sweeps are needed.  perm[r] = index of the r-th largest.
+__global__ void __launch_bounds__(1024) eig_sort_kernel(const PcpDev* __restrict__ st, double* __restrict__ Bd,
+                                                        int np, int nh, int* __restrict__ perm) {
+  if (st->done) return;
+  extern __shared__ double dsort[];
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) dsort[i] = Bd[(int64_t)i * (np + 1)];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) {
+    const double di = dsort[i];
+    int r = 0;
+    for (int j = 0; j < nh; ++j) {
+      const double dj = dsort[j];
+      r += (dj > di || (dj == di && j < i)) ? 1 : 0;
+    }
+    perm[r] = i;
+    Bd[(int64_t)r * (np + 1)] = di;
+  }
+}
+
+__global__ void eig_permute_kernel(const PcpDev* __restrict__ st, const double* __restrict__ V,
+                                   double* __restrict__ Vout, int np, int nh, const int* __restrict__ perm) {
+  if (st->done) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)np * np;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / np), c = (int)(e % np);
+    Vout[e] = V[(int64_t)r * np + (c < nh ? perm[c] : c)];
+  }
+}
+
 // Coarse SVT from the (all-reduced) Gram in red: B = G^-1 K G^-1; Jacobi
 // on X = B V (warm start V); W~ = G^-1 V diag(f) V^T; Z = A W~.
 int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
@@ -1228,6 +1260,17 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   p->timer.begin(st);
   pcp_after_jacobi<<<1, 1, 0, st>>>(p->dev, p->jac_result);
   MLR_LAUNCH_CHECK("pcp_after_jacobi");
+  if (p->eig_sort) {
+    // sort the eigenpairs (warm start of the next iteration); fw is free until svt_weights
+    int* perm = reinterpret_cast<int*>(p->fw);
+    const int nh = p->ch.nh;
+    eig_sort_kernel<<<1, 1024, sizeof(double) * nh, st>>>(p->dev, p->Bm, np, nh, perm);
+    MLR_LAUNCH_CHECK("eig_sort_kernel");
+    eig_permute_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)np * np, 256), 1184), 256, 0, st>>>(
+        p->dev, p->Vm, p->T1, np, nh, perm);
+    MLR_LAUNCH_CHECK("eig_permute_kernel");
+    MLR_CUDA(cudaMemcpyAsync(p->Vm, p->T1, sizeof(double) * np * np, cudaMemcpyDeviceToDevice, st));
+  }
   // lambda_i = diag(B~) after convergence; f_i = (sigma_i - tau)+ / sigma_i
   if (p->trunc_sv0 > 0) {
     svt_weights_trunc_kernel<<<1, 1024, 0, st>>>(p->dev, np, p->ch.nh, p->Bm, p->sig, p->fw);

@@ -47,6 +47,7 @@ struct PcpPlan {
   int lz_fused_ctas;  // > 0: one-pass D^T D q (n <= 2048)
   int coarse_ksplit;  // split-K of the n_p^3 coarse products (<= gram_splits)
   int lz_run_ctas;    // > 0: the whole Lanczos run in one cooperative kernel (one rank, n <= 4096)
+  int eig_sort;       // sort the eigenpairs after each Jacobi (warm start of the next)
   double* lzRed;      // lz_run_ctas x (2 (kmax + 1) + 4) dot partials
   double jac_tol_host;
   double jac_floor_rel;
