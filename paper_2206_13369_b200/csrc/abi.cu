@@ -185,6 +185,10 @@ static void carve_cpcp(CpcpPlan& p, Carver& c) {
   p.gram_part = c.take<double>(8 * (p.fine ? 1 : nn * p.gram_splits));
   p.row_part = c.take<double>(8 * 9 * (size_t)p.row_blocks);
   p.dots_part = c.take<double>(8 * 3 * (size_t)p.row_blocks);
+  if (p.coarse_dots) {
+    p.mgd = c.take<void>(tb * (size_t)std::max<int64_t>(p.m_local, 1) * np);
+    p.mgo = c.take<void>(tb * (size_t)std::max<int64_t>(p.m_local, 1) * np);
+  }
   if (p.fine) {
     p.ft = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
     p.fz = c.take<double>(8 * np);
@@ -215,6 +219,8 @@ static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_
   const char* e = getenv("MLR_CPCP_FINE");
   p.fine = ch.nh == ch.n && world == 1 && !(e && e[0] == '0');
   p.fine_ctas = sms;
+  const char* cd = getenv("MLR_CPCP_COARSE_DOTS");
+  p.coarse_dots = !(cd && cd[0] == '0');
 }
 
 }  // namespace mlr

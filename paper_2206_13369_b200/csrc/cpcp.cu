@@ -529,6 +529,104 @@ __global__ void cp_lmo_scalars(CpcpDev* st, const double* __restrict__ am_all, i
   st->spike = st->corner_s ? -st->u_s * (b.val > 0.0 ? 1.0 : (b.val < 0.0 ? -1.0 : 0.0)) : 0.0;
 }
 
+// Masked chain Gram per row, once per solve: M_i = sum_j mask_ij R_j^T R_j is
+// tridiagonal (R_j has two adjacent taps), so the segment-QP quadratic form
+// aa = sum_ij mask_ij (E_i R_j^T)^2 = sum_i E_i M_i E_i^T needs no fine pass.
+//   mgd[i][k] = sum_{j in [lo_k, hi_k)} mask_ij (weight of j on k)^2
+//   mgo[i][k] = sum_{j : c0_j = k} mask_ij w0_j w1_j
+template <typename T>
+__global__ void __launch_bounds__(256) cp_maskgram_kernel(ChainDev ch, int64_t m, const uint32_t* __restrict__ mask,
+                                                          int64_t ldm, T* __restrict__ mgd, T* __restrict__ mgo) {
+  const int np = ch.np, nh = ch.nh;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * np; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / np;
+    const int k = (int)(e % np);
+    double d = 0.0, o = 0.0;
+    if (k < nh) {
+      const uint32_t* mrow = mask + i * ldm;
+      for (int j = ch.lo[k]; j < ch.hi[k]; ++j) {
+        if (!((__ldg(mrow + (j >> 5)) >> (j & 31)) & 1u)) continue;
+        const bool own = ch.c0[j] == k;
+        const double w = own ? ch.w0[j] : ch.w1[j];
+        d = fma(w, w, d);
+        if (own) o = fma(ch.w0[j], ch.w1[j], o);
+      }
+    }
+    mgd[e] = (T)d;
+    mgo[e] = (T)o;
+  }
+}
+
+// Segment-QP dots from coarse data only (warp per row):
+//   u_i = g_H[i] . vin / sqrt(s2), E_i = coef u_i v - L_H[i]
+//   aa += E_i M_i E_i^T (M_i from cp_maskgram_kernel, or G_R when fully observed)
+//   ab += -E_i . s~_i (+ spike * a_{i_s j_s}),  ar += E_i . g_H[i]
+template <typename T>
+__global__ void __launch_bounds__(256)
+cp_dots_coarse_kernel(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row0, const T* __restrict__ LH,
+                      const T* __restrict__ GH, const T* __restrict__ SH, const T* __restrict__ mgd,
+                      const T* __restrict__ mgo, const double* __restrict__ v, const double* __restrict__ vin,
+                      double* __restrict__ u, double* __restrict__ part) {
+  if (st->done) return;
+  __shared__ double scratch[3 * 32];
+  const int nh = ch.nh, np = ch.np;
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int64_t wglob = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+  const int64_t wstride = (int64_t)gridDim.x * warps;
+  const double coef = st->coef;
+  const double rs2 = st->none ? 0.0 : 1.0 / sqrt(st->s2);
+  const bool spike_on = st->corner_s;
+  const long long i_s = st->i_s;
+  const int j_s = st->j_s;
+  const double spike = st->spike;
+  double aa = 0.0, ab = 0.0, ar = 0.0;
+  for (int64_t i = wglob; i < m; i += wstride) {
+    const T* g = GH + i * np;
+    const T* lh = LH + i * np;
+    const T* sh = SH + i * np;
+    double d = 0.0;
+    for (int k = lane; k < nh; k += 32) d = fma((double)g[k], vin[k], d);
+    d = warp_sum(d);
+    const double ui = st->none ? 0.0 : d * rs2;
+    if (lane == 0) u[i] = ui;
+    const double cu = coef * ui;
+    double e_ab = 0.0, e_ar = 0.0, e_aa = 0.0;
+    for (int k = lane; k < nh; k += 32) {
+      const double e = cu * v[k] - (double)lh[k];
+      const double e1 = k + 1 < nh ? cu * v[k + 1] - (double)lh[k + 1] : 0.0;
+      double dk, ok;
+      if (mgd) {
+        dk = (double)mgd[i * np + k];
+        ok = (double)mgo[i * np + k];
+      } else {  // fully observed: M_i = G_R = L D L^T (tridiagonal)
+        dk = ch.gd[k] + (k > 0 ? ch.gl[k - 1] * ch.gl[k - 1] * ch.gd[k - 1] : 0.0);
+        ok = k + 1 < nh ? ch.gl[k] * ch.gd[k] : 0.0;
+      }
+      e_aa = fma(e * dk, e, e_aa);
+      e_aa = fma(2.0 * e * ok, e1, e_aa);
+      e_ab = fma(e, (double)sh[k], e_ab);
+      e_ar = fma(e, (double)g[k], e_ar);
+    }
+    ab -= e_ab;
+    ar += e_ar;
+    aa += e_aa;
+    if (spike_on && (row0 + i) == i_s && lane == 0) {
+      const int c = ch.c0[j_s];
+      const double ec = cu * v[c] - (double)lh[c];
+      const double ec1 = c + 1 < nh ? cu * v[c + 1] - (double)lh[c + 1] : 0.0;
+      ab += spike * (ec * ch.w0[j_s] + ec1 * ch.w1[j_s]);
+    }
+  }
+  double vals[3] = {aa, ab, ar};
+  block_sum<3>(vals, scratch);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x + 0] = vals[0];
+    part[3 * blockIdx.x + 1] = vals[1];
+    part[3 * blockIdx.x + 2] = vals[2];
+  }
+}
+
 // Per-row coarse evaluation of the segment-QP dots (warp per row):
 //   u_i  = g_H[i] . vin / sqrt(s2)           (left vector of the triple)
 //   E_i  = coef * u_i * v - L_H[i]          (a = P[E R^T])
@@ -805,6 +903,15 @@ int cpcp_start(CpcpPlan* p, const void* D, int64_t ldd, const uint32_t* mask, in
   MLR_LAUNCH_CHECK("cp_start_scalars");
   const int np = p->ch.np;
   MLR_CUDA(cudaMemsetAsync(p->hist, 0, sizeof(double) * kCpHistCols * p->max_iters, st));
+  if (p->m_local > 0 && p->coarse_dots && mask) {
+    const int blocks = (int)std::min<int64_t>(ceil_div(p->m_local * np, 256), 148 * 16);
+    if (p->f32)
+      cp_maskgram_kernel<float><<<blocks, 256, 0, st>>>(p->ch, p->m_local, mask, ldm, (float*)p->mgd, (float*)p->mgo);
+    else
+      cp_maskgram_kernel<double><<<blocks, 256, 0, st>>>(p->ch, p->m_local, mask, ldm, (double*)p->mgd,
+                                                         (double*)p->mgo);
+    MLR_LAUNCH_CHECK("cp_maskgram_kernel");
+  }
   if (p->m_local > 0) {
     MLR_CUDA(cudaMemsetAsync(p->LH, 0, tb * p->m_local * np, st));
     MLR_CUDA(cudaMemsetAsync(p->SH, 0, tb * p->m_local * np, st));
@@ -901,7 +1008,24 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   MLR_LAUNCH_CHECK("cp_lmo_scalars");
   p->timer.end(1, st);
   p->timer.begin(st);
-  if (p->m_local > 0 && (size_t)p->ch.np * 16 + 8 * (size_t)(p->ch.np + 2) * 8 <= 200 * 1024) {
+  if (p->m_local > 0 && p->coarse_dots) {
+    const int blocks = p->row_blocks;
+    const void* mgd = p->mask_dev ? p->mgd : nullptr;
+    const void* mgo = p->mask_dev ? p->mgo : nullptr;
+    if (p->f32)
+      cp_dots_coarse_kernel<float><<<blocks, 256, 0, st>>>(p->dev, p->ch, p->m_local, p->row0, (const float*)p->LH,
+                                                           (const float*)p->GH, (const float*)p->SH,
+                                                           (const float*)mgd, (const float*)mgo, p->v, p->vin, p->u,
+                                                           p->dots_part);
+    else
+      cp_dots_coarse_kernel<double><<<blocks, 256, 0, st>>>(p->dev, p->ch, p->m_local, p->row0,
+                                                            (const double*)p->LH, (const double*)p->GH,
+                                                            (const double*)p->SH, (const double*)mgd,
+                                                            (const double*)mgo, p->v, p->vin, p->u, p->dots_part);
+    MLR_LAUNCH_CHECK("cp_dots_coarse_kernel");
+    cp_dots_reduce<<<1, 256, 0, st>>>(p->dots_part, blocks, dots, p->dev);
+    MLR_LAUNCH_CHECK("cp_dots_reduce");
+  } else if (p->m_local > 0 && (size_t)p->ch.np * 16 + 8 * (size_t)(p->ch.np + 2) * 8 <= 200 * 1024) {
     const int rc = cp_dots_rows(p, st);
     if (rc) return rc;
     cp_dots_reduce<<<1, 256, 0, st>>>(p->dots_part, p->row_blocks, dots, p->dev);

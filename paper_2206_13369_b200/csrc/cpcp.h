@@ -44,6 +44,10 @@ struct CpcpPlan {
   double* dots_part; // row_blocks x 3
   const uint32_t* mask_dev;  // bound at start (may be null: fully observed)
   int64_t ldm_dev;
+  // segment-QP dots from coarse data (masked chain Gram per row, once per solve)
+  bool coarse_dots;
+  void* mgd;         // m_local x np (T): diagonal of M_i
+  void* mgo;         // m_local x np (T): super-diagonal of M_i
   // full-width solve (identity chain, one rank): the LMO's power passes run as
   // matvecs on g_H = r instead of on the n x n Gram, which is never formed
   bool fine;
