@@ -159,6 +159,8 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
                             : 0;
     const char* r = getenv("MLR_LZ_RUN");
     p.lz_run_ctas = (ch.n <= 4096 && m_local > 0 && !(r && r[0] == '0')) ? sms : 0;
+    const char* rc = getenv("MLR_LZ_RUN_CTAS");
+    if (p.lz_run_ctas && rc) p.lz_run_ctas = std::max(1, std::min(sms, atoi(rc)));
   }
   p.lz_kmax = std::min(500, std::max(8, ch.n));
   {
