@@ -34,27 +34,28 @@ class _Snapshots:
     _pool: dict = {}
     _lock = threading.Lock()
 
-    def __init__(self, nbytes):
-        self.nbytes = int(nbytes)
-        self.buf = [torch.empty(self.nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    def __init__(self, nbytes, device_index):
+        self.key = (int(nbytes), int(device_index))  # events belong to one device
+        self.buf = [torch.empty(int(nbytes), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         self.ev = [torch.cuda.Event(), torch.cuda.Event()]
         self.next = 0
 
     @classmethod
     def get(cls, nbytes):
+        key = (int(nbytes), torch.cuda.current_device())
         with cls._lock:
-            free = cls._pool.get(int(nbytes))
+            free = cls._pool.get(key)
             if free:
                 snap = free.pop()
                 snap.next = 0
                 return snap
-        return cls(nbytes)
+        return cls(*key)
 
     def release(self):
         for e in self.ev:
             e.synchronize()  # no copy into these buffers is still in flight
         with self._lock:
-            self._pool.setdefault(self.nbytes, []).append(self)
+            self._pool.setdefault(self.key, []).append(self)
 
     def take(self, copy_fn):
         i = self.next
