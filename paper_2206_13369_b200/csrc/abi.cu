@@ -324,6 +324,13 @@ int mlr_chain_create(int n, int nh, const int32_t* c0, const double* w0, const d
       }
       if (reg) d.reg_lgp = lg;
     }
+    // FP32 stencil weights of column j >= 128 equal those of 128 + j % 128
+    d.reg_periodic = 0;
+    if (d.reg_lgp > 0) {
+      bool per = true;
+      for (int j = 256; j < n && per; ++j) per = w0f[j] == w0f[128 + j % 128] && w1f[j] == w1f[128 + j % 128];
+      d.reg_periodic = per ? 1 : 0;
+    }
   }
   auto up = [&](void** dst, const void* src, size_t bytes) -> int {
     void* p = nullptr;

@@ -54,6 +54,7 @@ struct ChainDev {
   int keys_dense;       // c0 starts at 0, steps by <= 1 and reaches nh-2 (segmented restriction valid)
   int max_run;          // longest run of equal c0
   int reg_lgp;          // > 0: regular chain, c0[j] = max(0, (j+1)/P - 1) with P = 2^reg_lgp, n = n_H * P
+  int reg_periodic;     // FP32 weights repeat with period 128 after the first 128 columns (rows.cu fast path)
 };
 
 int ldl_solve(const int* skip, const ChainDev& ch, const double* in, double* out, int trans_in,

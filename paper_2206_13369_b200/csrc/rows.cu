@@ -18,7 +18,11 @@
 //   cp_rows_warp<T, MODE>  : ML-CPCP init / update / output passes
 //                            (cpcp.py:352-354, 399-427)
 //   cp_dots_warp<T>        : ML-CPCP segment-QP dots from coarse data (cpcp.py:387-395)
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
+#include <initializer_list>
+#include <type_traits>
 
 #include "common.cuh"
 #include "cpcp.h"
@@ -582,6 +586,216 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
   }
 }
 
+// ------------------------------------------------- FP32 regular-chain fast path
+// The update passes of both solvers specialised for what every BASELINE
+// config has: FP32, a regular chain with P = 2^LGP fine columns per coarse
+// column (compile-time, so the lane-group butterflies unroll), n % 4 == 0,
+// 16-byte aligned rows.  Same per-element arithmetic (and so the same
+// results) as the general kernels; what goes is the per-chunk overhead the
+// general ones pay: bounds checks and stencil loads on interior chunks (the
+// weights are periodic after chunk 0 and sit in registers), 64-bit index
+// arithmetic in the prefetch ring, runtime-bounded shuffle loops, a branchy
+// arg-max.  The last, partial chunk of a row takes the checked path.  The
+// next row's coarse row (Z, or L_H for ML-CPCP) rides in the prefetch ring
+// when a row has at least RING_ST chunks and the double buffer fits (ZPF).
+// Grid = the resident CTAs (one wave); unused partial-result slots up to the
+// plan's row_blocks are written empty.
+constexpr int FAST_CH = 128;  // 32 lanes x float4
+
+// lane-strided cp.async of one coarse row (np floats, np % 4 == 0) into smem
+__device__ __forceinline__ void copy_coarse_row(float* dst, const float* src, int np, int lane) {
+  for (int k = lane * 4; k < np; k += 128) cp_async16(dst + k, src + k, 16);
+}
+
+template <int LGP, bool ZPF>
+__global__ void __launch_bounds__(RW_THREADS, 3)
+pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* __restrict__ D, int64_t ldd,
+                const float* __restrict__ Yin, float* __restrict__ Yout, int64_t ldy, const float* __restrict__ Z,
+                float* __restrict__ A, double* __restrict__ part, int part_slots) {
+  if (st->done) return;
+  constexpr int NV = 4, CH = FAST_CH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = ch.n, np = ch.np;
+  const int zlen = round_up_dev(np + 2, 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem_raw + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + RING_BYTES);
+  float* zbuf = reinterpret_cast<float*>(wbase);
+  const LaneRing ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
+  if (blockIdx.x == 0)
+    for (int b = gridDim.x + threadIdx.x; b < part_slots; b += blockDim.x)
+      part[3 * b] = part[3 * b + 1] = part[3 * b + 2] = 0.0;
+
+  const double mu_d = st->mu;
+  const float inv = (float)(1.0 / mu_d);
+  const float mu = (float)mu_d;
+  const float thr = (float)(st->lam * (1.0 / mu_d));
+  const float inv_next = (float)(1.0 / (mu_d * st->rho));
+  double acc_res = 0.0, acc_l1 = 0.0, acc_nnz = 0.0;
+  const float* __restrict__ w0p = ch.w0f;
+  const float* __restrict__ w1p = ch.w1f;
+  float cw0[NV], cw1[NV], rw0[NV], rw1[NV];
+#pragma unroll
+  for (int e = 0; e < NV; ++e) {
+    const int j0 = lane * NV + e, j1 = CH + lane * NV + e;
+    cw0[e] = j0 < n ? __ldg(w0p + j0) : 0.f;
+    cw1[e] = j0 < n ? __ldg(w1p + j0) : 0.f;
+    rw0[e] = j1 < n ? __ldg(w0p + j1) : 0.f;
+    rw1[e] = j1 < n ? __ldg(w1p + j1) : 0.f;
+  }
+  const int nfull = n / CH, nc = (n + CH - 1) / CH;
+  const int first = blockIdx.x * RW_WARPS + warp, stride = gridDim.x * RW_WARPS;
+  int irow = first, ic = 0, isl = 0;
+  const float* dnext = D + (int64_t)first * ldd;
+  const float* ynext = Yin + (int64_t)first * ldy;
+  auto issue = [&]() {
+    if (irow < m) {
+      const int jq = ic * CH + lane * NV;
+      const bool in = jq < n;
+      cp_async16(ring.slot(isl, 0, lane), dnext + (in ? jq : 0), in ? 16 : 0);
+      cp_async16(ring.slot(isl, 1, lane), ynext + (in ? jq : 0), in ? 16 : 0);
+    }
+    cp_commit();
+    isl = (isl + 1) & (RING_ST - 1);
+    if (++ic == nc) {
+      ic = 0;
+      irow += stride;
+      dnext += (int64_t)stride * ldd;
+      ynext += (int64_t)stride * ldy;
+    }
+  };
+  if (ZPF && first < m) copy_coarse_row(zbuf, Z + (int64_t)first * np, np, lane);
+#pragma unroll
+  for (int q = 0; q < RING_ST - 1; ++q) issue();
+  int csl = 0, zb = 0;
+  RegRestrict<float, 1, NV> rr;
+
+  for (int i = first; i < m; i += stride) {
+    float* zrow = zbuf + (ZPF ? zb * zlen : 0);
+    if (ZPF) {
+      // this row's Z went out with the ring group of the previous row's chunk 0
+      // (>= RING_ST groups ago) or, for the first row, with the first group
+      cp_wait<RING_ST - 2>();
+      __syncwarp();
+      if (lane < zlen - np) zrow[np + lane] = 0.f;
+      if (i + stride < m) copy_coarse_row(zbuf + (zb ^ 1) * zlen, Z + (int64_t)(i + stride) * np, np, lane);
+      zb ^= 1;
+    } else {
+      for (int k = lane; k < zlen; k += 32) zrow[k] = k < np ? Z[(int64_t)i * np + k] : 0.f;
+    }
+    __syncwarp();
+    float* yrow = Yout + (int64_t)i * ldy;
+    rr.begin();
+    float* const outp[1] = {A + (int64_t)i * np};
+
+    auto chunk = [&](int c, const float(&w0)[NV], const float(&w1)[NV], auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      const int cbase = c * CH;
+      const int j = cbase + lane * NV;
+      issue();
+      cp_wait<RING_ST - 1>();
+      const int sl = csl;
+      csl = (csl + 1) & (RING_ST - 1);
+      float dv[NV], yv[NV];
+      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 0, lane)), dv);
+      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 1, lane)), yv);
+      int k0 = max(0, (j >> LGP) - 1), k3 = max(0, ((j + 4) >> LGP) - 1);
+      if (!FULL) {
+        k0 = min(k0, zlen - 2);
+        k3 = min(k3, zlen - 2);
+      }
+      const float z0 = zrow[k0], z1 = zrow[k0 + 1], z3a = zrow[k3], z3b = zrow[k3 + 1];
+      float x[1][NV], yo[NV];
+      float c_res = 0.f, c_l1 = 0.f;
+      int c_nnz = 0;
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const float za = e < 3 ? z0 : z3a, zb_ = e < 3 ? z1 : z3b;
+        const float l = w0[e] * za + w1[e] * zb_;
+        const float d = dv[e], y = yv[e];
+        const float w = y * inv + d - l;
+        const float s = soft_thr<float>(w, thr);
+        const float res = (d - l) - s;  // zero past n (d = l = s = 0 there)
+        const float ynew = y + res * mu;
+        yo[e] = ynew;
+        c_res = fmaf(res, res, c_res);
+        c_l1 += fabsf(s);
+        c_nnz += s != 0.f ? 1 : 0;
+        x[0][e] = ynew * inv_next + d - s;
+      }
+      acc_res += (double)c_res;
+      acc_l1 += (double)c_l1;
+      acc_nnz += (double)c_nnz;
+      if (FULL || j < n) *reinterpret_cast<float4*>(yrow + j) = Vec<float>::pack(yo);
+      rr.chunk(w0, w1, x, cbase, outp, lane, LGP);
+    };
+    if (nfull > 0) {
+      chunk(0, cw0, cw1, std::true_type{});
+      for (int c = 1; c < nfull; ++c) chunk(c, rw0, rw1, std::true_type{});
+    }
+    if (nfull < nc) {
+      float t0[NV], t1[NV];
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const bool in = nfull * CH + lane * NV + e < n;
+        t0[e] = in ? (nfull == 0 ? cw0[e] : rw0[e]) : 0.f;
+        t1[e] = in ? (nfull == 0 ? cw1[e] : rw1[e]) : 0.f;
+      }
+      chunk(nfull, t0, t1, std::false_type{});
+    }
+    rr.finish(outp, n, np, lane, LGP);
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __shared__ double scratch[3 * 32];
+  double v[3] = {acc_res, acc_l1, acc_nnz};
+  block_sum<3>(v, scratch);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x + 0] = v[0];
+    part[3 * blockIdx.x + 1] = v[1];
+    part[3 * blockIdx.x + 2] = v[2];
+  }
+}
+
+// fast path applicability (both solvers): FP32, regular chain with 4 <= P <= 32,
+// periodic weights after chunk 0, n % 4 == 0, 16-byte aligned leading dimensions
+static bool fast_ok(const ChainDev& ch, bool f32, std::initializer_list<int64_t> lds) {
+  if (!f32 || ch.reg_lgp < 2 || ch.reg_lgp > 5 || !ch.reg_periodic || ch.n % 4 != 0 || ch.np % 4 != 0) return false;
+  for (int64_t l : lds)
+    if (l % 4 != 0) return false;
+  const char* env = getenv("MLR_FAST_ROWS");
+  return !(env && env[0] == '0');
+}
+
+template <typename K>
+static int fast_grid(K kern, size_t smem, int want) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, RW_THREADS, smem);
+  return std::max(1, std::min(want, sms * std::max(per, 1)));
+}
+
+// double-buffer the coarse row when a row has >= RING_ST chunks and 3 CTAs still fit
+static bool fast_zpf(const ChainDev& ch, size_t fixed) {
+  const size_t zl = (size_t)round_up(ch.np + 2, 4) * 4;
+  return (ch.n + FAST_CH - 1) / FAST_CH >= RING_ST && fixed + RW_WARPS * (2 * zl + RING_BYTES) <= 74 * 1024;
+}
+
+template <int LGP>
+static int pcp_fast_launch(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy,
+                           cudaStream_t st) {
+  const bool zpf = fast_zpf(p->ch, 0);
+  const size_t smem = RW_WARPS * ((zpf ? 2 : 1) * (size_t)round_up(p->ch.np + 2, 4) * 4 + RING_BYTES);
+  auto kern = zpf ? pcp_update_fast<LGP, true> : pcp_update_fast<LGP, false>;
+  MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = fast_grid(kern, smem, p->row_blocks);
+  kern<<<grid, RW_THREADS, smem, st>>>(p->dev, p->ch, (int)p->m_local, (const float*)D, ldd, (const float*)Yin,
+                                       (float*)Yout, ldy, (const float*)p->Z, (float*)p->A, p->row_part,
+                                       p->row_blocks);
+  MLR_LAUNCH_CHECK("pcp_update_fast");
+  return kOk;
+}
+
 bool rows_warp_ok(const ChainDev& ch, bool) { return ch.keys_dense != 0; }
 // regular chains whose groups are whole lanes and fit a chunk
 static bool rows_reg_ok(const ChainDev& ch, bool f32) {
@@ -593,6 +807,14 @@ int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, 
              void* Sout, int64_t ldo, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
   const bool reg = rows_reg_ok(p->ch, p->f32);
+  if (mode == kWUpdate && fast_ok(p->ch, p->f32, {ldd, ldy}) && p->m_local < INT_MAX) {
+    switch (p->ch.reg_lgp) {
+      case 2: return pcp_fast_launch<2>(p, D, ldd, Yin, Yout, ldy, st);
+      case 3: return pcp_fast_launch<3>(p, D, ldd, Yin, Yout, ldy, st);
+      case 4: return pcp_fast_launch<4>(p, D, ldd, Yin, Yout, ldy, st);
+      default: return pcp_fast_launch<5>(p, D, ldd, Yin, Yout, ldy, st);
+    }
+  }
   const size_t stage = reg ? 0 : (p->f32 ? SegRestrict<float, 1, 4>::STAGE_BYTES : SegRestrict<double, 1, 2>::STAGE_BYTES);
   // the cp.async ring only while 3 CTAs per SM still fit (occupancy first)
   const size_t base = RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
@@ -867,10 +1089,256 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
   }
 }
 
+// ML-CPCP update pass, FP32 regular-chain fast path (see pcp_update_fast)
+template <int LGP, bool ZPF>
+__global__ void __launch_bounds__(RW_THREADS, 3)
+cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0, int64_t m_global,
+               const float* __restrict__ D, int64_t ldd, const uint32_t* __restrict__ mask, int64_t ldm,
+               float* __restrict__ S, int64_t lds, float* __restrict__ LH, float* __restrict__ GH,
+               float* __restrict__ SH, const double* __restrict__ u, const double* __restrict__ vg,
+               double* __restrict__ part, int part_slots) {
+  if (st->done) return;
+  constexpr int NV = 4, CH = FAST_CH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = ch.n, nh = ch.nh, np = ch.np;
+  const int zlen = round_up_dev(np + 2, 4);
+  double* vs = reinterpret_cast<double*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + RING_BYTES);
+  float* lbuf = reinterpret_cast<float*>(wbase);
+  const LaneRing ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
+  for (int k = threadIdx.x; k < np; k += blockDim.x) vs[k] = vg[k];
+  if (blockIdx.x == 0)  // empty partial-result slots past the grid
+    for (int b = gridDim.x + threadIdx.x; b < part_slots; b += blockDim.x) {
+      double* o = part + 9 * b;
+      for (int q = 0; q < 8; ++q) o[q] = 0.0;
+      o[8] = -1.0;
+    }
+  __syncthreads();
+
+  const double ga = st->ga, gb = st->gb, coef = st->coef;
+  const float one_ga = (float)(1.0 - ga), one_gb = (float)(1.0 - gb);
+  const float lam_s = (float)st->lam_s;
+  const bool spike_on = st->corner_s;
+  const long long i_s = st->i_s;
+  const int j_s = st->j_s;
+  const float spike_add = (float)(gb * st->spike);
+  const float* __restrict__ w0p = ch.w0f;
+  const float* __restrict__ w1p = ch.w1f;
+  // stencil weights: chunk 0 (the first coarse group differs) and the
+  // periodic interior chunks, held for the whole kernel
+  float cw0[NV], cw1[NV], rw0[NV], rw1[NV];
+#pragma unroll
+  for (int e = 0; e < NV; ++e) {
+    const int j0 = lane * NV + e, j1 = CH + lane * NV + e;
+    cw0[e] = j0 < n ? __ldg(w0p + j0) : 0.f;
+    cw1[e] = j0 < n ? __ldg(w1p + j0) : 0.f;
+    rw0[e] = j1 < n ? __ldg(w0p + j1) : 0.f;
+    rw1[e] = j1 < n ? __ldg(w1p + j1) : 0.f;
+  }
+  double a_sq = 0.0, a_l1 = 0.0, a_nnz = 0.0, a_ss = 0.0, a_sr = 0.0;
+  float bm = -1.f, bval = 0.f, bsv = 0.f;
+  int bj = INT_MAX, brow = -1;
+  const int nfull = n / CH;
+  const int nc = (n + CH - 1) / CH;
+  const int first = blockIdx.x * RW_WARPS + warp, stride = gridDim.x * RW_WARPS;
+  struct {
+    int irow, ic, isl;
+  } cur{first, 0, 0};
+  const float* dnext = D + (int64_t)first * ldd;
+  const float* snext = S + (int64_t)first * lds;
+  const uint32_t* mnext = mask + (int64_t)first * ldm;
+  auto issue = [&]() {
+    if (cur.irow < m) {
+      const int jq = cur.ic * CH + lane * NV;
+      const bool in = jq < n;
+      cp_async16(ring.slot(cur.isl, 0, lane), dnext + (in ? jq : 0), in ? 16 : 0);
+      cp_async16(ring.slot(cur.isl, 1, lane), snext + (in ? jq : 0), in ? 16 : 0);
+      cp_async4(ring.mslot(cur.isl, lane), mnext + (in ? (jq >> 5) : 0), in ? 4 : 0);
+    }
+    cp_commit();
+    cur.isl = (cur.isl + 1) & (RING_ST - 1);
+    if (++cur.ic == nc) {
+      cur.ic = 0;
+      cur.irow += stride;
+      dnext += (int64_t)stride * ldd;
+      snext += (int64_t)stride * lds;
+      mnext += (int64_t)stride * ldm;
+    }
+  };
+  if (ZPF && first < m) copy_coarse_row(lbuf, LH + (int64_t)first * np, np, lane);
+#pragma unroll
+  for (int q = 0; q < RING_ST - 1; ++q) issue();
+  int csl = 0, lb = 0;
+  RegRestrict<float, 2, NV> rr;
+
+  for (int i = first; i < m; i += stride) {
+    float* lhrow = LH + (int64_t)i * np;
+    float* lrow = lbuf + (ZPF ? lb * zlen : 0);
+    if (ZPF) {  // this row's L_H arrived with an earlier ring group (see pcp_update_fast)
+      cp_wait<RING_ST - 2>();
+      __syncwarp();
+    }
+    {
+      // coarse rank-1 update L_H <- (1-ga) L_H + ga * coef * u_i v^T (cpcp.py:399-402)
+      const double cu = ga * coef * u[i];
+      for (int k = lane; k < zlen; k += 32) {
+        const float old = k < nh ? (ZPF ? lrow[k] : lhrow[k]) : 0.f;
+        const float val = k < nh ? (float)((double)one_ga * (double)old + cu * vs[k]) : 0.f;
+        lrow[k] = val;
+        if (k < np) lhrow[k] = val;
+      }
+    }
+    if (ZPF) {
+      if (i + stride < m) copy_coarse_row(lbuf + (lb ^ 1) * zlen, LH + (int64_t)(i + stride) * np, np, lane);
+      lb ^= 1;
+    }
+    __syncwarp();
+    float* sro = S + (int64_t)i * lds;
+    const long long gi = row0 + i;
+    const bool spike_row = spike_on && gi == i_s;
+    rr.begin();
+    float* const outs[2] = {GH + (int64_t)i * np, SH + (int64_t)i * np};
+
+    auto chunk = [&](int c, const float(&w0)[NV], const float(&w1)[NV], auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      const int cbase = c * CH;
+      const int j = cbase + lane * NV;
+      issue();
+      cp_wait<RING_ST - 1>();
+      const int sl = csl;
+      csl = (csl + 1) & (RING_ST - 1);
+      float dv[NV], sold[NV];
+      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 0, lane)), dv);
+      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 1, lane)), sold);
+      const uint32_t bits = (FULL || j < n) ? (*ring.mslot(sl, lane) >> (j & 31)) : 0u;
+      float sh[NV];
+#pragma unroll
+      for (int e = 0; e < NV; ++e) sh[e] = one_gb * sold[e];
+      if (spike_row) {
+#pragma unroll
+        for (int e = 0; e < NV; ++e)
+          if (j + e == j_s) sh[e] += spike_add;
+      }
+      // coarse keys of the lane's 4 columns: k0 for e < 3, k3 for e = 3 (P >= 4)
+      int k0 = max(0, (j >> LGP) - 1), k3 = max(0, ((j + 4) >> LGP) - 1);
+      if (!FULL) {
+        k0 = min(k0, zlen - 2);
+        k3 = min(k3, zlen - 2);
+      }
+      const float z0 = lrow[k0], z1 = lrow[k0 + 1], z3a = lrow[k3], z3b = lrow[k3 + 1];
+      float x[2][NV];
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const float za = e < 3 ? z0 : z3a, zb = e < 3 ? z1 : z3b;
+        const float l = w0[e] * za + w1[e] * zb;
+        const float d = dv[e];
+        const bool obs = (bits >> e) & 1u;
+        const float rh = (l + sh[e]) - d;
+        const float sn = soft_thr<float>(obs ? sh[e] - rh : sh[e], lam_s);  // cpcp.py:414-415
+        x[0][e] = obs ? (l + sn) - d : 0.f;
+        x[1][e] = sn;
+      }
+      float c_sq = 0.f, c_l1 = 0.f, c_ss = 0.f, c_sr = 0.f;
+      int c_nnz = 0;
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const float r = x[0][e], sn = x[1][e];
+        c_sq = fmaf(r, r, c_sq);
+        c_l1 += fabsf(sn);
+        c_nnz += sn != 0.f ? 1 : 0;
+        c_ss = fmaf(sn, sn, c_ss);
+        c_sr = fmaf(sn, r, c_sr);
+        // arg-max |r|, ties to the smallest column-major index: within a lane
+        // rows only grow and columns grow within a row, so on a tie the new
+        // entry wins iff its column is smaller
+        const float mg = fabsf(r);
+        const bool take = (FULL || j + e < n) && (mg > bm || (mg == bm && j + e < bj));
+        bm = take ? mg : bm;
+        bval = take ? r : bval;
+        bsv = take ? sn : bsv;
+        bj = take ? j + e : bj;
+        brow = take ? i : brow;
+      }
+      a_sq += (double)c_sq;
+      a_l1 += (double)c_l1;
+      a_nnz += (double)c_nnz;
+      a_ss += (double)c_ss;
+      a_sr += (double)c_sr;
+      if (FULL || j < n) *reinterpret_cast<float4*>(sro + j) = Vec<float>::pack(x[1]);
+      rr.chunk(w0, w1, x, cbase, outs, lane, LGP);
+    };
+    if (nfull > 0) {
+      chunk(0, cw0, cw1, std::true_type{});
+      for (int c = 1; c < nfull; ++c) chunk(c, rw0, rw1, std::true_type{});
+    }
+    if (nfull < nc) {
+      float t0[NV], t1[NV];
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const bool in = nfull * CH + lane * NV + e < n;
+        t0[e] = in ? (nfull == 0 ? cw0[e] : rw0[e]) : 0.f;
+        t1[e] = in ? (nfull == 0 ? cw1[e] : rw1[e]) : 0.f;
+      }
+      chunk(nfull, t0, t1, std::false_type{});
+    }
+    rr.finish(outs, n, np, lane, LGP);
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __shared__ double scratch[5 * 32];
+  __shared__ AmRecW amw[RW_WARPS];
+  double vals[5] = {a_sq, a_l1, a_nnz, a_ss, a_sr};
+  block_sum<5>(vals, scratch);
+  const long long bidx = brow >= 0 ? (long long)bj * m_global + row0 + brow : -1;
+  AmRecW best{bidx >= 0 ? (double)bm : 0.0, (double)bval, (double)bsv, bidx};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    AmRecW b;
+    b.mag = __shfl_xor_sync(kFull, best.mag, o);
+    b.val = __shfl_xor_sync(kFull, best.val, o);
+    b.sval = __shfl_xor_sync(kFull, best.sval, o);
+    b.idx = __shfl_xor_sync(kFull, best.idx, o);
+    am_merge_w(best, b);
+  }
+  if (lane == 0) amw[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    AmRecW b = amw[0];
+    for (int w = 1; w < RW_WARPS; ++w) am_merge_w(b, amw[w]);
+    double* o = part + 9 * blockIdx.x;
+    for (int q = 0; q < 5; ++q) o[q] = vals[q];
+    o[5] = b.mag;
+    o[6] = b.val;
+    o[7] = b.sval;
+    o[8] = (double)b.idx;
+  }
+}
+
 int cp_rows(CpcpPlan* p, int mode, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S,
             int64_t lds, void* Lout, int64_t ldl, cudaStream_t st) {
   const size_t tb = p->f32 ? 4 : 8;
   const bool reg = rows_reg_ok(p->ch, p->f32);
+  if (mode == kCWUpdate && mask && fast_ok(p->ch, p->f32, {ldd, lds}) && p->m_local < INT_MAX) {
+    size_t smem = (size_t)round_up(p->ch.np * 8, 16) +
+                  RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * 4 + RING_BYTES);
+    const bool zpf = fast_zpf(p->ch, (size_t)round_up(p->ch.np * 8, 16));
+    if (zpf) smem += RW_WARPS * (size_t)round_up(p->ch.np + 2, 4) * 4;
+    auto pick = [&](auto lgp) {
+      constexpr int L = decltype(lgp)::value;
+      return zpf ? cp_update_fast<L, true> : cp_update_fast<L, false>;
+    };
+    const int lg = p->ch.reg_lgp;
+    auto kern = lg == 2 ? pick(std::integral_constant<int, 2>{}) : lg == 3 ? pick(std::integral_constant<int, 3>{})
+              : lg == 4 ? pick(std::integral_constant<int, 4>{}) : pick(std::integral_constant<int, 5>{});
+    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = fast_grid(kern, smem, p->row_blocks);
+    kern<<<grid, RW_THREADS, smem, st>>>(p->dev, p->ch, (int)p->m_local, p->row0, p->m_global, (const float*)D, ldd,
+                                         mask, ldm, (float*)S, lds, (float*)p->LH, (float*)p->GH, (float*)p->SH, p->u,
+                                         p->v, p->row_part, p->row_blocks);
+    MLR_LAUNCH_CHECK("cp_update_fast");
+    return kOk;
+  }
   const size_t stage = reg ? 0 : (p->f32 ? SegRestrict<float, 2, 4>::STAGE_BYTES : SegRestrict<double, 2, 2>::STAGE_BYTES);
   const size_t base = (size_t)round_up(p->ch.np * 8, 16) + RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * tb + stage);
   const bool ring = base + RW_WARPS * RING_BYTES <= 80 * 1024;
