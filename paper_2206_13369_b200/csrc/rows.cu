@@ -601,6 +601,23 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
 // Grid = the resident CTAs (one wave); unused partial-result slots up to the
 // plan's row_blocks are written empty.
 constexpr int FAST_CH = 128;  // 32 lanes x float4
+#ifndef FAST_RING
+#define FAST_RING 4
+#endif
+constexpr int FAST_RING_BYTES = FAST_RING * (2 * 512 + 128);
+template <int ST>
+struct LaneRingT {
+  unsigned char* base;
+  __device__ __forceinline__ unsigned char* slot(int s, int q, int lane) const {
+    return base + ((s * 2 + q) * 32 + lane) * 16;
+  }
+  __device__ __forceinline__ uint32_t* mslot(int s, int lane) const {
+    return reinterpret_cast<uint32_t*>(base + ST * 1024 + (s * 32 + lane) * 4);
+  }
+};
+#ifndef FAST_MINB
+#define FAST_MINB 2
+#endif
 
 // lane-strided cp.async of one coarse row (np floats, np % 4 == 0) into smem
 __device__ __forceinline__ void copy_coarse_row(float* dst, const float* src, int np, int lane) {
@@ -608,7 +625,7 @@ __device__ __forceinline__ void copy_coarse_row(float* dst, const float* src, in
 }
 
 template <int LGP, bool ZPF>
-__global__ void __launch_bounds__(RW_THREADS, 3)
+__global__ void __launch_bounds__(RW_THREADS, FAST_MINB)
 pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* __restrict__ D, int64_t ldd,
                 const float* __restrict__ Yin, float* __restrict__ Yout, int64_t ldy, const float* __restrict__ Z,
                 float* __restrict__ A, double* __restrict__ part, int part_slots) {
@@ -618,9 +635,9 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
   const int n = ch.n, np = ch.np;
   const int zlen = round_up_dev(np + 2, 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + RING_BYTES);
+  unsigned char* wbase = smem_raw + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + FAST_RING_BYTES);
   float* zbuf = reinterpret_cast<float*>(wbase);
-  const LaneRing ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
+  const LaneRingT<FAST_RING> ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
   if (blockIdx.x == 0)
     for (int b = gridDim.x + threadIdx.x; b < part_slots; b += blockDim.x)
       part[3 * b] = part[3 * b + 1] = part[3 * b + 2] = 0.0;
@@ -630,7 +647,8 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
   const float mu = (float)mu_d;
   const float thr = (float)(st->lam * (1.0 / mu_d));
   const float inv_next = (float)(1.0 / (mu_d * st->rho));
-  double acc_res = 0.0, acc_l1 = 0.0, acc_nnz = 0.0;
+  double acc_res = 0.0, acc_l1 = 0.0;
+  long long i_nnz = 0;
   const float* __restrict__ w0p = ch.w0f;
   const float* __restrict__ w1p = ch.w1f;
   float cw0[NV], cw1[NV], rw0[NV], rw1[NV];
@@ -655,7 +673,7 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       cp_async16(ring.slot(isl, 1, lane), ynext + (in ? jq : 0), in ? 16 : 0);
     }
     cp_commit();
-    isl = (isl + 1) & (RING_ST - 1);
+    isl = (isl + 1) & (FAST_RING - 1);
     if (++ic == nc) {
       ic = 0;
       irow += stride;
@@ -665,7 +683,7 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
   };
   if (ZPF && first < m) copy_coarse_row(zbuf, Z + (int64_t)first * np, np, lane);
 #pragma unroll
-  for (int q = 0; q < RING_ST - 1; ++q) issue();
+  for (int q = 0; q < FAST_RING - 1; ++q) issue();
   int csl = 0, zb = 0;
   RegRestrict<float, 1, NV> rr;
 
@@ -673,8 +691,8 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
     float* zrow = zbuf + (ZPF ? zb * zlen : 0);
     if (ZPF) {
       // this row's Z went out with the ring group of the previous row's chunk 0
-      // (>= RING_ST groups ago) or, for the first row, with the first group
-      cp_wait<RING_ST - 2>();
+      // (>= FAST_RING groups ago) or, for the first row, with the first group
+      cp_wait<FAST_RING - 2>();
       __syncwarp();
       if (lane < zlen - np) zrow[np + lane] = 0.f;
       if (i + stride < m) copy_coarse_row(zbuf + (zb ^ 1) * zlen, Z + (int64_t)(i + stride) * np, np, lane);
@@ -692,9 +710,9 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       const int cbase = c * CH;
       const int j = cbase + lane * NV;
       issue();
-      cp_wait<RING_ST - 1>();
+      cp_wait<FAST_RING - 1>();
       const int sl = csl;
-      csl = (csl + 1) & (RING_ST - 1);
+      csl = (csl + 1) & (FAST_RING - 1);
       float dv[NV], yv[NV];
       Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 0, lane)), dv);
       Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 1, lane)), yv);
@@ -724,7 +742,7 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       }
       acc_res += (double)c_res;
       acc_l1 += (double)c_l1;
-      acc_nnz += (double)c_nnz;
+      i_nnz += c_nnz;
       if (FULL || j < n) *reinterpret_cast<float4*>(yrow + j) = Vec<float>::pack(yo);
       rr.chunk(w0, w1, x, cbase, outp, lane, LGP);
     };
@@ -747,7 +765,7 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
   }
   cp_wait<0>();
   __shared__ double scratch[3 * 32];
-  double v[3] = {acc_res, acc_l1, acc_nnz};
+  double v[3] = {acc_res, acc_l1, (double)i_nnz};
   block_sum<3>(v, scratch);
   if (threadIdx.x == 0) {
     part[3 * blockIdx.x + 0] = v[0];
@@ -775,17 +793,17 @@ static int fast_grid(K kern, size_t smem, int want) {
   return std::max(1, std::min(want, sms * std::max(per, 1)));
 }
 
-// double-buffer the coarse row when a row has >= RING_ST chunks and 3 CTAs still fit
+// double-buffer the coarse row when a row has >= FAST_RING chunks and 2 CTAs still fit
 static bool fast_zpf(const ChainDev& ch, size_t fixed) {
   const size_t zl = (size_t)round_up(ch.np + 2, 4) * 4;
-  return (ch.n + FAST_CH - 1) / FAST_CH >= RING_ST && fixed + RW_WARPS * (2 * zl + RING_BYTES) <= 74 * 1024;
+  return (ch.n + FAST_CH - 1) / FAST_CH >= FAST_RING && fixed + RW_WARPS * (2 * zl + FAST_RING_BYTES) <= 110 * 1024;
 }
 
 template <int LGP>
 static int pcp_fast_launch(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy,
                            cudaStream_t st) {
   const bool zpf = fast_zpf(p->ch, 0);
-  const size_t smem = RW_WARPS * ((zpf ? 2 : 1) * (size_t)round_up(p->ch.np + 2, 4) * 4 + RING_BYTES);
+  const size_t smem = RW_WARPS * ((zpf ? 2 : 1) * (size_t)round_up(p->ch.np + 2, 4) * 4 + FAST_RING_BYTES);
   auto kern = zpf ? pcp_update_fast<LGP, true> : pcp_update_fast<LGP, false>;
   MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = fast_grid(kern, smem, p->row_blocks);
@@ -1091,7 +1109,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
 
 // ML-CPCP update pass, FP32 regular-chain fast path (see pcp_update_fast)
 template <int LGP, bool ZPF>
-__global__ void __launch_bounds__(RW_THREADS, 3)
+__global__ void __launch_bounds__(RW_THREADS, FAST_MINB)
 cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0, int64_t m_global,
                const float* __restrict__ D, int64_t ldd, const uint32_t* __restrict__ mask, int64_t ldm,
                float* __restrict__ S, int64_t lds, float* __restrict__ LH, float* __restrict__ GH,
@@ -1104,9 +1122,9 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
   const int zlen = round_up_dev(np + 2, 4);
   double* vs = reinterpret_cast<double*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + RING_BYTES);
+  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + FAST_RING_BYTES);
   float* lbuf = reinterpret_cast<float*>(wbase);
-  const LaneRing ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
+  const LaneRingT<FAST_RING> ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
   for (int k = threadIdx.x; k < np; k += blockDim.x) vs[k] = vg[k];
   if (blockIdx.x == 0)  // empty partial-result slots past the grid
     for (int b = gridDim.x + threadIdx.x; b < part_slots; b += blockDim.x) {
@@ -1136,7 +1154,8 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
     rw0[e] = j1 < n ? __ldg(w0p + j1) : 0.f;
     rw1[e] = j1 < n ? __ldg(w1p + j1) : 0.f;
   }
-  double a_sq = 0.0, a_l1 = 0.0, a_nnz = 0.0, a_ss = 0.0, a_sr = 0.0;
+  double a_sq = 0.0, a_l1 = 0.0, a_ss = 0.0, a_sr = 0.0;
+  long long i_nnz = 0;  // exact, as the per-chunk FP64 sum of the general kernel
   float bm = -1.f, bval = 0.f, bsv = 0.f;
   int bj = INT_MAX, brow = -1;
   const int nfull = n / CH;
@@ -1157,7 +1176,7 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       cp_async4(ring.mslot(cur.isl, lane), mnext + (in ? (jq >> 5) : 0), in ? 4 : 0);
     }
     cp_commit();
-    cur.isl = (cur.isl + 1) & (RING_ST - 1);
+    cur.isl = (cur.isl + 1) & (FAST_RING - 1);
     if (++cur.ic == nc) {
       cur.ic = 0;
       cur.irow += stride;
@@ -1168,7 +1187,7 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
   };
   if (ZPF && first < m) copy_coarse_row(lbuf, LH + (int64_t)first * np, np, lane);
 #pragma unroll
-  for (int q = 0; q < RING_ST - 1; ++q) issue();
+  for (int q = 0; q < FAST_RING - 1; ++q) issue();
   int csl = 0, lb = 0;
   RegRestrict<float, 2, NV> rr;
 
@@ -1176,7 +1195,7 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
     float* lhrow = LH + (int64_t)i * np;
     float* lrow = lbuf + (ZPF ? lb * zlen : 0);
     if (ZPF) {  // this row's L_H arrived with an earlier ring group (see pcp_update_fast)
-      cp_wait<RING_ST - 2>();
+      cp_wait<FAST_RING - 2>();
       __syncwarp();
     }
     {
@@ -1205,9 +1224,9 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       const int cbase = c * CH;
       const int j = cbase + lane * NV;
       issue();
-      cp_wait<RING_ST - 1>();
+      cp_wait<FAST_RING - 1>();
       const int sl = csl;
-      csl = (csl + 1) & (RING_ST - 1);
+      csl = (csl + 1) & (FAST_RING - 1);
       float dv[NV], sold[NV];
       Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 0, lane)), dv);
       Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 1, lane)), sold);
@@ -1249,20 +1268,27 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
         c_nnz += sn != 0.f ? 1 : 0;
         c_ss = fmaf(sn, sn, c_ss);
         c_sr = fmaf(sn, r, c_sr);
-        // arg-max |r|, ties to the smallest column-major index: within a lane
-        // rows only grow and columns grow within a row, so on a tie the new
-        // entry wins iff its column is smaller
-        const float mg = fabsf(r);
-        const bool take = (FULL || j + e < n) && (mg > bm || (mg == bm && j + e < bj));
-        bm = take ? mg : bm;
-        bval = take ? r : bval;
-        bsv = take ? sn : bsv;
-        bj = take ? j + e : bj;
-        brow = take ? i : brow;
+      }
+      // arg-max |r|, ties to the smallest column-major index: within a lane
+      // rows only grow and columns grow within a row, so on a tie the new
+      // entry wins iff its column is smaller.  Chunks whose largest |r| is
+      // below the running best (nearly all) skip the per-element test.
+      const float m4 = fmaxf(fmaxf(fabsf(x[0][0]), fabsf(x[0][1])), fmaxf(fabsf(x[0][2]), fabsf(x[0][3])));
+      if (m4 >= bm) {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) {
+          const float r = x[0][e], mg = fabsf(r);
+          const bool take = (FULL || j + e < n) && (mg > bm || (mg == bm && j + e < bj));
+          bm = take ? mg : bm;
+          bval = take ? r : bval;
+          bsv = take ? x[1][e] : bsv;
+          bj = take ? j + e : bj;
+          brow = take ? i : brow;
+        }
       }
       a_sq += (double)c_sq;
       a_l1 += (double)c_l1;
-      a_nnz += (double)c_nnz;
+      i_nnz += c_nnz;
       a_ss += (double)c_ss;
       a_sr += (double)c_sr;
       if (FULL || j < n) *reinterpret_cast<float4*>(sro + j) = Vec<float>::pack(x[1]);
@@ -1288,7 +1314,7 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
   cp_wait<0>();
   __shared__ double scratch[5 * 32];
   __shared__ AmRecW amw[RW_WARPS];
-  double vals[5] = {a_sq, a_l1, a_nnz, a_ss, a_sr};
+  double vals[5] = {a_sq, a_l1, (double)i_nnz, a_ss, a_sr};
   block_sum<5>(vals, scratch);
   const long long bidx = brow >= 0 ? (long long)bj * m_global + row0 + brow : -1;
   AmRecW best{bidx >= 0 ? (double)bm : 0.0, (double)bval, (double)bsv, bidx};
@@ -1321,7 +1347,7 @@ int cp_rows(CpcpPlan* p, int mode, const void* D, int64_t ldd, const uint32_t* m
   const bool reg = rows_reg_ok(p->ch, p->f32);
   if (mode == kCWUpdate && mask && fast_ok(p->ch, p->f32, {ldd, lds}) && p->m_local < INT_MAX) {
     size_t smem = (size_t)round_up(p->ch.np * 8, 16) +
-                  RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * 4 + RING_BYTES);
+                  RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * 4 + FAST_RING_BYTES);
     const bool zpf = fast_zpf(p->ch, (size_t)round_up(p->ch.np * 8, 16));
     if (zpf) smem += RW_WARPS * (size_t)round_up(p->ch.np + 2, 4) * 4;
     auto pick = [&](auto lgp) {
