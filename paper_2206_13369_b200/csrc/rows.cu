@@ -372,7 +372,7 @@ struct RegRestrict {
         bb += __shfl_xor_sync(kFull, bb, o);
       }
       const T an = L < 32 ? __shfl_down_sync(kFull, a, L) : T(0);
-      if ((lane & (L - 1)) == 0 && lane + L < 32) out[b][pbase + (lane >> (lgp - (NV == 4 ? 2 : 1)))] = bb + an;
+      if ((lane & (L - 1)) == 0 && lane + L < 32) out[b][pbase + (lane >> (lgp - (NV == 8 ? 3 : NV == 4 ? 2 : 1)))] = bb + an;
       if (lane == 0 && have) out[b][pbase - 1] = carry[b] + a;
       carry[b] = __shfl_sync(kFull, bb, 31);
     }
@@ -600,21 +600,49 @@ pcp_rows_warp(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* __
 // when a row has at least RING_ST chunks and the double buffer fits (ZPF).
 // Grid = the resident CTAs (one wave); unused partial-result slots up to the
 // plan's row_blocks are written empty.
-constexpr int FAST_CH = 128;  // 32 lanes x float4
 #ifndef FAST_RING
 #define FAST_RING 4
 #endif
-constexpr int FAST_RING_BYTES = FAST_RING * (2 * 512 + 128);
-template <int ST>
+// per warp: FAST_RING slots of two streams (VB = 4 NV bytes per lane each) + the mask word
+__host__ __device__ constexpr int fast_ring_bytes(int nv) { return FAST_RING * (2 * 32 * 4 * nv + 128); }
+template <int ST, int VB>
 struct LaneRingT {
   unsigned char* base;
   __device__ __forceinline__ unsigned char* slot(int s, int q, int lane) const {
-    return base + ((s * 2 + q) * 32 + lane) * 16;
+    return base + ((s * 2 + q) * 32 + lane) * VB;
   }
   __device__ __forceinline__ uint32_t* mslot(int s, int lane) const {
-    return reinterpret_cast<uint32_t*>(base + ST * 1024 + (s * 32 + lane) * 4);
+    return reinterpret_cast<uint32_t*>(base + ST * 64 * VB + (s * 32 + lane) * 4);
   }
 };
+// NV consecutive floats of one lane: ring slot <-> registers, global row <- registers
+template <int NV>
+__device__ __forceinline__ void ring_unpack(const unsigned char* slot, float (&o)[NV]) {
+#pragma unroll
+  for (int v = 0; v < NV / 4; ++v) {
+    const float4 q = reinterpret_cast<const float4*>(slot)[v];
+    o[4 * v] = q.x;
+    o[4 * v + 1] = q.y;
+    o[4 * v + 2] = q.z;
+    o[4 * v + 3] = q.w;
+  }
+}
+template <int NV, bool FULL>
+__device__ __forceinline__ void row_store(float* row, int j, int n, const float (&o)[NV]) {
+#pragma unroll
+  for (int v = 0; v < NV / 4; ++v)
+    if (FULL || j + 4 * v < n)
+      *reinterpret_cast<float4*>(row + j + 4 * v) = make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+}
+// lane-strided cp.async of NV floats of a fine row (n % 4 == 0; zero-filled past n)
+template <int NV>
+__device__ __forceinline__ void ring_issue(unsigned char* slot, const float* row, int jq, int n) {
+#pragma unroll
+  for (int v = 0; v < NV / 4; ++v) {
+    const bool in = jq + 4 * v < n;
+    cp_async16(slot + 16 * v, row + (in ? jq + 4 * v : 0), in ? 16 : 0);
+  }
+}
 #ifndef FAST_MINB
 #define FAST_MINB 2
 #endif
@@ -624,20 +652,20 @@ __device__ __forceinline__ void copy_coarse_row(float* dst, const float* src, in
   for (int k = lane * 4; k < np; k += 128) cp_async16(dst + k, src + k, 16);
 }
 
-template <int LGP, bool ZPF>
+template <int LGP, bool ZPF, int NV>
 __global__ void __launch_bounds__(RW_THREADS, FAST_MINB)
 pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* __restrict__ D, int64_t ldd,
                 const float* __restrict__ Yin, float* __restrict__ Yout, int64_t ldy, const float* __restrict__ Z,
                 float* __restrict__ A, double* __restrict__ part, int part_slots) {
   if (st->done) return;
-  constexpr int NV = 4, CH = FAST_CH;
+  constexpr int CH = 32 * NV, VB = 4 * NV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = ch.n, np = ch.np;
   const int zlen = round_up_dev(np + 2, 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + FAST_RING_BYTES);
+  unsigned char* wbase = smem_raw + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + fast_ring_bytes(NV));
   float* zbuf = reinterpret_cast<float*>(wbase);
-  const LaneRingT<FAST_RING> ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
+  const LaneRingT<FAST_RING, VB> ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
   if (blockIdx.x == 0)
     for (int b = gridDim.x + threadIdx.x; b < part_slots; b += blockDim.x)
       part[3 * b] = part[3 * b + 1] = part[3 * b + 2] = 0.0;
@@ -651,12 +679,11 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
   long long i_nnz = 0;
   const float* __restrict__ w0p = ch.w0f;
   const float* __restrict__ w1p = ch.w1f;
-  float cw0[NV], cw1[NV], rw0[NV], rw1[NV];
+  // chunk 0 weights are reloaded (L1) per row; interior chunks share rw
+  float rw0[NV], rw1[NV];
 #pragma unroll
   for (int e = 0; e < NV; ++e) {
-    const int j0 = lane * NV + e, j1 = CH + lane * NV + e;
-    cw0[e] = j0 < n ? __ldg(w0p + j0) : 0.f;
-    cw1[e] = j0 < n ? __ldg(w1p + j0) : 0.f;
+    const int j1 = CH + lane * NV + e;
     rw0[e] = j1 < n ? __ldg(w0p + j1) : 0.f;
     rw1[e] = j1 < n ? __ldg(w1p + j1) : 0.f;
   }
@@ -668,9 +695,8 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
   auto issue = [&]() {
     if (irow < m) {
       const int jq = ic * CH + lane * NV;
-      const bool in = jq < n;
-      cp_async16(ring.slot(isl, 0, lane), dnext + (in ? jq : 0), in ? 16 : 0);
-      cp_async16(ring.slot(isl, 1, lane), ynext + (in ? jq : 0), in ? 16 : 0);
+      ring_issue<NV>(ring.slot(isl, 0, lane), dnext, jq, n);
+      ring_issue<NV>(ring.slot(isl, 1, lane), ynext, jq, n);
     }
     cp_commit();
     isl = (isl + 1) & (FAST_RING - 1);
@@ -714,9 +740,10 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       const int sl = csl;
       csl = (csl + 1) & (FAST_RING - 1);
       float dv[NV], yv[NV];
-      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 0, lane)), dv);
-      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 1, lane)), yv);
-      int k0 = max(0, (j >> LGP) - 1), k3 = max(0, ((j + 4) >> LGP) - 1);
+      ring_unpack<NV>(ring.slot(sl, 0, lane), dv);
+      ring_unpack<NV>(ring.slot(sl, 1, lane), yv);
+      // coarse keys of the lane's NV columns: k0 for e < NV - 1, k3 for the last (P >= NV)
+      int k0 = max(0, (j >> LGP) - 1), k3 = max(0, ((j + NV) >> LGP) - 1);
       if (!FULL) {
         k0 = min(k0, zlen - 2);
         k3 = min(k3, zlen - 2);
@@ -727,7 +754,7 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       int c_nnz = 0;
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
-        const float za = e < 3 ? z0 : z3a, zb_ = e < 3 ? z1 : z3b;
+        const float za = e < NV - 1 ? z0 : z3a, zb_ = e < NV - 1 ? z1 : z3b;
         const float l = w0[e] * za + w1[e] * zb_;
         const float d = dv[e], y = yv[e];
         const float w = y * inv + d - l;
@@ -743,10 +770,16 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       acc_res += (double)c_res;
       acc_l1 += (double)c_l1;
       i_nnz += c_nnz;
-      if (FULL || j < n) *reinterpret_cast<float4*>(yrow + j) = Vec<float>::pack(yo);
+      row_store<NV, FULL>(yrow, j, n, yo);
       rr.chunk(w0, w1, x, cbase, outp, lane, LGP);
     };
     if (nfull > 0) {
+      float cw0[NV], cw1[NV];
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        cw0[e] = __ldg(w0p + lane * NV + e);
+        cw1[e] = __ldg(w1p + lane * NV + e);
+      }
       chunk(0, cw0, cw1, std::true_type{});
       for (int c = 1; c < nfull; ++c) chunk(c, rw0, rw1, std::true_type{});
     }
@@ -754,9 +787,10 @@ pcp_update_fast(const PcpDev* __restrict__ st, ChainDev ch, int m, const float* 
       float t0[NV], t1[NV];
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
-        const bool in = nfull * CH + lane * NV + e < n;
-        t0[e] = in ? (nfull == 0 ? cw0[e] : rw0[e]) : 0.f;
-        t1[e] = in ? (nfull == 0 ? cw1[e] : rw1[e]) : 0.f;
+        const int jt = nfull * CH + lane * NV + e;
+        const bool in = jt < n;
+        t0[e] = in ? (nfull == 0 ? __ldg(w0p + jt) : rw0[e]) : 0.f;
+        t1[e] = in ? (nfull == 0 ? __ldg(w1p + jt) : rw1[e]) : 0.f;
       }
       chunk(nfull, t0, t1, std::false_type{});
     }
@@ -793,18 +827,28 @@ static int fast_grid(K kern, size_t smem, int want) {
   return std::max(1, std::min(want, sms * std::max(per, 1)));
 }
 
-// double-buffer the coarse row when a row has >= FAST_RING chunks and 2 CTAs still fit
-static bool fast_zpf(const ChainDev& ch, size_t fixed) {
-  const size_t zl = (size_t)round_up(ch.np + 2, 4) * 4;
-  return (ch.n + FAST_CH - 1) / FAST_CH >= FAST_RING && fixed + RW_WARPS * (2 * zl + FAST_RING_BYTES) <= 110 * 1024;
+// Columns per lane.  8 (when a coarse group spans >= 8) halves the per-chunk
+// overhead; measured (B200): ML-CPCP C4 -10%, C3 -15%, but ML-PCP C2 +8% and
+// C5 +12% (its larger ring no longer leaves room for two CTAs' coarse rows).
+static int fast_nv(const ChainDev& ch, bool cpcp) {
+  const char* env = getenv("MLR_FAST_NV");
+  if (env && (env[0] == '4' || env[0] == '8')) return ch.reg_lgp >= 3 ? env[0] - '0' : 4;
+  return cpcp && ch.reg_lgp >= 3 ? 8 : 4;
 }
 
-template <int LGP>
+// double-buffer the coarse row when a row has >= FAST_RING chunks and 2 CTAs still fit
+static bool fast_zpf(const ChainDev& ch, size_t fixed, int nv) {
+  const size_t zl = (size_t)round_up(ch.np + 2, 4) * 4;
+  return (ch.n + 32 * nv - 1) / (32 * nv) >= FAST_RING &&
+         fixed + RW_WARPS * (2 * zl + fast_ring_bytes(nv)) <= 110 * 1024;
+}
+
+template <int LGP, int NV>
 static int pcp_fast_launch(PcpPlan* p, const void* D, int64_t ldd, const void* Yin, void* Yout, int64_t ldy,
                            cudaStream_t st) {
-  const bool zpf = fast_zpf(p->ch, 0);
-  const size_t smem = RW_WARPS * ((zpf ? 2 : 1) * (size_t)round_up(p->ch.np + 2, 4) * 4 + FAST_RING_BYTES);
-  auto kern = zpf ? pcp_update_fast<LGP, true> : pcp_update_fast<LGP, false>;
+  const bool zpf = fast_zpf(p->ch, 0, NV);
+  const size_t smem = RW_WARPS * ((zpf ? 2 : 1) * (size_t)round_up(p->ch.np + 2, 4) * 4 + fast_ring_bytes(NV));
+  auto kern = zpf ? pcp_update_fast<LGP, true, NV> : pcp_update_fast<LGP, false, NV>;
   MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = fast_grid(kern, smem, p->row_blocks);
   kern<<<grid, RW_THREADS, smem, st>>>(p->dev, p->ch, (int)p->m_local, (const float*)D, ldd, (const float*)Yin,
@@ -826,11 +870,15 @@ int pcp_rows(PcpPlan* p, int mode, const void* D, int64_t ldd, const void* Yin, 
   const size_t tb = p->f32 ? 4 : 8;
   const bool reg = rows_reg_ok(p->ch, p->f32);
   if (mode == kWUpdate && fast_ok(p->ch, p->f32, {ldd, ldy}) && p->m_local < INT_MAX) {
+    const bool v8 = fast_nv(p->ch, false) == 8;
     switch (p->ch.reg_lgp) {
-      case 2: return pcp_fast_launch<2>(p, D, ldd, Yin, Yout, ldy, st);
-      case 3: return pcp_fast_launch<3>(p, D, ldd, Yin, Yout, ldy, st);
-      case 4: return pcp_fast_launch<4>(p, D, ldd, Yin, Yout, ldy, st);
-      default: return pcp_fast_launch<5>(p, D, ldd, Yin, Yout, ldy, st);
+      case 2: return pcp_fast_launch<2, 4>(p, D, ldd, Yin, Yout, ldy, st);
+      case 3: return v8 ? pcp_fast_launch<3, 8>(p, D, ldd, Yin, Yout, ldy, st)
+                        : pcp_fast_launch<3, 4>(p, D, ldd, Yin, Yout, ldy, st);
+      case 4: return v8 ? pcp_fast_launch<4, 8>(p, D, ldd, Yin, Yout, ldy, st)
+                        : pcp_fast_launch<4, 4>(p, D, ldd, Yin, Yout, ldy, st);
+      default: return v8 ? pcp_fast_launch<5, 8>(p, D, ldd, Yin, Yout, ldy, st)
+                         : pcp_fast_launch<5, 4>(p, D, ldd, Yin, Yout, ldy, st);
     }
   }
   const size_t stage = reg ? 0 : (p->f32 ? SegRestrict<float, 1, 4>::STAGE_BYTES : SegRestrict<double, 1, 2>::STAGE_BYTES);
@@ -1108,7 +1156,7 @@ cp_rows_warp(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row
 }
 
 // ML-CPCP update pass, FP32 regular-chain fast path (see pcp_update_fast)
-template <int LGP, bool ZPF>
+template <int LGP, bool ZPF, int NV>
 __global__ void __launch_bounds__(RW_THREADS, FAST_MINB)
 cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0, int64_t m_global,
                const float* __restrict__ D, int64_t ldd, const uint32_t* __restrict__ mask, int64_t ldm,
@@ -1116,15 +1164,15 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
                float* __restrict__ SH, const double* __restrict__ u, const double* __restrict__ vg,
                double* __restrict__ part, int part_slots) {
   if (st->done) return;
-  constexpr int NV = 4, CH = FAST_CH;
+  constexpr int CH = 32 * NV, VB = 4 * NV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = ch.n, nh = ch.nh, np = ch.np;
   const int zlen = round_up_dev(np + 2, 4);
   double* vs = reinterpret_cast<double*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + FAST_RING_BYTES);
+  unsigned char* wbase = smem_raw + round_up_dev(np * 8, 16) + (size_t)warp * ((ZPF ? 2 : 1) * zlen * 4 + fast_ring_bytes(NV));
   float* lbuf = reinterpret_cast<float*>(wbase);
-  const LaneRingT<FAST_RING> ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
+  const LaneRingT<FAST_RING, VB> ring{wbase + (ZPF ? 2 : 1) * zlen * 4};
   for (int k = threadIdx.x; k < np; k += blockDim.x) vs[k] = vg[k];
   if (blockIdx.x == 0)  // empty partial-result slots past the grid
     for (int b = gridDim.x + threadIdx.x; b < part_slots; b += blockDim.x) {
@@ -1145,12 +1193,10 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
   const float* __restrict__ w1p = ch.w1f;
   // stencil weights: chunk 0 (the first coarse group differs) and the
   // periodic interior chunks, held for the whole kernel
-  float cw0[NV], cw1[NV], rw0[NV], rw1[NV];
+  float rw0[NV], rw1[NV];  // chunk 0 weights are reloaded (L1) per row
 #pragma unroll
   for (int e = 0; e < NV; ++e) {
-    const int j0 = lane * NV + e, j1 = CH + lane * NV + e;
-    cw0[e] = j0 < n ? __ldg(w0p + j0) : 0.f;
-    cw1[e] = j0 < n ? __ldg(w1p + j0) : 0.f;
+    const int j1 = CH + lane * NV + e;
     rw0[e] = j1 < n ? __ldg(w0p + j1) : 0.f;
     rw1[e] = j1 < n ? __ldg(w1p + j1) : 0.f;
   }
@@ -1171,8 +1217,8 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
     if (cur.irow < m) {
       const int jq = cur.ic * CH + lane * NV;
       const bool in = jq < n;
-      cp_async16(ring.slot(cur.isl, 0, lane), dnext + (in ? jq : 0), in ? 16 : 0);
-      cp_async16(ring.slot(cur.isl, 1, lane), snext + (in ? jq : 0), in ? 16 : 0);
+      ring_issue<NV>(ring.slot(cur.isl, 0, lane), dnext, jq, n);
+      ring_issue<NV>(ring.slot(cur.isl, 1, lane), snext, jq, n);
       cp_async4(ring.mslot(cur.isl, lane), mnext + (in ? (jq >> 5) : 0), in ? 4 : 0);
     }
     cp_commit();
@@ -1228,8 +1274,8 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       const int sl = csl;
       csl = (csl + 1) & (FAST_RING - 1);
       float dv[NV], sold[NV];
-      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 0, lane)), dv);
-      Vec<float>::unpack(*reinterpret_cast<const float4*>(ring.slot(sl, 1, lane)), sold);
+      ring_unpack<NV>(ring.slot(sl, 0, lane), dv);
+      ring_unpack<NV>(ring.slot(sl, 1, lane), sold);
       const uint32_t bits = (FULL || j < n) ? (*ring.mslot(sl, lane) >> (j & 31)) : 0u;
       float sh[NV];
 #pragma unroll
@@ -1239,8 +1285,8 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
         for (int e = 0; e < NV; ++e)
           if (j + e == j_s) sh[e] += spike_add;
       }
-      // coarse keys of the lane's 4 columns: k0 for e < 3, k3 for e = 3 (P >= 4)
-      int k0 = max(0, (j >> LGP) - 1), k3 = max(0, ((j + 4) >> LGP) - 1);
+      // coarse keys of the lane's NV columns: k0 for e < NV - 1, k3 for the last (P >= NV)
+      int k0 = max(0, (j >> LGP) - 1), k3 = max(0, ((j + NV) >> LGP) - 1);
       if (!FULL) {
         k0 = min(k0, zlen - 2);
         k3 = min(k3, zlen - 2);
@@ -1249,7 +1295,7 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       float x[2][NV];
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
-        const float za = e < 3 ? z0 : z3a, zb = e < 3 ? z1 : z3b;
+        const float za = e < NV - 1 ? z0 : z3a, zb = e < NV - 1 ? z1 : z3b;
         const float l = w0[e] * za + w1[e] * zb;
         const float d = dv[e];
         const bool obs = (bits >> e) & 1u;
@@ -1273,7 +1319,9 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       // rows only grow and columns grow within a row, so on a tie the new
       // entry wins iff its column is smaller.  Chunks whose largest |r| is
       // below the running best (nearly all) skip the per-element test.
-      const float m4 = fmaxf(fmaxf(fabsf(x[0][0]), fabsf(x[0][1])), fmaxf(fabsf(x[0][2]), fabsf(x[0][3])));
+      float m4 = fabsf(x[0][0]);
+#pragma unroll
+      for (int e = 1; e < NV; ++e) m4 = fmaxf(m4, fabsf(x[0][e]));
       if (m4 >= bm) {
 #pragma unroll
         for (int e = 0; e < NV; ++e) {
@@ -1291,10 +1339,16 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       i_nnz += c_nnz;
       a_ss += (double)c_ss;
       a_sr += (double)c_sr;
-      if (FULL || j < n) *reinterpret_cast<float4*>(sro + j) = Vec<float>::pack(x[1]);
+      row_store<NV, FULL>(sro, j, n, x[1]);
       rr.chunk(w0, w1, x, cbase, outs, lane, LGP);
     };
     if (nfull > 0) {
+      float cw0[NV], cw1[NV];
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        cw0[e] = __ldg(w0p + lane * NV + e);
+        cw1[e] = __ldg(w1p + lane * NV + e);
+      }
       chunk(0, cw0, cw1, std::true_type{});
       for (int c = 1; c < nfull; ++c) chunk(c, rw0, rw1, std::true_type{});
     }
@@ -1302,9 +1356,10 @@ cp_update_fast(const CpcpDev* __restrict__ st, ChainDev ch, int m, int64_t row0,
       float t0[NV], t1[NV];
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
-        const bool in = nfull * CH + lane * NV + e < n;
-        t0[e] = in ? (nfull == 0 ? cw0[e] : rw0[e]) : 0.f;
-        t1[e] = in ? (nfull == 0 ? cw1[e] : rw1[e]) : 0.f;
+        const int jt = nfull * CH + lane * NV + e;
+        const bool in = jt < n;
+        t0[e] = in ? (nfull == 0 ? __ldg(w0p + jt) : rw0[e]) : 0.f;
+        t1[e] = in ? (nfull == 0 ? __ldg(w1p + jt) : rw1[e]) : 0.f;
       }
       chunk(nfull, t0, t1, std::false_type{});
     }
@@ -1346,17 +1401,21 @@ int cp_rows(CpcpPlan* p, int mode, const void* D, int64_t ldd, const uint32_t* m
   const size_t tb = p->f32 ? 4 : 8;
   const bool reg = rows_reg_ok(p->ch, p->f32);
   if (mode == kCWUpdate && mask && fast_ok(p->ch, p->f32, {ldd, lds}) && p->m_local < INT_MAX) {
-    size_t smem = (size_t)round_up(p->ch.np * 8, 16) +
-                  RW_WARPS * ((size_t)round_up(p->ch.np + 2, 4) * 4 + FAST_RING_BYTES);
-    const bool zpf = fast_zpf(p->ch, (size_t)round_up(p->ch.np * 8, 16));
-    if (zpf) smem += RW_WARPS * (size_t)round_up(p->ch.np + 2, 4) * 4;
-    auto pick = [&](auto lgp) {
-      constexpr int L = decltype(lgp)::value;
-      return zpf ? cp_update_fast<L, true> : cp_update_fast<L, false>;
+    const int nv = fast_nv(p->ch, true);
+    const size_t fixed = (size_t)round_up(p->ch.np * 8, 16);
+    const bool zpf = fast_zpf(p->ch, fixed, nv);
+    const size_t smem = fixed + RW_WARPS * ((zpf ? 2 : 1) * (size_t)round_up(p->ch.np + 2, 4) * 4 + fast_ring_bytes(nv));
+    auto pick = [&](auto lgp, auto v) {
+      constexpr int L = decltype(lgp)::value, V = decltype(v)::value;
+      return zpf ? cp_update_fast<L, true, V> : cp_update_fast<L, false, V>;
     };
+    using I4 = std::integral_constant<int, 4>;
+    using I8 = std::integral_constant<int, 8>;
     const int lg = p->ch.reg_lgp;
-    auto kern = lg == 2 ? pick(std::integral_constant<int, 2>{}) : lg == 3 ? pick(std::integral_constant<int, 3>{})
-              : lg == 4 ? pick(std::integral_constant<int, 4>{}) : pick(std::integral_constant<int, 5>{});
+    auto kern = lg == 2   ? pick(std::integral_constant<int, 2>{}, I4{})
+                : lg == 3 ? (nv == 8 ? pick(std::integral_constant<int, 3>{}, I8{}) : pick(std::integral_constant<int, 3>{}, I4{}))
+                : lg == 4 ? (nv == 8 ? pick(std::integral_constant<int, 4>{}, I8{}) : pick(std::integral_constant<int, 4>{}, I4{}))
+                          : (nv == 8 ? pick(std::integral_constant<int, 5>{}, I8{}) : pick(std::integral_constant<int, 5>{}, I4{}));
     MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = fast_grid(kern, smem, p->row_blocks);
     kern<<<grid, RW_THREADS, smem, st>>>(p->dev, p->ch, (int)p->m_local, p->row0, p->m_global, (const float*)D, ldd,
