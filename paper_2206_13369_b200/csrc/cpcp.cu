@@ -14,8 +14,11 @@
 // mask once and writes S once.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "cpcp.h"
@@ -627,6 +630,119 @@ cp_dots_coarse_kernel(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, in
   }
 }
 
+// FP32 masked variant of cp_dots_coarse_kernel: each lane owns 4 consecutive
+// coarse columns and moves them as float4 (one 16-byte load per array per
+// 128 columns instead of four 4-byte loads), and with n_p <= 128 (SEG1) all
+// five coarse rows are loaded before the u_i reduction so their latency
+// overlaps it.  E_i's right neighbour (the tridiagonal term) comes from the
+// next lane by a shuffle.
+template <bool SEG1>
+__global__ void __launch_bounds__(256)
+cp_dots_coarse_v4(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t row0, const float* __restrict__ LH,
+                  const float* __restrict__ GH, const float* __restrict__ SH, const float* __restrict__ mgd,
+                  const float* __restrict__ mgo, const double* __restrict__ v, const double* __restrict__ vin,
+                  double* __restrict__ u, double* __restrict__ part) {
+  if (st->done) return;
+  __shared__ double scratch[3 * 32];
+  const int nh = ch.nh, np = ch.np;
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int64_t wglob = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+  const int64_t wstride = (int64_t)gridDim.x * warps;
+  const double coef = st->coef;
+  const double rs2 = st->none ? 0.0 : 1.0 / sqrt(st->s2);
+  const bool spike_on = st->corner_s;
+  const long long i_s = st->i_s;
+  const int j_s = st->j_s;
+  const double spike = st->spike;
+  double aa = 0.0, ab = 0.0, ar = 0.0;
+  auto ld4 = [](const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); };
+  const int k1 = lane * 4;
+  // SEG1: the next row's five coarse rows are in flight while this one is evaluated
+  float4 n_g = make_float4(0.f, 0.f, 0.f, 0.f), n_l = n_g, n_s = n_g, n_d = n_g, n_o = n_g;
+  auto prefetch = [&](int64_t r) {
+    if (SEG1 && r < m && k1 < np) {
+      n_g = ld4(GH + r * np + k1);
+      n_l = ld4(LH + r * np + k1);
+      n_s = ld4(SH + r * np + k1);
+      n_d = ld4(mgd + r * np + k1);
+      n_o = ld4(mgo + r * np + k1);
+    }
+  };
+  prefetch(wglob);
+  for (int64_t i = wglob; i < m; i += wstride) {
+    const float* g = GH + i * np;
+    const float* lh = LH + i * np;
+    const float* sh = SH + i * np;
+    const float* md = mgd + i * np;
+    const float* mo = mgo + i * np;
+    const float4 g4 = n_g, l4 = n_l, s4 = n_s, d4 = n_d, o4 = n_o;
+    prefetch(i + wstride);
+    double d = 0.0;
+    for (int base = 0; base < np; base += 128) {
+      const int k = base + k1;
+      if (k >= np) break;
+      const float4 gg = SEG1 ? g4 : ld4(g + k);
+      const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k + q < nh) d = fma((double)gv[q], vin[k + q], d);
+    }
+    d = warp_sum(d);
+    const double ui = st->none ? 0.0 : d * rs2;
+    if (lane == 0) u[i] = ui;
+    const double cu = coef * ui;
+    double e_ab = 0.0, e_ar = 0.0, e_aa = 0.0;
+    for (int base = 0; base < np; base += 128) {  // uniform trip count (shuffles below)
+      const int k = base + k1;
+      const bool act = k < np;
+      float4 gg = g4, ll = l4, ss = s4, dd = d4, oo = o4;
+      if (!SEG1 && act) {
+        gg = ld4(g + k);
+        ll = ld4(lh + k);
+        ss = ld4(sh + k);
+        dd = ld4(md + k);
+        oo = ld4(mo + k);
+      }
+      const float gv[4] = {gg.x, gg.y, gg.z, gg.w}, lv[4] = {ll.x, ll.y, ll.z, ll.w};
+      const float sv[4] = {ss.x, ss.y, ss.z, ss.w}, dv[4] = {dd.x, dd.y, dd.z, dd.w};
+      const float ov[4] = {oo.x, oo.y, oo.z, oo.w};
+      double e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) e[q] = (act && k + q < nh) ? cu * v[k + q] - (double)lv[q] : 0.0;
+      double enext = __shfl_down_sync(0xffffffffu, e[0], 1);
+      if (lane == 31) {  // first column of the next 128-column segment
+        const int kn = base + 128;
+        enext = kn < nh ? cu * v[kn] - (double)lh[kn] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double e1 = q < 3 ? e[q + 1] : enext;
+        e_aa = fma(e[q] * (double)dv[q], e[q], e_aa);
+        e_aa = fma(2.0 * e[q] * (double)ov[q], e1, e_aa);
+        e_ab = fma(e[q], (double)sv[q], e_ab);
+        e_ar = fma(e[q], (double)gv[q], e_ar);
+      }
+    }
+    ab -= e_ab;
+    ar += e_ar;
+    aa += e_aa;
+    if (spike_on && (row0 + i) == i_s && lane == 0) {
+      const int c = ch.c0[j_s];
+      const double ec = cu * v[c] - (double)lh[c];
+      const double ec1 = c + 1 < nh ? cu * v[c + 1] - (double)lh[c + 1] : 0.0;
+      ab += spike * (ec * ch.w0[j_s] + ec1 * ch.w1[j_s]);
+    }
+  }
+  double vals[3] = {aa, ab, ar};
+  block_sum<3>(vals, scratch);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x + 0] = vals[0];
+    part[3 * blockIdx.x + 1] = vals[1];
+    part[3 * blockIdx.x + 2] = vals[2];
+  }
+}
+
 // Per-row coarse evaluation of the segment-QP dots (warp per row):
 //   u_i  = g_H[i] . vin / sqrt(s2)           (left vector of the triple)
 //   E_i  = coef * u_i * v - L_H[i]          (a = P[E R^T])
@@ -1009,10 +1125,21 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   p->timer.end(1, st);
   p->timer.begin(st);
   if (p->m_local > 0 && p->coarse_dots) {
-    const int blocks = p->row_blocks;
+    int blocks = p->row_blocks;
     const void* mgd = p->mask_dev ? p->mgd : nullptr;
     const void* mgo = p->mask_dev ? p->mgo : nullptr;
-    if (p->f32)
+    const char* v4env = getenv("MLR_DOTS_V4");
+    if (p->f32 && mgd && p->ch.np % 4 == 0 && !(v4env && v4env[0] == '0')) {
+      auto kern = p->ch.np <= 128 ? cp_dots_coarse_v4<true> : cp_dots_coarse_v4<false>;
+      int dev = 0, sms = 0, per = 0;  // one wave: every warp pipelines its rows
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0);
+      blocks = std::max(1, std::min(blocks, sms * std::max(per, 1)));
+      kern<<<blocks, 256, 0, st>>>(p->dev, p->ch, p->m_local, p->row0, (const float*)p->LH, (const float*)p->GH,
+                                   (const float*)p->SH, (const float*)mgd, (const float*)mgo, p->v, p->vin, p->u,
+                                   p->dots_part);
+    } else if (p->f32)
       cp_dots_coarse_kernel<float><<<blocks, 256, 0, st>>>(p->dev, p->ch, p->m_local, p->row0, (const float*)p->LH,
                                                            (const float*)p->GH, (const float*)p->SH,
                                                            (const float*)mgd, (const float*)mgo, p->v, p->vin, p->u,
