@@ -802,6 +802,10 @@ __global__ void pcp_finalize_kernel(PcpDev* st, const double* __restrict__ red, 
 
 __global__ void pcp_after_jacobi(PcpDev* st, const int* __restrict__ jac_result) {
   if (st->done) return;
+  if (st->jac_skip) {  // rank 0 certified: no eigensolve this iteration
+    st->jac_sweeps = 0;
+    return;
+  }
   int r = jac_result[0];
   st->jac_sweeps = r;
   if (r <= 0) st->status = 3;
@@ -1230,6 +1234,120 @@ __global__ void eig_permute_kernel(const PcpDev* __restrict__ st, const double* 
   }
 }
 
+__global__ void pcp_jac_skip_done(PcpDev* st) { st->jac_skip = st->done; }
+
+// Rank-0 certificate (ahead of the coarse eigensolve).  When every singular
+// value of M_H is <= tau the SVT is zero (pcp.py:258-262: rank = #{sigma >
+// tau} = 0, L_H = 0, nuclear = 0) and the eigenvectors are not needed.  That
+// holds iff tau^2 I - B~ is positive definite, which a Cholesky factorisation
+// decides exactly.  The test uses tau^2 (1 - 1e-10), so a borderline case
+// falls back to the eigensolver.  Cheap exit first: any diagonal entry of B~
+// above tau^2 is a lower bound on lambda_max, so the rank is positive.
+// Two-CTA cluster, columns split by parity, each CTA holding the packed lower
+// part of its columns in shared memory; column k is published through DSMEM.
+// Sets st->jac_skip = done || certified.  (In the reference the first
+// iterations after the start often have rank 0: C2 iterations 2-5.)
+constexpr int R0_THREADS = 1024;
+
+__host__ __device__ __forceinline__ int64_t r0_off(int t, int n, int c) {  // packed start of local column t
+  return (int64_t)t * (n - c) - (int64_t)t * (t - 1);
+}
+int64_t rank0_smem_bytes(int nh) {
+  const int t1 = (nh + 1) / 2;  // columns of CTA 0 (the larger half)
+  return (r0_off(t1, nh, 0) + 3 * (int64_t)nh) * 8 + 64;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(R0_THREADS)
+pcp_rank0_test(PcpDev* st, const double* __restrict__ Bt, int np, int nh) {
+  extern __shared__ __align__(16) double r0s[];
+  __shared__ int s_flag;  // 0 running, 1 rank > 0 (exit)
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = R0_THREADS / 32;
+  const double tau = st->tau;
+  const double lim = tau * tau * (1.0 - 1e-10);
+  const int done = st->done;
+  const int ncols = (nh - c + 1) / 2;  // local columns j = 2t + c
+  double* col = r0s;                                    // packed lower parts
+  double* lbuf = r0s + r0_off((nh + 1) / 2, nh, 0);     // [2][nh] published column (same offset in both CTAs)
+  double* lloc = lbuf + 2 * (int64_t)nh;                // local copy of the published column
+  if (tid == 0) s_flag = done ? 1 : 0;
+  __syncthreads();
+  // cheap exit: max diagonal > lim  =>  lambda_max > tau^2
+  if (!done) {
+    int big = 0;
+    for (int i = tid; i < nh; i += R0_THREADS) big |= Bt[(int64_t)i * np + i] > lim;
+    if (__syncthreads_or(big) && tid == 0) s_flag = 1;
+    __syncthreads();
+  }
+  if (s_flag) {  // identical decision in both CTAs (same inputs)
+    if (c == 0 && tid == 0) st->jac_skip = done;
+    return;
+  }
+  // load lim I - B~ (lower part of my columns)
+  for (int t = warp; t < ncols; t += nwarps) {
+    const int j = 2 * t + c;
+    double* cj = col + r0_off(t, nh, c);
+    for (int i = j + lane; i < nh; i += 32) cj[i - j] = (i == j ? lim : 0.0) - Bt[(int64_t)i * np + j];
+  }
+  cl.sync();
+  int fail = 0;
+  for (int k = 0; k < nh; ++k) {
+    const int owner = k & 1, buf = k & 1;
+    if (c == owner) {
+      double* ck = col + r0_off(k >> 1, nh, c);
+      const double d = ck[0];
+      if (!(d > 0.0)) {
+        if (tid == 0) s_flag = 1;
+      } else {
+        const double r = rsqrt(d);
+        for (int i = k + 1 + tid; i < nh; i += R0_THREADS) lbuf[buf * nh + i] = ck[i - k] * r;
+      }
+    }
+    cl.sync();  // column k published (or the owner failed)
+    double* ob = cl.map_shared_rank(lbuf, owner);
+    const int* of = cl.map_shared_rank(&s_flag, owner);
+    if (*of) {
+      fail = 1;
+      break;
+    }
+    for (int i = k + 1 + tid; i < nh; i += R0_THREADS) lloc[i] = ob[buf * nh + i];
+    __syncthreads();
+    // trailing update of my columns j > k: a_ij -= l_i l_j (i >= j)
+    const int t0 = (k + 1 - c + 1) / 2;  // first local column with j > k
+    for (int t = t0 + warp; t < ncols; t += nwarps) {
+      const int j = 2 * t + c;
+      double* cj = col + r0_off(t, nh, c);
+      const double lj = lloc[j];
+      for (int i = j + lane; i < nh; i += 32) cj[i - j] = fma(-lloc[i], lj, cj[i - j]);
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA leaves while its shared memory may still be read
+  if (c == 0 && tid == 0) st->jac_skip = fail ? 0 : 1;
+}
+
+int pcp_rank0(PcpPlan* p, cudaStream_t st) {
+  const int nh = p->ch.nh, np = p->ch.np;
+  const int64_t smem = rank0_smem_bytes(nh);
+  static int max_optin = -1;
+  if (max_optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  const char* env = getenv("MLR_RANK0_TEST");
+  if (smem > max_optin || (env && env[0] == '0')) {
+    pcp_jac_skip_done<<<1, 1, 0, st>>>(p->dev);
+    MLR_LAUNCH_CHECK("pcp_jac_skip_done");
+    return kOk;
+  }
+  MLR_CUDA(cudaFuncSetAttribute(pcp_rank0_test, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pcp_rank0_test<<<2, R0_THREADS, smem, st>>>(p->dev, p->Bm, np, nh);
+  MLR_LAUNCH_CHECK("pcp_rank0_test");
+  return kOk;
+}
+
 // Coarse SVT from the (all-reduced) Gram in red: B = G^-1 K G^-1; Jacobi
 // on X = B V (warm start V); W~ = G^-1 V diag(f) V^T; Z = A W~.
 int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
@@ -1260,8 +1378,9 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   if ((rc = mm(p->T1, true, p->Xm, false, p->Bm, nullptr))) return rc;       // B~ = U^T T
   p->timer.end(kPhPre, st);
   p->timer.begin(st);
+  if ((rc = pcp_rank0(p, st))) return rc;
   if ((rc = jacobi2_eig(false, p->Bm, p->Vm, np, np, p->jac_tol_host, p->jac_floor_rel, p->jac_max_sweeps, p->qbuf,
-                        p->qflag, p->jac_off, p->jac_result, skip, st)))
+                        p->qflag, p->jac_off, p->jac_result, &p->dev->jac_skip, st)))
     return rc;
   p->timer.end(kPhJacobi, st);
   p->timer.begin(st);

@@ -28,6 +28,7 @@ struct PcpDev {
   int max_iters;
   int jac_sweeps;
   int trunc, sv, sv_cap;  // ialm_solve: keep only the top-sv triplets, adapt sv (pcp.py:157-165)
+  int jac_skip;     // Jacobi not needed this iteration: done, or rank 0 certified (pcp_rank0_test)
 };
 
 struct LanczosDev {
