@@ -322,9 +322,9 @@ def main():
     streaming = None
     if upd:
         ach = upd_bytes / (upd[0] / upd[1] / 1e3) / 1e9
-        t = traffic.get("pcp_rows_warp<float, 1>")
-        streaming = {"bound": "hbm", "kernel": "pcp_rows_warp<float,kUpdate> (fused prolong/shrink/dual/restrict, "
-                     "warp per row)", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+        t = traffic.get("pcp_update_fast")
+        streaming = {"bound": "hbm", "kernel": "pcp_update_fast<3,true,4> (FP32 regular-chain fused prolong/shrink/"
+                     "dual/restrict, warp per row)", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / peaks["hbm_gbs"], "traffic": t["dram_bytes_per_launch"] if t else None,
                      "algorithmic_bytes_per_launch": upd_bytes, "avg_us": 1e3 * upd[0] / upd[1],
                      "bytes_formula": "b (3 m n + 2 m n_p)"}
@@ -340,8 +340,8 @@ def main():
                "sample": f"1 full C2 solve ({it} iterations, oracle port of mlrpca.ml_ialm_solve, numpy/OpenBLAS FP64)"}
 
     lz = statistics.mean(s.get("lanczos_steps", 0) for s in sink) if sink else 0
-    # launches per solve (counted in profiles/r01_bench_launches_c2.csv): 20 per loop
-    # call (gram 3, pre 6 incl. split-K sums, jacobi + V update 2, after/weights 2,
+    # launches per solve (counted in profiles/r02_bench_launches_c2.csv): 21 per loop
+    # call (gram 3, pre 6 incl. split-K sums, rank-0 test 1, jacobi + V update 2, after/weights 2,
     # post 4, recon 1, update 1, finalize 1), 3 per Lanczos step (D^T D q, slice sum,
     # update), 11 fixed.  Calls and steps are issued in batches of 4 and the polling
     # is pipelined one batch deep, so one batch of each runs (as no-ops) past the end.
@@ -350,7 +350,7 @@ def main():
         lz_launches = 2  # init + the single cooperative Lanczos kernel
     else:
         lz_launches = 3 * (4 * math.ceil(lz / 4) + 4)
-    per_solve_launches = 20 * calls + lz_launches + 11
+    per_solve_launches = 21 * calls + lz_launches + 11
     secondary = cpcp_secondary(dev, args.seed) if (world == 1 and not args.no_secondary) else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
