@@ -57,9 +57,10 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
     if sumsq == 0.0:
         return None
     opts.validate()
-    # sigma_1(D) by Lanczos on D^T D (pcp.py:100, 114); float32 data only
-    # needs sigma_1 to ~1e-10 (mu0 = 1.25/sigma_1 scales every later mu)
-    lz_tol = LANCZOS_TOL if D.dtype == torch.float64 else 1e-11
+    # sigma_1(D) by Lanczos on D^T D (pcp.py:100, 114).  float32 data only
+    # needs sigma_1 far below its own rounding (6e-8): mu0 = 1.25/sigma_1 scales
+    # every later mu, and a 1e-9 relative error in theta moves mu0 by ~1e-9
+    lz_tol = LANCZOS_TOL if D.dtype == torch.float64 else 1e-9
     be.lanczos_init()
     steps = 0
     # one rank: the whole run is one cooperative kernel; otherwise batches of

@@ -43,7 +43,9 @@ def test_ml_ialm_golden(golden, name, tolrel):
     assert st.converged == bool(g["converged"])
     if st.iter == int(g["iter"]):
         assert st.history[-1].rank_l == int(g["h_rank"][-1])
-        assert np.isclose(st.mu, float(g["mu"]), rtol=1e-12)
+        # mu = rho^k 1.25 / sigma_1(D): FP64 computes sigma_1 to ~1e-15, FP32
+        # to 1e-9 (pcp.py lz_tol; far below the FP32 parity gate of 1e-4)
+        assert np.isclose(st.mu, float(g["mu"]), rtol=1e-12 if "f64" in name else 1e-8)
 
 
 def test_ml_ialm_c1_fp64_vs_oracle(golden):
