@@ -1240,91 +1240,128 @@ __global__ void pcp_jac_skip_done(PcpDev* st) { st->jac_skip = st->done; }
 // value of M_H is <= tau the SVT is zero (pcp.py:258-262: rank = #{sigma >
 // tau} = 0, L_H = 0, nuclear = 0) and the eigenvectors are not needed.  That
 // holds iff tau^2 I - B~ is positive definite, which a Cholesky factorisation
-// decides exactly.  The test uses tau^2 (1 - 1e-10), so a borderline case
-// falls back to the eigensolver.  Cheap exit first: any diagonal entry of B~
-// above tau^2 is a lower bound on lambda_max, so the rank is positive.
-// Two-CTA cluster, columns split by parity, each CTA holding the packed lower
-// part of its columns in shared memory; column k is published through DSMEM.
-// Sets st->jac_skip = done || certified.  (In the reference the first
-// iterations after the start often have rank 0: C2 iterations 2-5.)
-constexpr int R0_THREADS = 1024;
+// decides.  Cheap exit first: any diagonal entry of B~ above tau^2 bounds
+// lambda_max from below, so the rank is positive.  Otherwise the Cholesky of
+// A = tau^2 (1 - 1e-3) I - B~ runs in FP32 in one CTA (packed lower triangle
+// in shared memory): when it succeeds, A + E is PD with |E| <~ n eps_32 tau^2
+// (A's norm is <= tau^2 when B~ <= 2 tau^2; larger B~ fails), far below the
+// 1e-3 tau^2 margin, so lambda_max(B~) < tau^2 and the rank is 0 exactly as
+// the reference counts it.  Borderline cases (lambda_max within 0.1% of
+// tau^2) fail the test and take the eigensolver.  Sets st->jac_skip = done ||
+// certified.  (After the start the reference often has rank 0 for a few
+// iterations: C2 iterations 2-5.)
+constexpr int R0_THREADS = 768, R0_TPT = 3;  // 4x4 register tiles, up to 3 per thread (n_H <= 268)
 
-__host__ __device__ __forceinline__ int64_t r0_off(int t, int n, int c) {  // packed start of local column t
-  return (int64_t)t * (n - c) - (int64_t)t * (t - 1);
-}
 int64_t rank0_smem_bytes(int nh) {
-  const int t1 = (nh + 1) / 2;  // columns of CTA 0 (the larger half)
-  return (r0_off(t1, nh, 0) + 3 * (int64_t)nh) * 8 + 64;
+  const int T = (nh + 3) / 4;
+  return (T * (T + 1) / 2 <= R0_THREADS * R0_TPT) ? 1 : INT_MAX;  // register-resident; smem: l only
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(R0_THREADS)
-pcp_rank0_test(PcpDev* st, const double* __restrict__ Bt, int np, int nh) {
-  extern __shared__ __align__(16) double r0s[];
-  __shared__ int s_flag;  // 0 running, 1 rank > 0 (exit)
-  cg::cluster_group cl = cg::this_cluster();
-  const int c = (int)cl.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = R0_THREADS / 32;
+// Right-looking Cholesky with the lower triangle in 4x4 FP32 register tiles
+// (tile (I, J), I >= J, owned by one thread); per step two barriers: the
+// pivot, then the scaled column l broadcast through shared memory.
+__global__ void __launch_bounds__(R0_THREADS) pcp_rank0_test(PcpDev* st, const double* __restrict__ Bt, int np,
+                                                             int nh) {
+  __shared__ __align__(16) float l[4 * 96];
+  __shared__ float piv;
+  const int tid = threadIdx.x;
   const double tau = st->tau;
-  const double lim = tau * tau * (1.0 - 1e-10);
-  const int done = st->done;
-  const int ncols = (nh - c + 1) / 2;  // local columns j = 2t + c
-  double* col = r0s;                                    // packed lower parts
-  double* lbuf = r0s + r0_off((nh + 1) / 2, nh, 0);     // [2][nh] published column (same offset in both CTAs)
-  double* lloc = lbuf + 2 * (int64_t)nh;                // local copy of the published column
-  if (tid == 0) s_flag = done ? 1 : 0;
-  __syncthreads();
-  // cheap exit: max diagonal > lim  =>  lambda_max > tau^2
-  if (!done) {
-    int big = 0;
-    for (int i = tid; i < nh; i += R0_THREADS) big |= Bt[(int64_t)i * np + i] > lim;
-    if (__syncthreads_or(big) && tid == 0) s_flag = 1;
-    __syncthreads();
-  }
-  if (s_flag) {  // identical decision in both CTAs (same inputs)
-    if (c == 0 && tid == 0) st->jac_skip = done;
+  if (st->done) {
+    if (tid == 0) st->jac_skip = 1;
     return;
   }
-  // load lim I - B~ (lower part of my columns)
-  for (int t = warp; t < ncols; t += nwarps) {
-    const int j = 2 * t + c;
-    double* cj = col + r0_off(t, nh, c);
-    for (int i = j + lane; i < nh; i += 32) cj[i - j] = (i == j ? lim : 0.0) - Bt[(int64_t)i * np + j];
+  // cheap exit: a diagonal entry > tau^2 means lambda_max > tau^2
+  int big = 0;
+  for (int i = tid; i < nh; i += R0_THREADS) big |= Bt[(int64_t)i * np + i] > tau * tau;
+  if (__syncthreads_or(big)) {
+    if (tid == 0) st->jac_skip = 0;
+    return;
   }
-  cl.sync();
-  int fail = 0;
-  for (int k = 0; k < nh; ++k) {
-    const int owner = k & 1, buf = k & 1;
-    if (c == owner) {
-      double* ck = col + r0_off(k >> 1, nh, c);
-      const double d = ck[0];
-      if (!(d > 0.0)) {
-        if (tid == 0) s_flag = 1;
-      } else {
-        const double r = rsqrt(d);
-        for (int i = k + 1 + tid; i < nh; i += R0_THREADS) lbuf[buf * nh + i] = ck[i - k] * r;
+  const double lim = tau * tau * (1.0 - 1e-3);
+  const int T = (nh + 3) / 4, ntiles = T * (T + 1) / 2;
+  float a[R0_TPT][4][4];
+  int ti[R0_TPT], tj[R0_TPT];
+#pragma unroll
+  for (int q = 0; q < R0_TPT; ++q) {
+    int t = tid + q * R0_THREADS, I = 0;
+    if (t >= ntiles) {
+      ti[q] = tj[q] = -1;
+    } else {
+      while (t >= I + 1) {  // row I holds tiles (I, 0..I)
+        t -= I + 1;
+        ++I;
       }
+      ti[q] = I;
+      tj[q] = t;
     }
-    cl.sync();  // column k published (or the owner failed)
-    double* ob = cl.map_shared_rank(lbuf, owner);
-    const int* of = cl.map_shared_rank(&s_flag, owner);
-    if (*of) {
-      fail = 1;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 4 * ti[q] + r, j = 4 * tj[q] + c;
+        a[q][r][c] = (ti[q] >= 0 && i < nh && j < nh && j <= i)
+                         ? (float)((i == j ? lim : 0.0) - Bt[(int64_t)i * np + j])
+                         : (i == j ? 1.f : 0.f);  // padding: identity
+      }
+  }
+  for (int i = tid; i < 4 * 96; i += R0_THREADS) l[i] = 0.f;
+  int ok = 1;
+  const int n4 = 4 * T;
+  for (int k = 0; k < n4; ++k) {
+    const int kt = k >> 2, kr = k & 3;
+    // pivot a_kk (after the owner's update of step k - 1)
+#pragma unroll
+    for (int q = 0; q < R0_TPT; ++q)
+      if (ti[q] == kt && tj[q] == kt) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (r == kr) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (c == kr) piv = a[q][r][c];
+          }
+      }
+    __syncthreads();
+    const float d = piv;
+    if (!(d > 0.f)) {
+      ok = 0;
       break;
     }
-    for (int i = k + 1 + tid; i < nh; i += R0_THREADS) lloc[i] = ob[buf * nh + i];
+    const float rd = rsqrtf(d);
+    // column k below the diagonal, scaled: l_i = a_ik / sqrt(a_kk), i > k
+#pragma unroll
+    for (int q = 0; q < R0_TPT; ++q)
+      if (tj[q] == kt && ti[q] >= kt) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          float v = 0.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c == kr) v = a[q][r][c];
+          const int i = 4 * ti[q] + r;
+          if (i > k) l[i] = v * rd;
+          else if (i == k) l[i] = 0.f;
+        }
+      }
     __syncthreads();
-    // trailing update of my columns j > k: a_ij -= l_i l_j (i >= j)
-    const int t0 = (k + 1 - c + 1) / 2;  // first local column with j > k
-    for (int t = t0 + warp; t < ncols; t += nwarps) {
-      const int j = 2 * t + c;
-      double* cj = col + r0_off(t, nh, c);
-      const double lj = lloc[j];
-      for (int i = j + lane; i < nh; i += 32) cj[i - j] = fma(-lloc[i], lj, cj[i - j]);
-    }
-    __syncthreads();
+    // trailing update a_ij -= l_i l_j for j > k (tiles with J >= kt)
+#pragma unroll
+    for (int q = 0; q < R0_TPT; ++q)
+      if (tj[q] >= kt) {
+        const float4 li = *reinterpret_cast<const float4*>(&l[4 * ti[q]]);
+        const float4 lj = *reinterpret_cast<const float4*>(&l[4 * tj[q]]);
+        const float lr[4] = {li.x, li.y, li.z, li.w}, lc[4] = {lj.x, lj.y, lj.z, lj.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const bool live = tj[q] > kt || c > kr;
+            if (live) a[q][r][c] = fmaf(-lr[r], lc[c], a[q][r][c]);
+          }
+      }
+    // (l_i, i <= k, is zero from step i on; the next barrier orders l and piv reuse)
   }
-  cl.sync();  // no CTA leaves while its shared memory may still be read
-  if (c == 0 && tid == 0) st->jac_skip = fail ? 0 : 1;
+  if (tid == 0) st->jac_skip = ok;
 }
 
 int pcp_rank0(PcpPlan* p, cudaStream_t st) {
@@ -1343,7 +1380,7 @@ int pcp_rank0(PcpPlan* p, cudaStream_t st) {
     return kOk;
   }
   MLR_CUDA(cudaFuncSetAttribute(pcp_rank0_test, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  pcp_rank0_test<<<2, R0_THREADS, smem, st>>>(p->dev, p->Bm, np, nh);
+  pcp_rank0_test<<<1, R0_THREADS, smem, st>>>(p->dev, p->Bm, np, nh);
   MLR_LAUNCH_CHECK("pcp_rank0_test");
   return kOk;
 }
