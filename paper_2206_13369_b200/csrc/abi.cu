@@ -138,6 +138,10 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   p.row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m_local, (int64_t)sms * 8));
   const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64 + 1) / 2;  // symmetric Gram: upper-triangle tiles
   int64_t splits = ceil_div(2 * sms, tiles);
+  if (gram128_ok(ch.np)) {  // blocked Gram (gemm_f64.cu): about one CTA per SM
+    const int64_t b128 = (int64_t)(ch.np / 128) * (ch.np / 128 + 1) / 2;
+    splits = std::max<int64_t>(1, sms / b128);  // one wave (1 CTA per SM: 512 threads x 100 registers)
+  }
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
   {
@@ -214,6 +218,10 @@ static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_
   p.row_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(m_local, (int64_t)sms * 8));
   const int64_t tiles = (int64_t)(ch.np / 64) * (ch.np / 64 + 1) / 2;  // symmetric Gram: upper-triangle tiles
   int64_t splits = ceil_div(2 * sms, tiles);
+  if (gram128_ok(ch.np)) {  // blocked Gram (gemm_f64.cu): about one CTA per SM
+    const int64_t b128 = (int64_t)(ch.np / 128) * (ch.np / 128 + 1) / 2;
+    splits = std::max<int64_t>(1, sms / b128);  // one wave (1 CTA per SM: 512 threads x 100 registers)
+  }
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
   p.cluster = ch.np >= 256 ? 16 : 8;

@@ -27,6 +27,7 @@ struct GemmSpec {
   bool sym;              // C = op(A) op(B) is symmetric (Gram): upper-triangle tiles, mirrored
 };
 int gemm_f64(GemmSpec g, cudaStream_t st);
+bool gram128_ok(int n);  // the blocked Gram kernel handles width n (gemm_f64.cu)
 
 // frame-stack layout (frames.cu)
 int frames_to_matrix(const uint8_t* frames, int count, int H, int W, bool f32, void* x, int64_t ldx, cudaStream_t st);
