@@ -34,7 +34,7 @@ UNIT = "iterations/s"
 
 def _ncu_traffic():
     """dram bytes per launch from the committed ncu --set full capture (profiles/)."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic_c2.json")
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic_c2.json")
     try:
         with open(p) as f:
             return json.load(f)["kernels"]
