@@ -1364,6 +1364,84 @@ __global__ void __launch_bounds__(R0_THREADS) pcp_rank0_test(PcpDev* st, const d
   if (tid == 0) st->jac_skip = ok;
 }
 
+// Large n_H (C5: 1250): the same certificate as a grid-cooperative, panel
+// right-looking FP32 Cholesky of the full matrix (column-major, scratch in
+// the plan's free Gram slices, L2-resident).  Per panel of R0G_B columns:
+// every CTA loads the panel and factors it redundantly in shared memory
+// (identical arithmetic, so every CTA reaches the same verdict), then applies
+// the rank-R0G_B update to the trailing columns it owns (column j on CTA j mod
+// G); one grid barrier per panel.
+constexpr int R0G_B = 8, R0G_T = 256;
+
+__global__ void __launch_bounds__(R0G_T) pcp_rank0_grid(PcpDev* st, const double* __restrict__ Bt, int np, int nh,
+                                                        float* __restrict__ W) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) float pan[];  // [R0G_B][nh]
+  __shared__ int s_big;
+  const int tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
+  const double tau = st->tau;
+  if (st->done) {  // uniform across the grid
+    if (b == 0 && tid == 0) st->jac_skip = 1;
+    return;
+  }
+  if (tid == 0) s_big = 0;
+  __syncthreads();
+  {
+    int big = 0;
+    for (int i = tid; i < nh; i += R0G_T) big |= Bt[(int64_t)i * np + i] > tau * tau;
+    if (__syncthreads_or(big)) {  // same verdict in every CTA (same inputs)
+      if (b == 0 && tid == 0) st->jac_skip = 0;
+      return;
+    }
+  }
+  const float lim = (float)(tau * tau * (1.0 - 1e-3));
+  // W = lim I - B~, lower part, column-major (column j owned by CTA j mod G)
+  for (int j = b; j < nh; j += G)
+    for (int i = j + tid; i < nh; i += R0G_T)
+      W[(int64_t)j * nh + i] = (i == j ? lim : 0.f) - (float)Bt[(int64_t)i * np + j];
+  grid.sync();
+  int ok = 1;
+  for (int k = 0; k < nh; k += R0G_B) {
+    const int nbk = min(R0G_B, nh - k);
+    for (int c = 0; c < nbk; ++c)
+      for (int i = k + tid; i < nh; i += R0G_T) pan[c * nh + i] = W[(int64_t)(k + c) * nh + i];
+    __syncthreads();
+    for (int c = 0; c < nbk; ++c) {  // factor the panel (rows >= k + c of column c)
+      const float d = pan[c * nh + k + c];
+      if (!(d > 0.f)) {
+        ok = 0;
+        break;
+      }
+      const float r = rsqrtf(d);
+      __syncthreads();
+      for (int i = k + c + 1 + tid; i < nh; i += R0G_T) pan[c * nh + i] *= r;
+      __syncthreads();
+      for (int c2 = c + 1; c2 < nbk; ++c2) {
+        const float lj = pan[c * nh + k + c2];
+        for (int i = k + c2 + tid; i < nh; i += R0G_T) pan[c2 * nh + i] = fmaf(-pan[c * nh + i], lj, pan[c2 * nh + i]);
+      }
+      __syncthreads();
+    }
+    if (!ok) break;  // uniform: every CTA factored the same panel
+    // trailing update of my columns j >= k + nbk: a_ij -= sum_c l_ic l_jc
+    const int j0 = k + nbk;
+    for (int j = j0 + ((b - j0 % G) + G) % G; j < nh; j += G) {
+      float lj[R0G_B];
+#pragma unroll
+      for (int c = 0; c < R0G_B; ++c) lj[c] = c < nbk ? pan[c * nh + j] : 0.f;
+      float* wj = W + (int64_t)j * nh;
+      for (int i = j + tid; i < nh; i += R0G_T) {
+        float v = wj[i];
+#pragma unroll
+        for (int c = 0; c < R0G_B; ++c) v = fmaf(-pan[c * nh + i], lj[c], v);
+        wj[i] = v;
+      }
+    }
+    grid.sync();
+  }
+  if (b == 0 && tid == 0) st->jac_skip = ok;
+}
+
 int pcp_rank0(PcpPlan* p, cudaStream_t st) {
   const int nh = p->ch.nh, np = p->ch.np;
   const int64_t smem = rank0_smem_bytes(nh);
@@ -1374,6 +1452,28 @@ int pcp_rank0(PcpPlan* p, cudaStream_t st) {
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   const char* env = getenv("MLR_RANK0_TEST");
+  const size_t gscratch = (size_t)nh * nh * sizeof(float);
+  const size_t gfree = (size_t)p->gram_splits * np * np * sizeof(double);  // Gram slices: free until post
+  if (!(env && env[0] == '0') && smem > max_optin && gscratch <= gfree && nh >= R0G_B) {
+    const size_t psm = (size_t)R0G_B * nh * sizeof(float);
+    static int sms = -1, per = 0;
+    if (sms < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    MLR_CUDA(cudaFuncSetAttribute(pcp_rank0_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    MLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pcp_rank0_grid, R0G_T, psm));
+    if (per >= 1) {
+      PcpDev* dev = p->dev;
+      const double* bm = p->Bm;
+      int npv = np, nhv = nh;
+      float* w = reinterpret_cast<float*>(p->gram_part);
+      void* args[] = {&dev, &bm, &npv, &nhv, &w};
+      MLR_CUDA(cudaLaunchCooperativeKernel((void*)pcp_rank0_grid, dim3(sms), dim3(R0G_T), args, psm, st));
+      return kOk;
+    }
+  }
   if (smem > max_optin || (env && env[0] == '0')) {
     pcp_jac_skip_done<<<1, 1, 0, st>>>(p->dev);
     MLR_LAUNCH_CHECK("pcp_jac_skip_done");
