@@ -114,6 +114,36 @@ __global__ void __launch_bounds__(256) lz_dv_kernel(const LanczosDev* __restrict
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   constexpr int NV = 16 / sizeof(T);
   const bool vec = (n % NV == 0) && (ldd % NV == 0);
+  // FP32, aligned: two rows per warp share every q load (q is re-read from
+  // L1/L2 for each row; halving those reads lifts the pass toward HBM speed)
+  if (sizeof(T) == 4 && vec) {
+    for (int64_t i = w0; i < m; i += 2 * nw) {
+      const bool two = i + nw < m;
+      const T* ra = D + i * ldd;
+      const T* rb = D + (two ? i + nw : i) * ldd;
+      double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+      for (int j = lane * 4; j < n; j += 128) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(ra + j));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(rb + j));
+        const double2 q01 = __ldg(reinterpret_cast<const double2*>(q + j));
+        const double2 q23 = __ldg(reinterpret_cast<const double2*>(q + j + 2));
+        sa0 = fma((double)a.x, q01.x, sa0);
+        sa1 = fma((double)a.y, q01.y, sa1);
+        sa0 = fma((double)a.z, q23.x, sa0);
+        sa1 = fma((double)a.w, q23.y, sa1);
+        sb0 = fma((double)b.x, q01.x, sb0);
+        sb1 = fma((double)b.y, q01.y, sb1);
+        sb0 = fma((double)b.z, q23.x, sb0);
+        sb1 = fma((double)b.w, q23.y, sb1);
+      }
+      const double sa = warp_sum(sa0 + sa1), sb = warp_sum(sb0 + sb1);
+      if (lane == 0) {
+        t[i] = sa;
+        if (two) t[i + nw] = sb;
+      }
+    }
+    return;
+  }
   for (int64_t i = w0; i < m; i += nw) {
     const T* row = D + i * ldd;
     double s0 = 0.0, s1 = 0.0;
@@ -163,6 +193,21 @@ __global__ void __launch_bounds__(256) lz_dtv_kernel(const LanczosDev* __restric
   const bool vec = (j0 + 8 <= n) && (n % NV == 0) && (ldd % NV == 0);
   if (vec) {
     int64_t i = r0;
+    for (; i + 3 < r1; i += 4) {  // four rows in flight
+      T a[4][8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int v = 0; v < 8 / NV; ++v)
+          *reinterpret_cast<float4*>(a[r] + v * NV) =
+              __ldg(reinterpret_cast<const float4*>(D + (i + r) * ldd + j0 + v * NV));
+      double tr[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) tr[r] = __ldg(t + i + r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        acc[e] = fma((double)a[3][e], tr[3], fma((double)a[2][e], tr[2], fma((double)a[1][e], tr[1], fma((double)a[0][e], tr[0], acc[e]))));
+    }
     for (; i + 1 < r1; i += 2) {
       T a[8], b[8];
       const T* ra = D + i * ldd + j0;
