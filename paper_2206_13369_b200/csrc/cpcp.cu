@@ -298,8 +298,8 @@ cp_power_kernel(CpcpDev* __restrict__ st, const double* __restrict__ K, int np, 
   const int R = np / cs;
   extern __shared__ __align__(16) double psm[];
   double* vv = psm;            // np : current v
-  double* kv = vv + np;        // np : K v (full, gathered)
-  double* red = kv + np;       // 64
+  double* kvb = vv + np;       // 2 x np : K v (full, gathered), double-buffered by pass parity
+  double* red = kvb + 2 * np;  // 64
   double* krows = red + 64;    // R x np (optional)
   const int tid = threadIdx.x;
   for (int j = tid; j < np; j += kPowThreads) vv[j] = v[j];
@@ -312,7 +312,11 @@ cp_power_kernel(CpcpDev* __restrict__ st, const double* __restrict__ K, int np, 
   const double rtol = st->rtol;
   const int maxp = st->max_passes;
   for (pass = 1; pass <= maxp; ++pass) {
-    // local rows of K v, pushed to every CTA of the cluster
+    // local rows of K v, pushed to every CTA of the cluster.  kv alternates
+    // between two buffers, so the one cluster barrier per pass also orders
+    // the reuse (a CTA writes this buffer again only two passes later, after
+    // every CTA has passed the barrier that follows its reads)
+    double* kv = kvb + (pass & 1) * np;
     for (int rr = wid; rr < R; rr += nw) {
       const double* krow = rows_in_smem ? krows + (int64_t)rr * np : K + (int64_t)(cr * R + rr) * np;
       double s = 0.0;
@@ -363,7 +367,7 @@ cp_power_kernel(CpcpDev* __restrict__ st, const double* __restrict__ K, int np, 
     }
     const bool stop = fabs(s2 - s2_prev) <= rtol * s2;
     s2_prev = s2;
-    cluster.sync();  // everyone done reading kv before the next pass writes it
+    __syncthreads();  // vv complete before this CTA's next Kv rows read it
     if (stop) break;
   }
   if (pass > maxp) pass = maxp;
@@ -1084,8 +1088,8 @@ int cpcp_lmo(CpcpPlan* p, const double* red, const double* amax_all, double* dot
   const int np = p->ch.np;
   int cs = p->cluster;
   const int R = np / cs;
-  const bool fit = (size_t)R * np * 8 + (2 * np + 64) * 8 <= 200 * 1024;
-  size_t smem = (2 * (size_t)np + 64) * 8 + (fit ? (size_t)R * np * 8 : 0);
+  const bool fit = (size_t)R * np * 8 + (3 * np + 64) * 8 <= 200 * 1024;
+  size_t smem = (3 * (size_t)np + 64) * 8 + (fit ? (size_t)R * np * 8 : 0);
   MLR_CUDA(cudaFuncSetAttribute(cp_power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (cs > 8) MLR_CUDA(cudaFuncSetAttribute(cp_power_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
