@@ -401,3 +401,31 @@ def test_jacobi_eigensolver_vs_lapack(n):
     assert np.abs(lam - ev).max() <= 1e-12 * ev[0]
     assert np.abs(v.T @ v - np.eye(n)).max() <= 1e-12
     assert np.linalg.norm(b @ v - v * lam) <= 1e-11 * np.linalg.norm(b)
+
+
+# --------------------------------------------- rank-0 certificate (pcp.cu)
+@pytest.mark.parametrize("m,n,rank,levels", [(600, 600, 30, 150),     # one-CTA register Cholesky
+                                             (1200, 1200, 60, 300)])  # grid panel Cholesky (n_H > 268)
+def test_rank0_certificate_matches_oracle(m, n, rank, levels):
+    """Iterations whose SVT keeps nothing (rank 0, pcp.py:258-262) skip the
+    eigensolve after the Cholesky certificate; the per-iteration rank column
+    and the iterates must still match the oracle, and the skipped iterations
+    must be exactly the rank-0 ones."""
+    from paper_2206_13369_b200 import pcp as P
+    d, _ = O.gaussian_rpca(m, n, rank, 0.10, 0)
+    ref = O.ml_ialm(d, levels=levels, tol=1e-7)
+    sink = []
+    P.TIMING_SINK = sink
+    try:
+        st = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=levels, tol_feasibility=1e-7))
+    finally:
+        P.TIMING_SINK = None
+    ranks_ref = [h.rank_l for h in ref.history]
+    ranks = [h.rank_l for h in st.history]
+    assert 0 in ranks_ref, "instance has no rank-0 iteration"
+    assert abs(st.iter - ref.iter) <= 1
+    n_cmp = min(len(ranks), len(ranks_ref))
+    assert ranks[:n_cmp] == ranks_ref[:n_cmp]
+    assert relf(st.l, ref.l) <= 1e-10 and relf(st.s, ref.s) <= 1e-10
+    sweeps = sink[0]["jac_sweeps"][:len(ranks)]
+    assert [s == 0 for s in sweeps] == [r == 0 for r in ranks]
