@@ -257,8 +257,12 @@ def main():
 
     # ---- e2e: pinned host D in, host L/S/Y out, through the public API
     d_pin = torch.from_numpy(d_host).pin_memory()
-    for _ in range(max(args.warmup, 3)):  # the pinned result buffers reach their steady state
-        solve(d_pin)
+    st = None
+    for _ in range(max(args.warmup, 3)):
+        # same pattern as the timed loop (the previous result stays alive while
+        # the next solve runs), so torch's pinned host cache holds both result
+        # sets before timing starts instead of growing inside the timed region
+        st = solve(d_pin)
     barrier()
     e2e_ms, e2e_iters = 0.0, 0
     for _ in range(args.steps):
