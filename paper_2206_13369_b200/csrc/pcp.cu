@@ -1280,6 +1280,14 @@ __global__ void eig_permute_kernel(const PcpDev* __restrict__ st, const double* 
 }
 
 __global__ void pcp_jac_skip_done(PcpDev* st) { st->jac_skip = st->done; }
+// Z = 0 on a certified rank-0 iteration (the reconstruction GEMM was skipped)
+__global__ void pcp_zero_if_rank0(const PcpDev* __restrict__ st, uint32_t* __restrict__ z, int64_t n) {
+  if (st->done || !st->jac_skip) return;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < n; i += (int64_t)gridDim.x * blockDim.x * 4) {
+    if (i + 4 <= n && (i & 3) == 0) *reinterpret_cast<uint4*>(z + i) = make_uint4(0u, 0u, 0u, 0u);
+    else for (int64_t q = i; q < n && q < i + 4; ++q) z[q] = 0u;
+  }
+}
 
 // Rank-0 certificate (ahead of the coarse eigensolve).  When every singular
 // value of M_H is <= tau the SVT is zero (pcp.py:258-262: rank = #{sigma >
@@ -1587,7 +1595,10 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
                                &p->dev->nuclear, st))) {
     return rc;
   }
-  // W~ = G^-1 V diag(f) V^T = U' diag(f) V^T with U' = G^-1 V
+  // W~ = G^-1 V diag(f) V^T = U' diag(f) V^T with U' = G^-1 V.  A certified
+  // rank-0 iteration has W~ = 0 and Z = 0: the products are skipped
+  // (jac_skip) and Z is cleared instead.
+  skip = &p->dev->jac_skip;
   if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;
   if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw))) return rc;
   p->timer.end(kPhPost, st);
@@ -1601,6 +1612,10 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
     z.C = p->Z; z.ldc = np; z.c_f32 = p->f32; z.c_slice = 0; z.splits = 1; z.alpha = 1.0;
     z.kscale = nullptr; z.skip = skip;
     if ((rc = gemm_f64(z, st))) return rc;
+    const int64_t zn = p->m_local * np * (p->f32 ? 1 : 2);  // Z as 32-bit words
+    pcp_zero_if_rank0<<<(int)std::min<int64_t>(ceil_div(zn, 1024), 1184), 256, 0, st>>>(
+        p->dev, reinterpret_cast<uint32_t*>(p->Z), zn);
+    MLR_LAUNCH_CHECK("pcp_zero_if_rank0");
   }
   p->timer.end(kPhRecon, st);
   return kOk;
