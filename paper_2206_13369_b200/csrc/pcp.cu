@@ -1507,7 +1507,9 @@ int pcp_rank0(PcpPlan* p, cudaStream_t st) {
   const char* env = getenv("MLR_RANK0_TEST");
   const size_t gscratch = (size_t)nh * nh * sizeof(float);
   const size_t gfree = (size_t)p->gram_splits * np * np * sizeof(double);  // Gram slices: free until post
-  if (!(env && env[0] == '0') && smem > max_optin && gscratch <= gfree && nh >= R0G_B) {
+  const char* genv = getenv("MLR_RANK0_GRID");  // 1: grid version for every n_H, 0: never
+  const bool want_grid = genv ? genv[0] == '1' : smem > max_optin;
+  if (!(env && env[0] == '0') && want_grid && gscratch <= gfree && nh >= R0G_B) {
     const size_t psm = (size_t)R0G_B * nh * sizeof(float);
     static int sms = -1, per = 0;
     if (sms < 0) {
