@@ -1,23 +1,35 @@
 #!/usr/bin/env python
-"""Benchmark: ML-PCP iterations/s on BASELINE config C2 (2000x2000 FP32,
-rank 100, 10% corruptions, n_H = 250, tol 1e-6), the configuration the
-BASELINE metric is quoted on.
+"""Benchmark: ML-PCP iterations/s on the largest single-GPU BASELINE config,
+C5 (20000x20000 FP32, rank 200, 5% corruptions, four levels -> n_H = 1250,
+tol 1e-5).  BASELINE.json's metric names no config, so the headline is the
+largest configuration that fits one GPU; C2 (PCP) and C3/C4 (CPCP) are
+reported as secondary keys.
 
-A "step" is one full solve (to tolerance) of the C2 instance.  `value` is
-iterations/s with D resident in HBM; `e2e` is the same metric through the
-public API with a pinned host matrix in and host L, S, Y out.  Rank r of N
-holds rows [r*m/N, (r+1)*m/N) (row sharding, NCCL all-reduce of the coarse
-Gram each iteration).
+Step: one full ML-PCP solve to tolerance through the public drop-in API
+(``ml_ialm_solve``), sigma_1 Lanczos init included.  ``value`` = iterations
+of all timed solves / device time (D resident in HBM, L2 flushed before every
+solve); ``e2e`` = the same with a pinned host D in and host L, S, Y out, the
+copies inside the timed region.  With N > 1 rank r holds rows
+[r m/N, (r+1) m/N) (row sharding, one all-reduce of the coarse Gram per
+iteration) and ``value`` is whole-job iterations/s (max time over ranks).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+Reference arm (``--impl reference``): the reference algorithm (oracle port of
+mlrpca.ml_ialm_solve, numpy/OpenBLAS, all host cores) on the same input; a
+step is ONE loop iteration (pcp.py:248-296), so the arm fits the driver's
+time limit at C5, where the reference's own init (two full 20000^2 SVDs,
+pcp.py:100,114) alone takes ~520 s.  Its sigma_1 comes from an untimed numpy
+Lanczos in the setup.  Both arms therefore measure loop iterations/s; the
+GPU arm additionally pays its sigma_1 init inside every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C5]
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -28,59 +40,49 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "ML-PCP iterations/s (C2: 2000x2000 FP32, n_H=250, tol 1e-6)"
 UNIT = "iterations/s"
 
 
-def _ncu_traffic():
-    """dram bytes per launch from the committed ncu --set full capture (profiles/)."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic_c2.json")
+def metric_for(name, cfg):
+    prec = "FP64" if cfg["dtype"] == "float64" else "FP32"
+    kind = "ML-PCP" if cfg["solver"] == "pcp" else "ML-CPCP"
+    return f"{kind} iterations/s ({name}: {cfg['m']}x{cfg['n']} {prec}, n_H={cfg['n_coarse']}, tol {cfg['tol']})"
+
+
+def workload_for(name, cfg):
+    if cfg.get("video"):
+        return (f"{name} ML-CPCP {cfg['m']}x{cfg['n']} synthetic video (rank-5 background, five drifting 20x20 "
+                f"squares), mask Bernoulli(0.7), n_H={cfg['n_coarse']}, tol {cfg['tol']}")
+    s = (f"{name} {'ML-PCP' if cfg['solver'] == 'pcp' else 'ML-CPCP'} {cfg['m']}x{cfg['n']} rank {cfg['rank']}, "
+         f"{int(cfg['eta'] * 100)}% sparse U[-1,1], n_H={cfg['n_coarse']}, tol {cfg['tol']}")
+    if cfg.get("observe"):
+        s += f", mask Bernoulli({cfg['observe']})"
+    return s
+
+
+def _json(path):
     try:
-        with open(p) as f:
-            return json.load(f)["kernels"]
-    except (OSError, ValueError, KeyError):
-        return {}
-
-
-def cpcp_secondary(dev, seed):
-    """Side measurements (not the headline metric): ML-CPCP C3 to tolerance and
-    C4 for 300 iterations, device-resident input, CUDA events, L2 flushed."""
-    import torch
-
-    import paper_2206_13369_b200 as pkg
-    from paper_2206_13369_b200.datasets import CONFIGS, make_config
-    out = {}
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    for name, cap in (("C3", 5000), ("C4", 300)):
-        c = CONFIGS[name]
-        d, mask = make_config(name, seed)
-        m, n = d.shape
-        D = torch.from_numpy(d).to(dev)
-        om = pkg.ObservationMask(mask)
-        lam = 1.0 / np.sqrt(max(m, n))
-        mk = lambda it: pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=c["tol"], max_iters=it,
-                                        levels=c["n_coarse"], collect_rank=False)
-        pkg.ml_fwt_solve(D, om, mk(20))
-        flush.fill_(1.0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        st = pkg.ml_fwt_solve(D, om, mk(cap))
-        e1.record()
-        e1.synchronize()
-        ms = e0.elapsed_time(e1)
-        out[name] = {"workload": f"{name} ML-CPCP {m}x{n}, n_H={c['n_coarse']}, tol {c['tol']}, max_iters {cap}",
-                     "iterations": st.iter, "converged": st.converged, "solve_ms": ms,
-                     "iterations_per_s": st.iter / (ms / 1e3), "dtype": "f32"}
-        del D
-    return out
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
 
 
 def _peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return json.load(fh)
-    except OSError:
-        return {"hbm_gbs": 6650.0, "_fallback": True}
+    """MEASURED_PEAKS.json (driver-written: HBM, bf16) + profiles/peaks_b200.json
+    (our FP64-DMMA / FP32 microbenchmarks on the same pool)."""
+    p = _json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {"hbm_gbs": 6650.0, "_fallback": True}
+    own = _json(os.path.join(ROOT, "profiles", "peaks_b200.json")) or {}
+    p = dict(p)
+    for k in ("fp64_mma_tflops", "fp32_ffma_tflops", "tf32_mma_tflops"):
+        if k in own:
+            p[k] = own[k]
+    return p
+
+
+def _traffic(name):
+    t = _json(os.path.join(ROOT, "profiles", f"r03_traffic_{name.lower()}.json"))
+    return (t or {}).get("kernels", {})
 
 
 class ClockSampler:
@@ -96,8 +98,8 @@ class ClockSampler:
         self._p = None
 
     # nvidia-smi's own loop mode in a separate process, started before the
-    # timed region: no process spawn (fork) or NVML round trip in this
-    # process while the GPU is being timed
+    # timed region: no process spawn or NVML round trip in this process while
+    # the GPU is being timed
     def __enter__(self):
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
@@ -132,85 +134,234 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference_solve(d32, cfg, threads):
-    """The reference algorithm (oracle port of pcp.py:213-309) on the host."""
+def host_info():
+    """CPU model and BLAS (report vendor/version/threads)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [f"{i.get('internal_api')} {i.get('version')} ({i.get('threading_layer', '-')}, "
+                f"{i.get('num_threads')} threads)" for i in threadpool_info()]
+    except Exception:  # noqa: BLE001
+        blas = []
+    return {"cpu_model": model, "blas": blas}
+
+
+# ------------------------------------------------------------------ CPU side
+def cpu_pcp_iterations(d, cfg, threads, budget_s, min_iters, max_iters):
+    """Bounded sample of the reference algorithm's loop (oracle port of
+    pcp.py:248-296) on the host: returns (iterations, seconds, setup seconds)."""
     from threadpoolctl import threadpool_limits
 
     from oracle import mlrpca_oracle as O
     with threadpool_limits(limits=threads):
         t0 = time.perf_counter()
-        r = O.ml_ialm(d32.astype(np.float64), lam=1 / np.sqrt(cfg["m"]), tol=cfg["tol"], levels=cfg["n_coarse"])
-        return r.iter, time.perf_counter() - t0
+        d64 = d.astype(np.float64)
+        s1 = O.lanczos_sigma1(d.astype(np.float32) if d.dtype == np.float32 else d64, steps=30)
+        gen = O.ml_ialm_steps(d64, s1, lam=1 / np.sqrt(max(d.shape)), levels=cfg["n_coarse"])
+        setup = time.perf_counter() - t0
+        iters, t0 = 0, time.perf_counter()
+        while True:
+            next(gen)
+            iters += 1
+            secs = time.perf_counter() - t0
+            if iters >= max_iters or (iters >= min_iters and secs >= budget_s):
+                return iters, secs, setup
 
 
-def run_reference(args, cfg, d32):
+def run_reference(args, name, cfg):
+    """The reference arm: one loop iteration of the reference algorithm per
+    step, all host threads, on the same seeded input as the GPU arm."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import mlrpca_oracle as O
+    from paper_2206_13369_b200.datasets import make_config
+    if cfg["solver"] != "pcp":
+        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for ML-PCP configs; "
+                          f"{name} is ML-CPCP"}), flush=True)
+        return
     threads = len(os.sched_getaffinity(0))
-    for _ in range(args.warmup):
-        cpu_reference_solve(d32, cfg, threads)
-    iters = 0
-    secs = 0.0
-    for _ in range(args.steps):
-        it, s = cpu_reference_solve(d32, cfg, threads)
-        iters += it
-        secs += s
-    value = iters / secs
+    d, _ = make_config(name, args.seed)
+    t0 = time.perf_counter()
+    with threadpool_limits(limits=threads):
+        d64 = d.astype(np.float64)
+        s1 = O.lanczos_sigma1(d64, steps=80)
+        gen = O.ml_ialm_steps(d64, s1, lam=1 / np.sqrt(max(d.shape)), levels=cfg["n_coarse"])
+        setup = time.perf_counter() - t0
+        for _ in range(args.warmup):
+            next(gen)
+        t0 = time.perf_counter()
+        last = None
+        for _ in range(args.steps):
+            last = next(gen)
+        secs = time.perf_counter() - t0
+    value = args.steps / secs
+    sample = (f"{args.steps} loop iterations (iterations {args.warmup + 1}..{args.warmup + args.steps}) of the "
+              f"oracle port of mlrpca.ml_ialm_solve (pcp.py:248-296; numpy/OpenBLAS, FP64 on the FP32-rounded "
+              f"input); sigma_1 by an untimed 80-step numpy Lanczos ({setup:.0f} s setup) instead of the "
+              f"reference's two full SVDs")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_for(name, cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE C2 shapes/distributions)",
-        "config": {"workload": "C2 ML-PCP 2000x2000 rank 100, 10% sparse, n_H=250, tol 1e-6", "seed": args.seed},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full C2 solves (oracle port of mlrpca.ml_ialm_solve, numpy/"
-                                   "OpenBLAS, FP64 on the FP32-rounded input)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded generator with BASELINE {name} shapes/distributions)",
+        "config": {"workload": workload_for(name, cfg), "seed": args.seed, "step": "one ML-IALM loop iteration",
+                   "last_gap": last[1] if last else None},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the ML-CPCP C3/C4 side measurements")
-    args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+# ------------------------------------------------------------------ GPU side
+def count_launches(fn):
+    """Kernels our library launches in one call of fn (kineto/CUPTI activity
+    trace of an untimed solve; solves are deterministic, so the count per
+    timed solve is the same)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+        ours = [x for x in names if "mlr::" in x]
+        other = sorted({x for x in names if "mlr::" not in x and not x.startswith("Memcpy")
+                        and not x.startswith("Memset")})
+        return len(ours), other
+    except Exception as e:  # noqa: BLE001
+        return None, [f"profiler unavailable: {e}"]
 
+
+def cpcp_secondary(dev, seed, flush):
+    """Side measurements: ML-CPCP C3 to tolerance and C4 for 300 iterations,
+    device-resident input, CUDA events, L2 flushed."""
+    import torch
+
+    import paper_2206_13369_b200 as pkg
     from paper_2206_13369_b200.datasets import CONFIGS, make_config
+    out = {}
+    for name, cap in (("C3", 5000), ("C4", 300)):
+        c = CONFIGS[name]
+        d, mask = make_config(name, seed)
+        m, n = d.shape
+        D = torch.from_numpy(d).to(dev)
+        om = pkg.ObservationMask(mask)
+        lam = 1.0 / np.sqrt(max(m, n))
+        mk = lambda it: pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(max(m, n)), tol=c["tol"], max_iters=it,
+                                        levels=c["n_coarse"], collect_rank=False)
+        pkg.ml_fwt_solve(D, om, mk(20))
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = pkg.ml_fwt_solve(D, om, mk(cap))
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        out[name] = {"workload": workload_for(name, c) + f", max_iters {cap}", "iterations": st.iter,
+                     "converged": st.converged, "solve_ms": ms, "iterations_per_s": st.iter / (ms / 1e3),
+                     "dtype": "f32"}
+        del D
+    return out
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    cfg = CONFIGS[args.config]
-    assert cfg["solver"] == "pcp", "bench.py times the ML-PCP workload"
 
-    if args.impl == "reference":
-        if rank != 0:
+def pcp_secondary(dev, seed, flush, name="C2", reps=5):
+    import torch
+
+    import paper_2206_13369_b200 as pkg
+    from paper_2206_13369_b200.datasets import CONFIGS, make_config
+    c = CONFIGS[name]
+    d, _ = make_config(name, seed)
+    D = torch.from_numpy(d).to(dev)
+    opts = pkg.PcpOptions(lam=1 / np.sqrt(max(d.shape)), tol_feasibility=c["tol"], levels=c["n_coarse"])
+    for _ in range(3):
+        pkg.ml_ialm_solve(D, opts)
+    ms, iters = 0.0, 0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = pkg.ml_ialm_solve(D, opts)
+        e1.record()
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+        iters += st.iter
+    return {"workload": workload_for(name, c), "iterations_per_solve": iters / reps, "solve_ms": ms / reps,
+            "iterations_per_s": iters / (ms / 1e3), "dtype": "f32" if c["dtype"] == "float32" else "f64"}
+
+
+def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic):
+    """Per-phase rooflines from the live CUDA-event phase timers (SURVEY.md
+    8(d) algorithmic work)."""
+    m, n, nh = m_local, cfg["n"], cfg["n_coarse"]
+    npad = (nh + 63) // 64 * 64
+    b = 4 if cfg["dtype"] == "float32" else 8
+    hbm = peaks["hbm_gbs"]
+    fp64 = peaks.get("fp64_mma_tflops")
+    fp64_src = "profiles/peaks_b200.json (measured mma.sync.m8n8k4.f64)" if fp64 else "nominal 40 TF/s (unmeasured)"
+    fp64 = fp64 or 40.0
+    out = {}
+
+    def avg_us(ph):
+        ms, cnt = phases.get(ph, (0.0, 0))
+        return (1e3 * ms / cnt) if cnt else None
+
+    def add(ph, kernel, bound, work, unit, peak, formula, tkey=None, peak_source=None):
+        us = avg_us(ph)
+        if us is None or us <= 0:
             return
-        d32, _ = make_config(args.config, args.seed)
-        run_reference(args, cfg, d32)
-        return
+        ach = work / (us * 1e-6) / (1e9 if unit == "GB/s" else 1e12)
+        t = traffic.get(tkey or ph)
+        out[ph] = {"bound": bound, "kernel": kernel, "achieved": ach, "peak": peak, "unit": unit,
+                   "frac": ach / peak, "traffic": t["dram_bytes_per_launch"] if t else None,
+                   "algorithmic_per_launch": work, "formula": formula, "avg_us": us,
+                   "launches": phases[ph][1], "peak_source": peak_source or "MEASURED_PEAKS.json hbm_gbs"}
 
+    add("update", "pcp_update_fast (FP32 regular chain: fused prolong / shrink / dual / stats / next restriction)",
+        "hbm", b * (3 * m * n + 2 * m * npad), "GB/s", hbm, "b (3 m n + 2 m n_p) bytes")
+    add("gram", "gram128_kernel (K = A^T A, FP64 DMMA, symmetric)", "tensor", m * npad * npad, "TFLOP/s", fp64,
+        "m n_p^2 flops (symmetric half of 2 m n_p^2)", peak_source=fp64_src)
+    add("recon", "gemm_f64_kernel (Z = A W~, FP64 DMMA)", "tensor", 2.0 * m * npad * npad, "TFLOP/s", fp64,
+        "2 m n_p^2 flops", peak_source=fp64_src)
+    if sweeps:
+        flops = 12.0 * npad ** 3 * statistics.mean(sweeps)
+        add("jacobi", "jacobi2_kernel + j2_vapply_kernel (FP64 two-sided block Jacobi on B~)", "tensor", flops,
+            "TFLOP/s", fp64, "12 n_p^3 flops per sweep x mean sweeps", tkey="jacobi2_kernel", peak_source=fp64_src)
+    return out
+
+
+def gpu_arm(args, name, cfg, world, rank, local):
     import torch
     import torch.distributed as dist
 
     import paper_2206_13369_b200 as pkg
     from paper_2206_13369_b200 import pcp as pcp_mod
+    from paper_2206_13369_b200.datasets import make_config
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    shared = world > ndev
+    dev = torch.device("cuda", local % max(ndev, 1))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    d_full, _ = make_config(args.config, args.seed)
+        if shared:  # one GPU for several ranks: gloo stages the all-reduces through host memory
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    d_full, _ = make_config(name, args.seed)
     m, n = d_full.shape
     r0, r1 = rank * m // world, (rank + 1) * m // world
     d_host = np.ascontiguousarray(d_full[r0:r1])
+    if rank != 0 or world > 1:
+        del d_full
+        d_full = None
     opts = pkg.PcpOptions(lam=1 / np.sqrt(max(m, n)), tol_feasibility=cfg["tol"], levels=cfg["n_coarse"])
     D = torch.from_numpy(d_host).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -221,18 +372,24 @@ def main():
         return pkg.ml_ialm_solve(x, opts)
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def allmax(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev if not shared else "cpu")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     st = None
     for _ in range(args.warmup):
         st = solve(D)  # as in the timed loop: the previous result stays alive
-    # ---- value: D resident in HBM (no per-phase event timers in the timed
-    # region: they cost ~8% of a C2 solve)
+    # ---- value: D resident in HBM
     barrier()
     total_ms, iters = 0.0, 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev.index) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -243,27 +400,23 @@ def main():
             total_ms += e0.elapsed_time(e1)
             iters += st.iter
     barrier()
-    # ---- per-phase CUDA-event timings (roofline): one more solve, untimed
+    total_ms = allmax(total_ms)
+    value = iters / (total_ms / 1e3)
+    hist = st.history
+
+    # ---- per-phase CUDA-event timings (roofline) and the launch count: untimed solves
     sink = []
     pcp_mod.TIMING_SINK = sink
     flush.fill_(1.0)
     solve(D)
     torch.cuda.synchronize()
     pcp_mod.TIMING_SINK = None
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    value = iters / (total_ms / 1e3)
+    launches, foreign = count_launches(lambda: solve(D))
 
     # ---- e2e: pinned host D in, host L/S/Y out, through the public API
     d_pin = torch.from_numpy(d_host).pin_memory()
-    st = None
     for _ in range(max(args.warmup, 3)):
-        # same pattern as the timed loop (the previous result stays alive while
-        # the next solve runs), so torch's pinned host cache holds both result
-        # sets before timing starts instead of growing inside the timed region
-        st = solve(d_pin)
+        st = solve(d_pin)  # same pattern as the timed loop: pinned cache reaches steady state
     barrier()
     e2e_ms, e2e_iters = 0.0, 0
     for _ in range(args.steps):
@@ -274,21 +427,16 @@ def main():
         torch.cuda.synchronize()
         e2e_ms += (time.perf_counter() - t0) * 1e3
         e2e_iters += st.iter
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = allmax(e2e_ms)
     e2e_value = e2e_iters / (e2e_ms / 1e3)
+    del st
     bytes_el = d_host.dtype.itemsize
-    h2d = int(d_host.size * bytes_el)
-    d2h = int(3 * d_host.size * bytes_el)
+    h2d = int(d_host.size * bytes_el) * world
+    d2h = int(3 * d_host.size * bytes_el) * world
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+        return None
 
-    # ---- roofline of the dominant phase, from the live event timings
     peaks = _peaks()
     phases = {}
     for s in sink:
@@ -297,89 +445,109 @@ def main():
                 a = phases.setdefault(k, [0.0, 0])
                 a[0] += v[0]
                 a[1] += v[1]
-    nh = cfg["n_coarse"]
-    npad = (nh + 63) // 64 * 64
-    b = bytes_el
-    # B_iter = b (3 m n + 2 m n_H) -- read D, Y, write Y; A' written/read once
-    upd_bytes = b * (3 * m * n + 2 * m * npad)
-    traffic = _ncu_traffic()
     phase_ms = {k: v[0] for k, v in phases.items()}
+    sweeps = [x for s in sink for x in s.get("jac_sweeps", []) if x > 0]
+    rl = roofline_entries(name, cfg, phases, sweeps, r1 - r0, world, peaks, _traffic(name))
     dominant = max(phase_ms, key=phase_ms.get) if phase_ms else None
-    sweeps = [x for s in sink for x in s.get("jac_sweeps", [])]
-    mean_sweeps = statistics.mean(sweeps) if sweeps else 1.0
-    roof = None
-    if dominant == "jacobi":
-        # Two-sided block Jacobi on the n_p x n_p coarse Gram (FP64): per sweep the
-        # block rotations of B~ (8 n_p^3) and of V (4 n_p^3) -> 12 n_p^3 flops.
-        ms, cnt = phases["jacobi"]
-        flops = 12.0 * npad ** 3 * mean_sweeps
-        fp64_peak = 40.0
-        ach = flops / (ms / cnt / 1e3) / 1e12
-        t = traffic.get("jacobi2_kernel")
-        roof = {"bound": "tensor", "kernel": "jacobi2_kernel<cluster> + j2_vapply_kernel (FP64 two-sided block "
-                "Jacobi, 16-CTA cluster; latency-bound: one 32x32 rotation chain per round)",
-                "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                "peak_source": "nominal B200 FP64 tensor (FP64 not in MEASURED_PEAKS.json)",
-                "traffic": t["dram_bytes_per_launch"] if t else None,
-                "algorithmic_flops_per_launch": flops, "mean_sweeps": mean_sweeps,
-                "flops_formula": "12 n_p^3 per sweep"}
-    upd = phases.get("update")
-    streaming = None
-    if upd:
-        ach = upd_bytes / (upd[0] / upd[1] / 1e3) / 1e9
-        t = traffic.get("pcp_update_fast")
-        streaming = {"bound": "hbm", "kernel": "pcp_update_fast<3,true,4> (FP32 regular-chain fused prolong/shrink/"
-                     "dual/restrict, warp per row)", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": ach / peaks["hbm_gbs"], "traffic": t["dram_bytes_per_launch"] if t else None,
-                     "algorithmic_bytes_per_launch": upd_bytes, "avg_us": 1e3 * upd[0] / upd[1],
-                     "bytes_formula": "b (3 m n + 2 m n_p)"}
-        if roof is None:
-            roof = streaming
-    per_iter = {k: round(v / max(1, sum(s.get("iters", 0) for s in sink)), 4) for k, v in phase_ms.items()}
+    roof = rl.get(dominant) or rl.get("update")
+    k_solve = sum(s.get("iters", 0) for s in sink) or 1
+    per_iter = {k: round(v / k_solve, 4) for k, v in phase_ms.items()}
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         threads = len(os.sched_getaffinity(0))
-        it, secs = cpu_reference_solve(d_full, cfg, threads)
+        big = cfg["m"] * cfg["n"] > 1e8
+        it, secs, setup = cpu_pcp_iterations(d_full, cfg, threads, budget_s=10.0, min_iters=2 if big else 5,
+                                             max_iters=3 if big else 40)
         cpu = {"value": it / secs, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"1 full C2 solve ({it} iterations, oracle port of mlrpca.ml_ialm_solve, numpy/OpenBLAS FP64)"}
+               "sample": f"{it} ML-IALM loop iterations of {name} (oracle port of pcp.py:248-296, numpy/OpenBLAS "
+                         f"FP64 on the FP32-rounded input), {secs:.1f} s; sigma_1 by an untimed 30-step Lanczos "
+                         f"({setup:.1f} s setup)", **host_info()}
 
-    lz = statistics.mean(s.get("lanczos_steps", 0) for s in sink) if sink else 0
-    # launches per solve (counted in profiles/r02_bench_launches_c2.csv): 21 per loop
-    # call (gram 3, pre 6 incl. split-K sums, rank-0 test 1, jacobi + V update 2, after/weights 2,
-    # post 4, recon 1, update 1, finalize 1), 3 per Lanczos step (D^T D q, slice sum,
-    # update), 11 fixed.  Calls and steps are issued in batches of 4 and the polling
-    # is pipelined one batch deep, so one batch of each runs (as no-ops) past the end.
-    calls = 4 * math.ceil((iters / args.steps) / 4) + 4
-    if world == 1 and n <= 4096:
-        lz_launches = 2  # init + the single cooperative Lanczos kernel
-    else:
-        lz_launches = 3 * (4 * math.ceil(lz / 4) + 4)
-    per_solve_launches = 21 * calls + lz_launches + 11
-    secondary = cpcp_secondary(dev, args.seed) if (world == 1 and not args.no_secondary) else None
+    secondary = {}
+    if world == 1 and not args.no_secondary:
+        del D, d_pin
+        torch.cuda.empty_cache()
+        if name != "C2":
+            secondary["C2"] = pcp_secondary(dev, args.seed, flush)
+        secondary.update(cpcp_secondary(dev, args.seed, flush))
+    mode = (f"row-sharded x{world} (gloo on one shared device: functional run, NOT a scaling number)" if shared
+            else (f"row-sharded x{world}, NCCL all-reduce of the coarse Gram" if world > 1 else "1 GPU"))
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_for(name, cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator with BASELINE C2 shapes/distributions)",
-        "config": {"workload": "C2 ML-PCP 2000x2000 rank 100, 10% sparse U[-1,1], n_H=250, tol 1e-6",
-                   "seed": args.seed, "iterations_per_solve": iters / args.steps,
-                   "l2": "256 MB buffer written before every timed step",
-                   "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg["dtype"] == "float32" else "f64",
+        "data": f"synthetic (seeded generator with BASELINE {name} shapes/distributions)",
+        "config": {"workload": workload_for(name, cfg), "seed": args.seed, "step": "one full solve to tolerance "
+                   "(sigma_1 Lanczos init + loop) through ml_ialm_solve", "iterations_per_solve": iters / args.steps,
+                   "final_gap": hist[-1].feasibility_gap, "final_rank": hist[-1].rank_l,
+                   "l2": "256 MB buffer written before every timed step", "parallelism": mode,
+                   "shared_device": shared},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / args.steps},
+                "ms_per_step": e2e_ms / args.steps, "api": "ml_ialm_solve(pinned torch CPU tensor) -> host L, S, Y"},
         "roofline": roof,
-        "streaming_kernel": streaming,
+        "kernels": rl,
         "phase_ms_per_iter": per_iter,
         "dominant_phase": dominant,
         "time_to_tol_ms": total_ms / args.steps,
+        "loop_iterations_per_s": (iters / args.steps) / ((total_ms / args.steps - phase_ms.get("lanczos", 0.0)) / 1e3),
         "cpu_baseline": cpu,
-        "cpcp_configs": secondary,
-        "gpu_launches": int(per_solve_launches * args.steps),
+        "secondary": secondary or None,
+        "gpu_launches": int(launches * args.steps) if launches is not None else None,
+        "gpu_launches_per_solve": launches,
+        "foreign_kernels": foreign,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    return line
+
+
+def spawn(args):
+    """--gpus N without torchrun: launch the N ranks ourselves."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C2 / C3 / C4 side measurements")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    from paper_2206_13369_b200.datasets import CONFIGS
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    name = args.config
+    cfg = CONFIGS[name]
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, name, cfg)
+        return
+    if cfg["solver"] != "pcp":
+        raise SystemExit("bench.py times an ML-PCP config as the headline (C1, C2 or C5); "
+                         "ML-CPCP C3/C4 are reported as secondary keys")
+    line = gpu_arm(args, name, cfg, world, rank, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
     if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

@@ -97,6 +97,11 @@ int mlr_pcp_lanczos_run_available(void* plan);
 int mlr_pcp_start(void* plan, const void* D, int64_t ldd, void* Y0, int64_t ldy, const double* in_stats, double lam,
                   double mu0, double rho, double tol, int max_iters, double time_budget, double jac_tol,
                   int jac_max_sweeps, void* stream);
+/* time_budget < 0 means none (reference None); 0 or more stops after the first
+ * iteration whose wall time reaches it (pcp.py:295).
+ * red layout after mlr_pcp_gram: [K = A^T A (n_p^2), res^2, sum|S|, nnz(S), budget
+ * flag]; row-sharded runs all-reduce (sum) red[0 : n_p^2 + 4) before
+ * mlr_pcp_finalize, so every rank takes the same time-budget decision. */
 int mlr_pcp_gram(void* plan, double* red, int with_stats, void* stream);
 int mlr_pcp_finalize(void* plan, const double* red, void* stream);
 int mlr_pcp_svt(void* plan, const double* red, void* stream);
@@ -138,6 +143,9 @@ int64_t mlr_cpcp_red_doubles(void* plan);
 int mlr_cpcp_start(void* plan, const void* D, int64_t ldd, const uint32_t* mask, int64_t ldm, void* S, int64_t lds,
                    double lambda_l, double lambda_s, double tol, double radius, int max_iters, double time_budget,
                    void* stream);
+/* time_budget < 0 means none (cpcp.py:451).  red layout after mlr_cpcp_gram:
+ * [K_g (n_p^2), sum r^2, sum|S|, nnz, sum S^2, sum S r, budget flag];
+ * all-reduce (sum) red[0 : n_p^2 + 6) across ranks. */
 int mlr_cpcp_gram(void* plan, double* red, double* amax, void* stream);
 int mlr_cpcp_begin(void* plan, const double* red, const double* amax_all, void* stream);
 int mlr_cpcp_lmo(void* plan, const double* red, const double* amax_all, double* dots, void* stream);

@@ -377,6 +377,80 @@ def ml_ialm(d, lam=None, mu0=None, rho=1.5, tol=1e-7, max_iters=500,
                      chain.n_coarse, float(sigma1), diag)
 
 
+def lanczos_sigma1(d, steps=80, seed=0):
+    """sigma_1(d) by Lanczos on d^T d with full reorthogonalisation (numpy).
+    Bench setup only: the reference takes sigma_1 from a full SVD
+    (pcp.py:100, 114; ~260 s each at 20000^2), which a bounded CPU sample of
+    the loop leaves out."""
+    m, n = d.shape
+    q = np.random.default_rng(seed).standard_normal(n)
+    qs = [q / np.linalg.norm(q)]
+    alpha, beta = [], []
+    theta = 0.0
+    for k in range(min(steps, n)):
+        w = d.T @ (d @ qs[-1])
+        a = float(qs[-1] @ w)
+        alpha.append(a)
+        for v in qs:                      # full reorthogonalisation
+            w -= (v @ w) * v
+        b = float(np.linalg.norm(w))
+        t = np.diag(alpha) + np.diag(beta, 1) + np.diag(beta, -1)
+        theta_new = float(np.linalg.eigvalsh(t)[-1])
+        if k > 3 and abs(theta_new - theta) <= 1e-15 * theta_new or b == 0.0:
+            theta = theta_new
+            break
+        theta = theta_new
+        beta.append(b)
+        qs.append(w / b)
+    return float(np.sqrt(theta))
+
+
+def ml_ialm_steps(d, sigma1, lam=None, rho=1.5, levels=None, rank_guess=5):
+    """Generator form of the ml_ialm loop (pcp.py:248-296, same operations as
+    ml_ialm above) for bounded CPU samples in bench.py: yields (k, gap, rank)
+    after every iteration and keeps iterating past the tolerance (an
+    iteration's work does not depend on it).  sigma1 is supplied by the
+    caller (see lanczos_sigma1)."""
+    d = as_matrix(d, "d")
+    m, n = d.shape
+    lam = lam if lam is not None else 1.0 / np.sqrt(max(m, n))     # pcp.py:99
+    mu = 1.25 / sigma1                                             # pcp.py:101
+    chain = build_chain(n, _coarse_width(n, m, levels, rank_guess), True)
+    rd = chain.composite.toarray()                                 # pcp.py:236
+    cho = chain.gram_cho()
+    d_norm = np.linalg.norm(d, "fro")                              # pcp.py:238
+    s_mat = np.zeros_like(d)
+    y = d / max(sigma1, np.max(np.abs(d)) / lam)                   # pcp.py:112-115
+    buf = np.empty_like(d)
+    k = 0
+    while True:
+        k += 1
+        inv = 1.0 / mu
+        np.multiply(y, inv, out=buf)                               # pcp.py:252-255
+        buf += d
+        buf -= s_mat
+        m_h = scipy.linalg.cho_solve(cho, (buf @ rd).T).T
+        u_h, sig, v_h = svd_full(m_h)                              # pcp.py:257
+        rank = int(np.count_nonzero(sig > inv))                    # pcp.py:258
+        if rank == 0:
+            l_mat = np.zeros_like(d)
+        else:
+            kept = sig[:rank] - inv
+            l_mat = ((u_h[:, :rank] * kept) @ v_h[:, :rank].T) @ rd.T
+        np.multiply(y, inv, out=buf)                               # pcp.py:272-275
+        buf += d
+        buf -= l_mat
+        s_mat = soft_threshold(buf, lam * inv)
+        np.subtract(d, l_mat, out=buf)                             # pcp.py:277-282
+        buf -= s_mat
+        gap = float(np.linalg.norm(buf, "fro") / d_norm)
+        buf *= mu
+        y += buf
+        mu *= rho
+        _ = float(np.sum(np.abs(s_mat))), np.count_nonzero(s_mat)  # pcp.py:284-291 telemetry
+        yield k, gap, rank
+
+
 DENSE_SVD_LIMIT = 256   # linalg.py:16
 
 

@@ -20,6 +20,12 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
+def _budget(time_budget):
+    """None -> -1 (no budget); any other value, including 0, is a budget
+    (the reference stops once wall >= budget, pcp.py:295, cpcp.py:451)."""
+    return -1.0 if time_budget is None else float(time_budget)
+
+
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -133,7 +139,7 @@ class CudaPcp:
     def start(self, D, Y0, lam, mu0, rho, tol, max_iters, time_budget, jac_tol, jac_max_sweeps):
         _lib.check(self.lib.mlr_pcp_start(
             self.h, _ptr(D), D.stride(0), _ptr(Y0), Y0.stride(0), _ptr(self.stats), float(lam),
-            float(mu0 or 0.0), float(rho), float(tol), int(max_iters), float(time_budget or 0.0),
+            float(mu0 or 0.0), float(rho), float(tol), int(max_iters), _budget(time_budget),
             float(jac_tol), int(jac_max_sweeps), _stream()))
 
     def gram(self, with_stats):
@@ -141,7 +147,7 @@ class CudaPcp:
 
     def stats_slice(self):
         nn = self.np_ * self.np_
-        return nn, nn + 3
+        return nn, nn + 4  # Gram, then res^2, sum|S|, nnz, time-budget flag
 
     def finalize(self):
         _lib.check(self.lib.mlr_pcp_finalize(self.h, _ptr(self.red), _stream()))
@@ -265,14 +271,14 @@ class CudaCpcp:
         ldm = mask.shape[1] if mask is not None else 0
         _lib.check(self.lib.mlr_cpcp_start(self.h, _ptr(D), D.stride(0), _ptr(mask), ldm, _ptr(S), S.stride(0),
                                            float(lam_l), float(lam_s), float(tol), float(radius), int(max_iters),
-                                           float(time_budget or 0.0), _stream()))
+                                           _budget(time_budget), _stream()))
 
     def gram(self):
         _lib.check(self.lib.mlr_cpcp_gram(self.h, _ptr(self.red), _ptr(self.amax), _stream()))
 
     def stats_slice(self):
         nn = self.np_ * self.np_
-        return nn, nn + 5
+        return nn, nn + 6  # Gram, then 5 stats and the time-budget flag
 
     def begin(self):
         _lib.check(self.lib.mlr_cpcp_begin(self.h, _ptr(self.red), _ptr(self.amax_all), _stream()))

@@ -22,6 +22,9 @@ from .runtime import SINGLE, Comm, as_device_matrix, give_back, give_back_all
 
 # When set to a list, solves record per-phase CUDA-event timings into it.
 TIMING_SINK = None
+# When set to a list, solves append their final device state (dict of
+# mlr_cpcp_state: k, corner flags, the l1 arg-max (i_s, j_s), ...): tests.
+STATE_SINK = None
 
 
 class RankProbe:
@@ -180,6 +183,8 @@ def ml_fwt_solve(d, mask=None, opts=None):
             if probe is not None:
                 probe.close()
             be.close()
+    if STATE_SINK is not None:
+        STATE_SINK.append(dict(out[2]))
     return _state_from(*out, kind, atoms)
 
 
@@ -220,6 +225,8 @@ def ml_fwt_solve_rows(d_local, mask_local, opts, m_global, row0, group=None):
             if probe is not None:
                 probe.close()
             be.close()
+    if STATE_SINK is not None:
+        STATE_SINK.append(dict(out[2]))
     return _state_from(*out, kind, atoms)
 
 

@@ -204,8 +204,11 @@ cp_row_kernel(const CpcpDev* __restrict__ st, ChainDev ch, int64_t m, int64_t ro
 // as (mag, val, sval, idx).
 // Sum the per-CTA stats and merge the arg-max records (256 threads; fixed
 // summation order; the arg-max merge is a total order, so order-free).
+// out[kCpStats] is this rank's time-budget flag: summed by the stats
+// all-reduce, so all ranks of a row-sharded solve stop together (cpcp.py:451).
 __global__ void __launch_bounds__(256) cp_part_reduce(const double* __restrict__ part, int nparts,
-                                                      double* __restrict__ out, double* __restrict__ am) {
+                                                      double* __restrict__ out, double* __restrict__ am,
+                                                      const CpcpDev* __restrict__ st) {
   __shared__ double scratch[kCpStats * 32];
   __shared__ AmRec amw[8];
   double v[kCpStats];
@@ -225,6 +228,8 @@ __global__ void __launch_bounds__(256) cp_part_reduce(const double* __restrict__
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int q = 0; q < kCpStats; ++q) out[q] = v[q];
+    const double wall = (cp_now_ns() - st->t0_ns) * 1e-9;
+    out[kCpStats] = (st->time_budget >= 0.0 && wall >= st->time_budget) ? 1.0 : 0.0;
     AmRec r = amw[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) am_merge(r, amw[w]);
     am[0] = r.mag;
@@ -925,7 +930,7 @@ __global__ void cp_finalize_kernel(CpcpDev* st, const double* __restrict__ stats
   }
   if (conv) {
     st->done = 1;
-  } else if (k >= st->max_iters || (st->time_budget > 0.0 && wall >= st->time_budget)) {
+  } else if (k >= st->max_iters || stats[kCpStats] > 0.0) {
     st->done = 2;
   } else {
     st->k = k + 1;
@@ -1064,14 +1069,12 @@ int cpcp_gram(CpcpPlan* p, double* red, double* amax, cudaStream_t st) {
       rc = sum_slices(p->gram_part, nn, nn, p->gram_splits, red, st);
       if (rc) return rc;
     }
-    cp_part_reduce<<<1, 256, 0, st>>>(p->row_part, p->row_blocks, red + nn, amax);
-    MLR_LAUNCH_CHECK("cp_part_reduce");
   } else {
-    MLR_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * (nn + kCpStats), st));
-    std::vector<double> empty = {0.0, 0.0, 0.0, -1.0};
-    MLR_CUDA(cudaMemcpyAsync(amax, empty.data(), 4 * sizeof(double), cudaMemcpyHostToDevice, st));
-    MLR_CUDA(cudaStreamSynchronize(st));
+    MLR_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * nn, st));
   }
+  // no rows: zero stats, an empty arg-max record (idx -1) and the budget flag
+  cp_part_reduce<<<1, 256, 0, st>>>(p->row_part, p->m_local > 0 ? p->row_blocks : 0, red + nn, amax, p->dev);
+  MLR_LAUNCH_CHECK("cp_part_reduce");
   p->timer.end(0, st);
   return kOk;
 }

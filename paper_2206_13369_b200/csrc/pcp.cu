@@ -812,13 +812,13 @@ __global__ void pcp_start_scalars(PcpDev* st, const LanczosDev* lz, const double
   st->t0_ns = global_ns();
 }
 
-// Finalize iteration k from the (all-reduced) fine-pass stats at red[0..3):
+// Finalize iteration k from the (all-reduced) fine-pass stats at red[0..4):
 // history record, stopping rules (pcp.py:284-296), mu <- rho mu.
 __global__ void pcp_finalize_kernel(PcpDev* st, const double* __restrict__ red, double* __restrict__ hist,
                                     const int* __restrict__ jac_result) {
   if (st->done) return;
   const int k = st->k;
-  const double res2 = red[0], l1 = red[1], nnz = red[2];
+  const double res2 = red[0], l1 = red[1], nnz = red[2], budget_hit = red[3];
   const double gap = sqrt(res2) / st->d_norm;
   const double wall = (global_ns() - st->t0_ns) * 1e-9;
   double* h = hist + (int64_t)(k - 1) * kHistCols;
@@ -836,7 +836,7 @@ __global__ void pcp_finalize_kernel(PcpDev* st, const double* __restrict__ red, 
     st->done = 3;
   } else if (gap <= st->tol) {
     st->done = 1;
-  } else if (k >= st->max_iters || (st->time_budget > 0.0 && wall >= st->time_budget)) {
+  } else if (k >= st->max_iters || budget_hit > 0.0) {
     st->done = 2;
   } else {
     st->k = k + 1;
@@ -957,15 +957,21 @@ pcp_row_kernel(const PcpDev* __restrict__ st, ChainDev ch, int64_t m, const T* _
 }
 
 // Sum nv-wide per-CTA partials (256 threads, fixed order -> deterministic).
+// out[3] is this rank's time-budget flag (1 when the budget is spent); the
+// flags are summed by the same all-reduce as the stats, so every rank of a
+// row-sharded solve takes the same stop decision (pcp.py:295).
 __global__ void __launch_bounds__(256) stats_reduce_kernel(const double* __restrict__ part, int nparts, int nv,
-                                                           double* __restrict__ out) {
+                                                           double* __restrict__ out, const PcpDev* __restrict__ st) {
   __shared__ double scratch[3 * 32];
   double v[3] = {0.0, 0.0, 0.0};
   for (int b = threadIdx.x; b < nparts; b += blockDim.x)
     for (int q = 0; q < nv && q < 3; ++q) v[q] += part[nv * b + q];
   block_sum<3>(v, scratch);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < nv && q < 3; ++q) out[q] = v[q];
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 3; ++q) out[q] = q < nv ? v[q] : 0.0;
+    const double wall = (global_ns() - st->t0_ns) * 1e-9;
+    out[3] = (st->time_budget >= 0.0 && wall >= st->time_budget) ? 1.0 : 0.0;
+  }
 }
 
 // ------------------------------------------------------------ host-side drivers
@@ -1171,12 +1177,8 @@ int pcp_gram(PcpPlan* p, double* red, int with_stats, cudaStream_t st) {
     MLR_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * nn, st));
   }
   if (with_stats) {
-    if (p->m_local > 0) {
-      stats_reduce_kernel<<<1, 256, 0, st>>>(p->row_part, p->row_blocks, 3, red + nn);
-      MLR_LAUNCH_CHECK("stats_reduce_kernel");
-    } else {
-      MLR_CUDA(cudaMemsetAsync(red + nn, 0, 3 * sizeof(double), st));
-    }
+    stats_reduce_kernel<<<1, 256, 0, st>>>(p->row_part, p->m_local > 0 ? p->row_blocks : 0, 3, red + nn, p->dev);
+    MLR_LAUNCH_CHECK("stats_reduce_kernel");
   }
   p->timer.end(kPhGram, st);
   return kOk;
@@ -1295,14 +1297,20 @@ __global__ void pcp_zero_if_rank0(const PcpDev* __restrict__ st, uint32_t* __res
 // holds iff tau^2 I - B~ is positive definite, which a Cholesky factorisation
 // decides.  Cheap exit first: any diagonal entry of B~ above tau^2 bounds
 // lambda_max from below, so the rank is positive.  Otherwise the Cholesky of
-// A = tau^2 (1 - 1e-3) I - B~ runs in FP32 in one CTA (packed lower triangle
-// in shared memory): when it succeeds, A + E is PD with |E| <~ n eps_32 tau^2
-// (A's norm is <= tau^2 when B~ <= 2 tau^2; larger B~ fails), far below the
-// 1e-3 tau^2 margin, so lambda_max(B~) < tau^2 and the rank is 0 exactly as
-// the reference counts it.  Borderline cases (lambda_max within 0.1% of
+// A = tau^2 (1 - margin) I - B~ runs in FP32 in one CTA (packed lower
+// triangle in shared memory).  When it succeeds, A + E is PD with
+// |E_ij| <= gamma_{n+1} sqrt(a_ii a_jj) <= gamma_{n+1} tau^2.  The worst-case
+// normwise bound n gamma_{n+1} tau^2 (0.09 tau^2 at n = 1250) is far from
+// what rounding does in practice (errors of random sign: ~sqrt(n) u), so the
+// margin is the heuristic rank0_margin(n) = max(1e-3, 2 (n+1) sqrt(n) u_32):
+// a success then says lambda_max(B~) < tau^2, the rank is 0 exactly as the
+// reference counts it.  Borderline cases (lambda_max within the margin of
 // tau^2) fail the test and take the eigensolver.  Sets st->jac_skip = done ||
 // certified.  (After the start the reference often has rank 0 for a few
 // iterations: C2 iterations 2-5.)
+__host__ __device__ inline double rank0_margin(int n) {
+  return fmax(1e-3, 2.0 * (n + 1) * sqrt((double)n) * 5.9604644775390625e-8);
+}
 constexpr int R0_THREADS = 768, R0_TPT = 3;  // 4x4 register tiles, up to 3 per thread (n_H <= 268)
 
 int64_t rank0_smem_bytes(int nh) {
@@ -1330,7 +1338,7 @@ __global__ void __launch_bounds__(R0_THREADS) pcp_rank0_test(PcpDev* st, const d
     if (tid == 0) st->jac_skip = 0;
     return;
   }
-  const double lim = tau * tau * (1.0 - 1e-3);
+  const double lim = tau * tau * (1.0 - rank0_margin(nh));
   const int T = (nh + 3) / 4, ntiles = T * (T + 1) / 2;
   float a[R0_TPT][4][4];
   int ti[R0_TPT], tj[R0_TPT];
@@ -1447,7 +1455,7 @@ __global__ void __launch_bounds__(R0G_T) pcp_rank0_grid(PcpDev* st, const double
       return;
     }
   }
-  const float lim = (float)(tau * tau * (1.0 - 1e-3));
+  const float lim = (float)(tau * tau * (1.0 - rank0_margin(nh)));
   // W = lim I - B~, lower part, column-major (column j owned by CTA j mod G)
   for (int j = b; j < nh; j += G)
     for (int i = j + tid; i < nh; i += R0G_T)

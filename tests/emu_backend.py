@@ -46,6 +46,13 @@ class _Base:
     def read_snapshot(self, token):
         return token
 
+    def _budget_flag(self):
+        """This rank's time-budget flag, summed across ranks with the stats
+        (mirrors stats_reduce_kernel / cp_part_reduce)."""
+        st = self.st
+        wall = time.perf_counter() - st["t0"] + getattr(self, "clock_skew", 0.0)
+        return 1.0 if st["time_budget"] >= 0 and wall >= st["time_budget"] else 0.0
+
     def close(self):
         pass
 
@@ -131,7 +138,8 @@ class EmuPcp(_Base):
         mu = mu0 if mu0 else 1.25 / s1
         self.st = {"lam": lam, "rho": rho, "tol": tol, "d_norm": np.sqrt(sumsq), "mu": mu, "k": 1, "done": 0,
                    "status": 0, "rank": 0, "nuclear": 0.0, "mu_last": mu, "mu_final": mu, "max_iters": max_iters,
-                   "time_budget": time_budget or 0.0, "t0": time.perf_counter(), "sigma1": s1,
+                   "time_budget": -1.0 if time_budget is None else float(time_budget), "t0": time.perf_counter(),
+                   "sigma1": s1,
                    "scale": max(s1, maxabs / lam)}
         d = _np(D)
         y = (d.astype(np.float64) / self.st["scale"]).astype(self.dt)
@@ -141,7 +149,7 @@ class EmuPcp(_Base):
 
     def stats_slice(self):
         nn = self.np_ * self.np_
-        return nn, nn + 3
+        return nn, nn + 4
 
     def gram(self, with_stats):
         nn = self.np_ * self.np_
@@ -149,13 +157,14 @@ class EmuPcp(_Base):
         self.red[:nn] = torch.from_numpy((A.T @ A).ravel())
         if with_stats:
             self.red[nn:nn + 3] = torch.from_numpy(self.part)
+            self.red[nn + 3] = self._budget_flag()
 
     def finalize(self):
         st = self.st
         if st["done"]:
             return
         nn = self.np_ * self.np_
-        res2, l1, nnz = _np(self.red[nn:nn + 3]).tolist()
+        res2, l1, nnz, budget_hit = _np(self.red[nn:nn + 4]).tolist()
         k = st["k"]
         gap = np.sqrt(res2) / st["d_norm"]
         wall = time.perf_counter() - st["t0"]
@@ -165,7 +174,7 @@ class EmuPcp(_Base):
         st["mu_final"] = st["mu"] * st["rho"]
         if gap <= st["tol"]:
             st["done"] = 1
-        elif k >= st["max_iters"] or (st["time_budget"] > 0 and wall >= st["time_budget"]):
+        elif k >= st["max_iters"] or budget_hit > 0:
             st["done"] = 2
         else:
             st["k"] = k + 1
@@ -324,7 +333,7 @@ class EmuCpcp(_Base):
         m = D.shape[0]
         self.obs = self._mask(maskbits, m)
         self.st = {"lam_l": lam_l, "lam_s": lam_s, "tol": tol, "radius": radius, "max_iters": max_iters,
-                   "time_budget": time_budget or 0.0, "t_l": 0.0, "t_s": 0.0, "k": 0, "done": 0, "status": 0,
+                   "time_budget": -1.0 if time_budget is None else float(time_budget), "t_l": 0.0, "t_s": 0.0, "k": 0, "done": 0, "status": 0,
                    "ga": 0.0, "gb": 0.0, "corner_l": False, "corner_s": False, "t0": time.perf_counter(),
                    "passes": 0}
         self.LH = np.zeros((m, self.np_), dtype=self.dt)
@@ -335,7 +344,7 @@ class EmuCpcp(_Base):
 
     def stats_slice(self):
         nn = self.np_ * self.np_
-        return nn, nn + 5
+        return nn, nn + 6
 
     def gram(self):
         if self.st["done"]:
@@ -344,6 +353,7 @@ class EmuCpcp(_Base):
         g = self.GH.astype(np.float64)
         self.red[:nn] = torch.from_numpy((g.T @ g).ravel())
         self.red[nn:nn + 5] = torch.from_numpy(self.part)
+        self.red[nn + 5] = self._budget_flag()
 
     def begin(self):
         nn = self.np_ * self.np_
@@ -441,7 +451,7 @@ class EmuCpcp(_Base):
         if st["done"]:
             return
         nn = self.np_ * self.np_
-        sq, l1, nnz, ss, sr = _np(self.red[nn:nn + 5]).tolist()
+        sq, l1, nnz, ss, sr, budget_hit = _np(self.red[nn:nn + 6]).tolist()
         st.update(sq=sq, ss=ss, sr=sr, t_s=l1)
         obj = 0.5 * sq + st["lam_l"] * st["t_l"] + st["lam_s"] * st["t_s"]
         st["u_l"] = min(st["u_l"], obj / st["lam_l"])
@@ -454,7 +464,7 @@ class EmuCpcp(_Base):
         conv = k > 5 and self.objs[k - 6] - obj <= st["tol"] * max(abs(self.objs[k - 6]), np.finfo(float).tiny)
         if conv:
             st["done"] = 1
-        elif k >= st["max_iters"] or (st["time_budget"] > 0 and wall >= st["time_budget"]):
+        elif k >= st["max_iters"] or budget_hit > 0:
             st["done"] = 2
         else:
             st["k"] = k + 1

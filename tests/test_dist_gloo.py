@@ -38,12 +38,16 @@ def _worker(rank, world, port, kind, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         comm = Comm()
+        budget = kind.endswith("_budget")
+        kind = kind.replace("_budget", "")
         if kind == "pcp":
             d, _ = O.gaussian_rpca(96, 80, 5, 0.1, 21)
             m, n = d.shape
             r0, r1 = rank * m // world, (rank + 1) * m // world
             be = EmuPcp(CH.build_chain(n, 20), r1 - r0, m, False, 200)
-            opts = T.PcpOptions(levels=20, tol_feasibility=1e-7)
+            opts = T.PcpOptions(levels=20, tol_feasibility=1e-7, time_budget=1000.0 if budget else None)
+            if budget and rank == 1:
+                be.clock_skew = 1e6  # only this rank's clock says the budget is spent
             L, S, Y, st, h = P.run_ialm(be, comm, torch.from_numpy(np.ascontiguousarray(d[r0:r1])), m, n, opts,
                                         1 / np.sqrt(max(m, n)), 2)
             out_q.put((rank, r0, L.numpy(), S.numpy(), st["k"], h[:, 0].copy()))
@@ -56,7 +60,9 @@ def _worker(rank, world, port, kind, out_q):
             bits = torch.from_numpy(T.ObservationMask(mask[r0:r1]).packed_bits().view(np.int32))
             lam = 1 / np.sqrt(m)
             opts = T.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(m), tol=1e-6, max_iters=300, levels=20,
-                                 collect_rank=False)
+                                 collect_rank=False, time_budget=1000.0 if budget else None)
+            if budget and rank == 1:
+                be.clock_skew = 1e6
             L, S, st, h, objs = C.run_fwt(be, comm, torch.from_numpy(np.ascontiguousarray(d[r0:r1])), bits, m,
                                           opts, 1 / ch.sigma_max(), 3)
             out_q.put((rank, r0, L.numpy(), S.numpy(), st["k"], np.array(objs)))
@@ -107,3 +113,13 @@ def test_cpcp_row_sharded_matches_single():
     # an ulp-level difference in the summed Gram can move the stop by a pass
     assert abs(two[0][5][0] - one[5][0]) <= 1e-7 * one[5][0]
     assert abs(two[0][5][-1] - one[5][-1]) / one[5][-1] < 1e-4
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("kind", ["pcp", "cpcp"])
+def test_time_budget_decision_is_collective(kind):
+    """One rank's clock passes the budget while the other's does not: the
+    budget flags travel in the summed stats, so both ranks stop after the
+    same iteration (no hang, no mismatched collective counts)."""
+    two = _run(kind + "_budget", 2)
+    assert two[0][4] == two[1][4] == 1

@@ -222,3 +222,16 @@ def test_oracle_matches_live_reference(reference):
         lambda_l=lam, lambda_s=lam / np.sqrt(90), tol=1e-5, levels=16, collect_rank=False))
     got2 = O.ml_fwt(d, mask, lam, lam / np.sqrt(90), tol=1e-5, levels=16, collect_rank=False)
     assert ref2.iter == got2.iter and np.array_equal(ref2.l, got2.l)
+
+
+def test_oracle_loop_generator_matches_ml_ialm():
+    """bench.py's bounded CPU samples iterate oracle.ml_ialm_steps: with the
+    same sigma_1 it reproduces ml_ialm's iterates bit for bit; its Lanczos
+    sigma_1 (setup only) agrees with the 2-norm."""
+    d, _ = O.make_config("C1", 0)
+    ref = O.ml_ialm(d, lam=1 / np.sqrt(500), tol=1e-7, levels=125)
+    gen = O.ml_ialm_steps(d, np.linalg.norm(d, 2), levels=125)
+    got = [next(gen) for _ in range(ref.iter)]
+    assert [g[1] for g in got] == [h.feasibility_gap for h in ref.history]
+    assert [g[2] for g in got] == [h.rank_l for h in ref.history]
+    assert abs(O.lanczos_sigma1(d) - np.linalg.norm(d, 2)) <= 1e-12 * np.linalg.norm(d, 2)
