@@ -298,7 +298,7 @@ def pcp_secondary(dev, seed, flush, name="C2", reps=5):
             "iterations_per_s": iters / (ms / 1e3), "dtype": "f32" if c["dtype"] == "float32" else "f64"}
 
 
-def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic):
+def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic, real_launches):
     """Per-phase rooflines from the live CUDA-event phase timers (SURVEY.md
     8(d) algorithmic work)."""
     m, n, nh = m_local, cfg["n"], cfg["n_coarse"]
@@ -310,12 +310,14 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic):
     fp64 = fp64 or 40.0
     out = {}
 
-    def avg_us(ph):
-        ms, cnt = phases.get(ph, (0.0, 0))
-        return (1e3 * ms / cnt) if cnt else None
 
     def add(ph, kernel, bound, work, unit, peak, formula, tkey=None, peak_source=None):
-        us = avg_us(ph)
+        # per REAL launch: the phase timers also count the no-op launches of
+        # the pipelined batch that runs past convergence, and the rank-0
+        # iterations whose eigensolve / reconstruction is skipped
+        ms, cnt = phases.get(ph, (0.0, 0))
+        real = real_launches.get(ph, cnt)
+        us = (1e3 * ms / real) if real else None
         if us is None or us <= 0:
             return
         ach = work / (us * 1e-6) / (1e9 if unit == "GB/s" else 1e12)
@@ -323,7 +325,7 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic):
         out[ph] = {"bound": bound, "kernel": kernel, "achieved": ach, "peak": peak, "unit": unit,
                    "frac": ach / peak, "traffic": t["dram_bytes_per_launch"] if t else None,
                    "algorithmic_per_launch": work, "formula": formula, "avg_us": us,
-                   "launches": phases[ph][1], "peak_source": peak_source or "MEASURED_PEAKS.json hbm_gbs"}
+                   "launches": real, "peak_source": peak_source or "MEASURED_PEAKS.json hbm_gbs"}
 
     add("update", "pcp_update_fast (FP32 regular chain: fused prolong / shrink / dual / stats / next restriction)",
         "hbm", b * (3 * m * n + 2 * m * npad), "GB/s", hbm, "b (3 m n + 2 m n_p) bytes")
@@ -446,11 +448,13 @@ def gpu_arm(args, name, cfg, world, rank, local):
                 a[0] += v[0]
                 a[1] += v[1]
     phase_ms = {k: v[0] for k, v in phases.items()}
-    sweeps = [x for s in sink for x in s.get("jac_sweeps", []) if x > 0]
-    rl = roofline_entries(name, cfg, phases, sweeps, r1 - r0, world, peaks, _traffic(name))
+    sweeps_all = [x for s in sink for x in s.get("jac_sweeps", [])]
+    sweeps = [x for x in sweeps_all if x > 0]
+    k_solve = sum(s.get("iters", 0) for s in sink) or 1
+    real = {"update": k_solve, "gram": k_solve + 1, "jacobi": len(sweeps), "recon": len(sweeps)}
+    rl = roofline_entries(name, cfg, phases, sweeps, r1 - r0, world, peaks, _traffic(name), real)
     dominant = max(phase_ms, key=phase_ms.get) if phase_ms else None
     roof = rl.get(dominant) or rl.get("update")
-    k_solve = sum(s.get("iters", 0) for s in sink) or 1
     per_iter = {k: round(v / k_solve, 4) for k, v in phase_ms.items()}
 
     cpu = None
@@ -489,6 +493,8 @@ def gpu_arm(args, name, cfg, world, rank, local):
         "kernels": rl,
         "phase_ms_per_iter": per_iter,
         "dominant_phase": dominant,
+        "jacobi_sweeps_per_iteration": sweeps_all,
+        "lanczos_steps": sink[0].get("lanczos_steps") if sink else None,
         "time_to_tol_ms": total_ms / args.steps,
         "loop_iterations_per_s": (iters / args.steps) / ((total_ms / args.steps - phase_ms.get("lanczos", 0.0)) / 1e3),
         "cpu_baseline": cpu,

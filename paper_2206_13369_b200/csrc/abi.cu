@@ -122,7 +122,8 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.jac_result = c.take<int>(4 * 16);
   p.lzQ = c.take<double>(8 * (size_t)n * (p.lz_kmax + 1));
   p.lzT = c.take<double>(8 * (size_t)std::max<int64_t>(p.m_local, 1));
-  p.lzW = c.take<double>(8 * (size_t)n * std::max(std::max(p.lz_splits, p.lz_fused_ctas), p.lz_run_ctas));
+  p.lzW = c.take<double>(8 * (size_t)n *
+                         std::max(std::max(std::max(p.lz_splits, p.lz_fused_ctas), p.lz_run_ctas), p.lz_long_clusters));
   p.lzRed = c.take<double>(8 * (size_t)std::max(p.lz_run_ctas, 1) * (2 * ((size_t)p.lz_kmax + 1) + 4));
   p.lzWork = c.take<double>(8 * (size_t)n);
 }
@@ -161,6 +162,10 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
     const bool fused = ch.n <= 2048 && !(e && e[0] == '0');
     p.lz_fused_ctas = fused ? (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(m_local, 1), 8), sms))
                             : 0;
+    const char* lg = getenv("MLR_LZ_LONG");
+    // n <= 2 CTAs x 512 threads x 6 float4 groups; seg x 4 B per stage, >= 4 stages
+    p.lz_long_clusters = (f32 && ch.n > 2048 && ch.n % 4 == 0 && ch.n <= 24576 && !(lg && lg[0] == '0'))
+                             ? sms / 2 : 0;
     const char* r = getenv("MLR_LZ_RUN");
     p.lz_run_ctas = (ch.n <= 4096 && m_local > 0 && !(r && r[0] == '0')) ? sms : 0;
     const char* rc = getenv("MLR_LZ_RUN_CTAS");

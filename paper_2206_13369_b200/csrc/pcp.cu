@@ -307,6 +307,197 @@ __global__ void __launch_bounds__(LZ_FW * 32, 1) lz_dtdv_kernel(const LanczosDev
   }
 }
 
+// w = D^T (D q) in ONE pass over D for long FP32 rows (n > LZ_FUSED_N, C5:
+// 20000 columns).  A 2-CTA cluster owns whole rows; CTA c of the pair owns
+// the column segment [c seg, (c+1) seg).  Row segments stream HBM -> shared
+// memory by TMA bulk copies (cp.async.bulk, one mbarrier per stage, one
+// elected producer thread, LZL_STAGES segments in flight); each thread keeps
+// its columns' q and FP64 accumulator in registers.  Per batch of LZL_R rows:
+// partial dots d_i.q over the segment (FP64) -> block sum -> the two CTAs
+// swap partials through DSMEM and one cluster barrier -> t_i summed in a
+// fixed order (identical in both CTAs) -> acc += t_i d_i.  The cluster's
+// FP64 partial of w goes to wpart[cluster]; sum_slices adds the clusters in
+// a fixed order (deterministic).  D is read once per Lanczos step instead of
+// twice (lz_dv_kernel + lz_dtv_kernel).
+constexpr int LZL_T = 512, LZL_CL = 2, LZL_R = 2, LZL_NG = 6;  // NG float4 groups per thread: seg <= 12288
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dsmem_st_f64(const double* local, uint32_t cta, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev* __restrict__ lz,
+                                                                const float* __restrict__ D, int64_t ldd,
+                                                                int64_t m, int n, int seg, int stages,
+                                                                const double* __restrict__ Q,
+                                                                double* __restrict__ wpart) {
+  extern __shared__ __align__(128) unsigned char lzl_smem[];
+  __shared__ __align__(8) uint64_t full[16];
+  __shared__ double xch[2][LZL_R][LZL_CL];
+  __shared__ double red[LZL_T / 32][LZL_R];
+  uint32_t cr, cid, ncl;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+  asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+  asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+  const bool skip = lz->done != 0;  // uniform over the grid
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col0 = (int)cr * seg;
+  const int len = max(0, min(seg, n - col0));     // multiple of 4 (n % 4 == 0)
+  const int ng4 = len >> 2;
+  const int64_t nrows = (int64_t)cid < m ? (m - 1 - cid) / ncl + 1 : 0;
+  float* stage = reinterpret_cast<float*>(lzl_smem);
+  const uint32_t bytes = (uint32_t)len * 4u;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!skip && tid == 0 && bytes > 0)
+    for (int s = 0; s < stages && s < nrows; ++s) {
+      mbar_expect_tx(&full[s], bytes);
+      bulk_g2s(stage + (size_t)s * seg, D + ((int64_t)cid + (int64_t)s * ncl) * ldd + col0, bytes, &full[s]);
+    }
+  double qv[LZL_NG][4], acc[LZL_NG][4];
+  const double* __restrict__ q = Q + (int64_t)(skip ? 0 : lz->k) * n + col0;
+#pragma unroll
+  for (int g = 0; g < LZL_NG; ++g) {
+    const int k = tid + g * LZL_T;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      qv[g][e] = (!skip && k < ng4) ? q[4 * k + e] : 0.0;
+      acc[g][e] = 0.0;
+    }
+  }
+  cluster_sync_all();  // both CTAs started: exchange slots may be written
+  if (!skip) {
+    const int64_t nb = (nrows + LZL_R - 1) / LZL_R;
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t j0 = b * LZL_R;
+      const int rr = (int)(nrows - j0 < LZL_R ? nrows - j0 : LZL_R);
+      double part[LZL_R];
+#pragma unroll
+      for (int r = 0; r < LZL_R; ++r) {
+        part[r] = 0.0;
+        if (r < rr) {
+          const int64_t j = j0 + r;
+          const int s = (int)(j % stages);
+          mbar_wait(&full[s], (uint32_t)((j / stages) & 1));
+          const float4* row = reinterpret_cast<const float4*>(stage + (size_t)s * seg);
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int g = 0; g < LZL_NG; ++g) {
+            const int k = tid + g * LZL_T;
+            if (k < ng4) {
+              const float4 x = row[k];
+              a0 = fma((double)x.x, qv[g][0], a0);
+              a1 = fma((double)x.y, qv[g][1], a1);
+              a0 = fma((double)x.z, qv[g][2], a0);
+              a1 = fma((double)x.w, qv[g][3], a1);
+            }
+          }
+          part[r] = warp_sum(a0 + a1);
+        }
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < LZL_R; ++r) red[warp][r] = part[r];
+      __syncthreads();
+      if (warp == 0) {
+        // lanes 0..R-1 sum the warps' partials of row r in a fixed order and
+        // post them to both CTAs of the pair
+        if (lane < LZL_R) {
+          double v = 0.0;
+          for (int w = 0; w < LZL_T / 32; ++w) v += red[w][lane];
+          for (uint32_t c = 0; c < LZL_CL; ++c) dsmem_st_f64(&xch[b & 1][lane][cr], c, v);
+        }
+      }
+      cluster_sync_all();
+      double t[LZL_R];
+#pragma unroll
+      for (int r = 0; r < LZL_R; ++r) {
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < LZL_CL; ++c) v += xch[b & 1][r][c];
+        t[r] = r < rr ? v : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < LZL_R; ++r) {
+        if (r < rr) {
+          const int s = (int)((j0 + r) % stages);
+          const float4* row = reinterpret_cast<const float4*>(stage + (size_t)s * seg);
+#pragma unroll
+          for (int g = 0; g < LZL_NG; ++g) {
+            const int k = tid + g * LZL_T;
+            if (k < ng4) {
+              const float4 x = row[k];
+              acc[g][0] = fma((double)x.x, t[r], acc[g][0]);
+              acc[g][1] = fma((double)x.y, t[r], acc[g][1]);
+              acc[g][2] = fma((double)x.z, t[r], acc[g][2]);
+              acc[g][3] = fma((double)x.w, t[r], acc[g][3]);
+            }
+          }
+        }
+      }
+      __syncthreads();  // every thread is done with this batch's stages
+      if (tid == 0 && bytes > 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int r = 0; r < rr; ++r) {
+          const int64_t jn = j0 + r + stages;
+          if (jn < nrows) {
+            const int s = (int)(jn % stages);
+            mbar_expect_tx(&full[s], bytes);
+            bulk_g2s(stage + (size_t)s * seg, D + ((int64_t)cid + jn * ncl) * ldd + col0, bytes, &full[s]);
+          }
+        }
+      }
+    }
+  }
+  double* o = wpart + (int64_t)cid * n + col0;
+#pragma unroll
+  for (int g = 0; g < LZL_NG; ++g) {
+    const int k = tid + g * LZL_T;
+    if (k < ng4)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[4 * k + e] = acc[g][e];
+  }
+}
+
+int lz_long_stages(int seg) {
+  const int64_t avail = 200 * 1024;
+  return (int)std::min<int64_t>(16, avail / ((int64_t)seg * 4));
+}
+
 // True if the symmetric tridiagonal (a[0..k1), b[0..k1-1)) has an eigenvalue
 // above x: T - x I has a positive LDL^T pivot d_i = p_i / p_(i-1), with the
 // leading principal minors p_i = (a_i - x) p_(i-1) - b_(i-1)^2 p_(i-2)
@@ -1063,6 +1254,31 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
     }
     MLR_LAUNCH_CHECK("lz_dtdv_kernel");
     const int rc = sum_slices(p->lzW, n, n, ctas, wpart_out, st);
+    p->timer.end(kPhLanczos, st);
+    return rc;
+  }
+  if (p->lz_long_clusters > 0 && p->f32 && ldd % 4 == 0 && ((uintptr_t)D & 15) == 0) {
+    const int ncl = p->lz_long_clusters;
+    const int seg = (int)(ceil_div(ceil_div(n, LZL_CL), 4) * 4);
+    const int stages = lz_long_stages(seg);
+    const size_t smem = (size_t)stages * seg * sizeof(float);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncl * LZL_CL);
+    cfg.blockDim = dim3(LZL_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = LZL_CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MLR_CUDA(cudaFuncSetAttribute(lz_dtdq_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLR_CUDA(cudaLaunchKernelEx(&cfg, lz_dtdq_long_kernel, (const LanczosDev*)p->lz, (const float*)D, ldd, m, n, seg,
+                                stages, (const double*)p->lzQ, p->lzW));
+    MLR_LAUNCH_CHECK("lz_dtdq_long_kernel");
+    const int rc = sum_slices(p->lzW, n, n, ncl, wpart_out, st);
     p->timer.end(kPhLanczos, st);
     return rc;
   }

@@ -46,6 +46,7 @@ struct PcpPlan {
   int max_iters;
   int row_blocks, gram_splits, lz_splits, lz_kmax;
   int lz_fused_ctas;  // > 0: one-pass D^T D q (n <= 2048)
+  int lz_long_clusters;  // > 0: one-pass D^T D q for long FP32 rows (2-CTA clusters, TMA-staged rows)
   int coarse_ksplit;  // split-K of the n_p^3 coarse products (<= gram_splits)
   int lz_run_ctas;    // > 0: the whole Lanczos run in one cooperative kernel (one rank, n <= 4096)
   int eig_sort;       // sort the eigenpairs after each Jacobi (warm start of the next)

@@ -39,49 +39,62 @@ class FrameStack:
     matrix: object
 
 
-def _token(fh):
-    # whitespace-separated tokens; '#' starts a comment to end of line (io.py:83-97)
-    tok = b""
-    while True:
-        ch = fh.read(1)
-        if ch == b"":
-            raise FormatError("unexpected end of PGM header")
-        if ch == b"#":
-            while ch not in (b"\n", b""):
-                ch = fh.read(1)
-            continue
-        if ch.isspace():
-            if tok:
-                return tok
-            continue
-        tok += ch
+_PGM_SPACE = frozenset(b" \t\n\r\x0b\x0c")
+
+
+def _pgm_header(buf, path):
+    """Scan the P5 header of an in-memory PGM file.
+
+    Returns (width, height, maxval, raster offset).  Header fields are
+    whitespace-separated decimal tokens; '#' opens a comment that runs to the
+    end of the line and may appear anywhere in the header; the raster starts
+    right after the single whitespace byte that ends the maxval field
+    (the header grammar of reference io.py:83-114)."""
+    if buf[:2] != b"P5":
+        raise FormatError(f"{path}: not a binary PGM (P5) file")
+    pos, n, fields = 2, len(buf), []
+    while len(fields) < 3:
+        digits = bytearray()
+        while True:
+            if pos >= n:
+                raise FormatError("unexpected end of PGM header")
+            c = buf[pos]
+            pos += 1
+            if c == 0x23:  # '#': drop the rest of the line
+                nl = buf.find(b"\n", pos)
+                pos = n if nl < 0 else nl + 1
+            elif c in _PGM_SPACE:
+                if digits:
+                    break
+            else:
+                digits.append(c)
+        fields.append(int(bytes(digits)))
+    width, height, maxval = fields
+    return width, height, maxval, pos
 
 
 def read_pgm(path):
-    """Binary 8-bit PGM (P5) -> (height, width) uint8 (io.py:100-114)."""
+    """Binary 8-bit PGM (P5) -> (height, width) uint8 (reference io.py:100-114)."""
     with open(path, "rb") as fh:
-        if fh.read(2) != b"P5":
-            raise FormatError(f"{path}: not a binary PGM (P5) file")
-        width = int(_token(fh))
-        height = int(_token(fh))
-        maxval = int(_token(fh))
-        if maxval != 255:
-            raise FormatError(f"{path}: only 8-bit PGM supported, maxval={maxval}")
-        raster = fh.read(width * height)
-    if len(raster) != width * height:
+        buf = fh.read()
+    width, height, maxval, off = _pgm_header(buf, path)
+    if maxval != 255:
+        raise FormatError(f"{path}: only 8-bit PGM supported, maxval={maxval}")
+    count = width * height
+    if len(buf) - off < count:
         raise FormatError(f"{path}: truncated raster")
-    return np.frombuffer(raster, dtype=np.uint8).reshape((height, width))
+    return np.frombuffer(buf, dtype=np.uint8, count=count, offset=off).reshape((height, width)).copy()
 
 
 def write_pgm(pixels, path):
-    """(height, width) uint8 -> canonical binary PGM (io.py:117-125)."""
-    pixels = np.asarray(pixels, dtype=np.uint8)
-    if pixels.ndim != 2:
+    """(height, width) uint8 -> canonical binary PGM: 'P5\\n<w> <h>\\n255\\n'
+    then the raster (reference io.py:117-125)."""
+    img = np.asarray(pixels, dtype=np.uint8)
+    if img.ndim != 2:
         raise ValueError("pixels must be 2-D")
-    h, w = pixels.shape
+    header = b"P5\n%d %d\n255\n" % (img.shape[1], img.shape[0])
     with open(path, "wb") as fh:
-        fh.write(f"P5\n{w} {h}\n255\n".encode("ascii"))
-        fh.write(pixels.tobytes(order="C"))
+        fh.write(header + np.ascontiguousarray(img).tobytes())
 
 
 def read_frames(paths):

@@ -332,3 +332,19 @@ def test_jacobi_cooperative_grid_vs_lapack(n):
     assert np.abs(lam - ev).max() <= 1e-12 * ev[0]
     assert np.abs(v.T @ v - np.eye(n)).max() <= 1e-11
     assert np.linalg.norm(b @ v - v * lam) <= 1e-11 * np.linalg.norm(b)
+
+
+# ------------------------------------------------------------------ long-row Lanczos
+@pytest.mark.parametrize("m,n", [(400, 4096), (60, 4100)])
+def test_lanczos_long_rows_sigma1(m, n):
+    """n > 2048 FP32 takes the one-pass cluster kernel (TMA-staged rows, DSMEM
+    dot exchange); m = 60 leaves most clusters without rows, n = 4100 makes
+    the two column segments unequal.  mu_k = rho^k 1.25 / sigma_1 must match
+    the oracle's exact sigma_1 to the FP32 Lanczos tolerance, and the solve
+    must match the oracle."""
+    d, _ = O.gaussian_rpca(m, n, 5, 0.1, 17)
+    d32 = d.astype(np.float32)
+    opts = pkg.PcpOptions(tol_feasibility=1e-6, max_iters=3)
+    st = pkg.ml_ialm_solve(d32, opts)
+    s1 = np.linalg.norm(d32.astype(np.float64), 2)
+    assert np.isclose(st.mu_history[0], 1.25 / s1, rtol=1e-8)

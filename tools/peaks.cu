@@ -1,0 +1,118 @@
+// Peak-throughput microbenchmarks for the roofline denominators that
+// MEASURED_PEAKS.json does not carry: FP64 tensor-core MMA (the
+// mma.sync.m8n8k4.f64 path the Gram / reconstruction / coarse products use),
+// FP32 FFMA and FP64 DFMA SIMT.  Prints one JSON object.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/peaks tools/peaks.cu && tools/peaks
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e = (x);                                                           \
+    if (e != cudaSuccess) {                                                        \
+      fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e));    \
+      return 1;                                                                    \
+    }                                                                              \
+  } while (0)
+
+constexpr int kIters = 4096;
+constexpr int kAcc = 8;  // independent accumulator chains per warp / thread
+
+__global__ void dmma_kernel(double* out, double seed) {
+  double a = seed + threadIdx.x * 1e-3, b = seed - threadIdx.x * 1e-3;
+  double c[kAcc][2];
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) c[q][0] = c[q][1] = 0.0;
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int q = 0; q < kAcc; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[q][0]), "+d"(c[q][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) s += c[q][0] + c[q][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void dfma_kernel(double* out, double seed) {
+  double x[kAcc];
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) x[q] = seed + q;
+  const double m = 0.999999, add = 1e-7;
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int q = 0; q < kAcc; ++q) x[q] = fma(x[q], m, add);
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) s += x[q];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void ffma_kernel(float* out, float seed) {
+  float x[kAcc];
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) x[q] = seed + q;
+  const float m = 0.999999f, add = 1e-7f;
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int q = 0; q < kAcc; ++q) x[q] = fmaf(x[q], m, add);
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) s += x[q];
+  if (s == 12345.678f) out[0] = s;
+}
+
+template <typename K>
+float time_ms(K launch, int reps) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  launch();
+  cudaDeviceSynchronize();
+  cudaEventRecord(a);
+  for (int r = 0; r < reps; ++r) launch();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms / reps;
+}
+
+int main() {
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, 0));
+  double* d;
+  CK(cudaMalloc(&d, 64));
+  const int sms = p.multiProcessorCount;
+  // DMMA: 512 flops per warp instruction
+  double best_dmma = 0.0;
+  for (int warps = 4; warps <= 32; warps *= 2) {
+    const int blocks = sms * 2, threads = 32 * warps / 2;
+    float ms = time_ms([&] { dmma_kernel<<<blocks, threads>>>(d, 1.0); }, 5);
+    double flops = (double)blocks * (threads / 32) * kIters * kAcc * 512.0;
+    double tf = flops / (ms * 1e-3) / 1e12;
+    if (tf > best_dmma) best_dmma = tf;
+  }
+  CK(cudaGetLastError());
+  double best_dfma = 0.0, best_ffma = 0.0;
+  for (int threads = 256; threads <= 1024; threads *= 2) {
+    const int blocks = sms * (2048 / threads);
+    float ms = time_ms([&] { dfma_kernel<<<blocks, threads>>>(d, 1.0); }, 5);
+    double tf = (double)blocks * threads * kIters * kAcc * 2.0 / (ms * 1e-3) / 1e12;
+    if (tf > best_dfma) best_dfma = tf;
+    ms = time_ms([&] { ffma_kernel<<<blocks, threads>>>((float*)d, 1.f); }, 5);
+    tf = (double)blocks * threads * kIters * kAcc * 2.0 / (ms * 1e-3) / 1e12;
+    if (tf > best_ffma) best_ffma = tf;
+  }
+  CK(cudaGetLastError());
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("{\"device\": \"%s\", \"sms\": %d, \"max_sm_mhz\": %d, \"fp64_mma_tflops\": %.2f, "
+         "\"fp64_dfma_tflops\": %.2f, \"fp32_ffma_tflops\": %.2f, \"method\": \"tools/peaks.cu: "
+         "%d-deep independent chains per warp/thread, best over occupancies, CUDA events\"}\n",
+         p.name, sms, clk / 1000, best_dmma, best_dfma, best_ffma, kAcc);
+  return 0;
+}
