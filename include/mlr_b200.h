@@ -78,6 +78,25 @@ int64_t mlr_eigh_work_doubles(int np);
 int mlr_eigh_psd(int np, const double* B, double* V, double* lam, double tol, int max_sweeps, double* work,
                  int* info, void* stream);
 
+/* ---------------------------------------------------------------- NCCL
+ * Communicator of the row-sharded solvers (the reference is
+ * single-process and has no counterpart).  One rank per GPU: rank 0 calls
+ * mlr_comm_unique_id, the 128-byte id is exchanged once out of band, every
+ * rank calls mlr_comm_create.  The host loops then all-reduce the plan's
+ * red buffer (mlr_pcp_gram / mlr_cpcp_gram layouts), all-gather the CPCP
+ * arg-max records and all-reduce the QP dots / Lanczos vectors on the
+ * plan's stream.  NCCL is dlopen'd at the first call (mlr_comm_available()
+ * reports whether it could be).  dtype: 8 = float64, 5 = int64; op: 0 = sum,
+ * 2 = max (NCCL's enum values). */
+int mlr_comm_available(void);
+int mlr_comm_unique_id(void* out128);
+int mlr_comm_create(const void* id128, int nranks, int rank, int device, void** comm_out);
+int mlr_comm_destroy(void* comm);
+int mlr_comm_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream);
+int mlr_comm_allgather(void* comm, const void* in, void* out, int64_t count, int dtype, void* stream);
+int mlr_comm_rank(void* comm);
+int mlr_comm_size(void* comm);
+
 /* ---------------------------------------------------------------- ML-PCP */
 int64_t mlr_pcp_workspace_bytes(void* chain, int64_t m_local, int f32, int max_iters);
 int mlr_pcp_create(void* chain, int64_t m_local, int64_t m_global, int f32, int max_iters, void* workspace,

@@ -35,6 +35,15 @@ _SIGS = {
     "mlr_eigh_work_doubles": (c_int64, [c_int]),
     "mlr_eigh_psd": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p,
                              c_void_p]),
+    # NCCL communicator (row-sharded solvers)
+    "mlr_comm_available": (c_int, []),
+    "mlr_comm_unique_id": (c_int, [c_void_p]),
+    "mlr_comm_create": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "mlr_comm_destroy": (c_int, [c_void_p]),
+    "mlr_comm_allreduce": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p]),
+    "mlr_comm_allgather": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "mlr_comm_rank": (c_int, [c_void_p]),
+    "mlr_comm_size": (c_int, [c_void_p]),
     # ML-PCP
     "mlr_pcp_workspace_bytes": (c_int64, [c_void_p, c_int64, c_int, c_int]),
     "mlr_pcp_create": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_void_p, POINTER(c_void_p)]),

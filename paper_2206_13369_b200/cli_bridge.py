@@ -12,6 +12,12 @@ selection, ``.lrml`` I/O and the metrics CSV stay the reference's own.
     mlrpca.cli.main(["compare", ...])
 
 ``install`` returns the previous bindings; ``uninstall`` restores them.
+
+``install_side_by_side`` instead keeps the reference's CPU solvers and adds
+GPU names (``ialm-gpu``, ``ml-ialm-gpu``, ``fwt-gpu``, ``ml-fwt-gpu``) to the
+CLI's solver tuples (cli.py:27-28), so ``mlrpca compare --solver-a ml-ialm
+--solver-b ml-ialm-gpu`` runs the reference and this package on the same
+input and writes both metric files (cli.py:336-361).
 """
 
 from __future__ import annotations
@@ -65,3 +71,36 @@ def install(cli_module, solvers=None, frame_io=True):
 def uninstall(cli_module, previous):
     for name, fn in previous.items():
         setattr(cli_module, name, fn)
+
+
+GPU_SUFFIX = "-gpu"
+
+
+def install_side_by_side(cli_module, solvers=None):
+    """Add '<name>-gpu' solver names next to the reference's own.  A GPU name
+    runs the reference's _solve_one (cli.py:218-236: same option handling,
+    timing and returned fields) with the four solver names bound to this
+    package for the duration of that one call."""
+    gpu = dict(solvers or GPU_SOLVERS)
+    previous = {"PCP_SOLVERS": cli_module.PCP_SOLVERS, "CPCP_SOLVERS": cli_module.CPCP_SOLVERS,
+                "_solve_one": cli_module._solve_one}
+    cli_module.PCP_SOLVERS = tuple(previous["PCP_SOLVERS"]) + tuple(
+        x + GPU_SUFFIX for x in previous["PCP_SOLVERS"])
+    cli_module.CPCP_SOLVERS = tuple(previous["CPCP_SOLVERS"]) + tuple(
+        x + GPU_SUFFIX for x in previous["CPCP_SOLVERS"])
+    cpu_solve_one = previous["_solve_one"]
+
+    def solve_one(solver, d, mask, cfg):
+        if not solver.endswith(GPU_SUFFIX):
+            return cpu_solve_one(solver, d, mask, cfg)
+        saved = {k: getattr(cli_module, k) for k in gpu if hasattr(cli_module, k)}
+        try:
+            for k in saved:
+                setattr(cli_module, k, gpu[k])
+            return cpu_solve_one(solver[:-len(GPU_SUFFIX)], d, mask, cfg)
+        finally:
+            for k, v in saved.items():
+                setattr(cli_module, k, v)
+
+    cli_module._solve_one = solve_one
+    return previous

@@ -128,6 +128,28 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.lzWork = c.take<double>(8 * (size_t)n);
 }
 
+// K slices of the blocked 128x128 Gram (one CTA per SM).  Small Grams (few
+// blocks) take one wave of sms / blocks slices; large ones (C5: 55 blocks)
+// the slice count whose CTA count best fills whole waves (C5: 8 slices ->
+// 440 CTAs = 2.97 waves of 148; the old one-wave rule gave 2 slices -> 110
+// CTAs on 148 SMs).
+static int64_t gram128_splits(int64_t b128, int sms, int64_t m_local) {
+  if (2 * b128 <= sms) return std::max<int64_t>(1, sms / b128);
+  int64_t best = 1;
+  double best_e = 0.0;
+  for (int64_t s = 1; s <= 16; ++s) {
+    if (s > 1 && m_local / s < 512) break;
+    const int64_t ctas = b128 * s;
+    const double e = (double)ctas / (double)(ceil_div(ctas, (int64_t)sms) * sms);
+    if (e > best_e + 0.02) {
+      best_e = e;
+      best = s;
+    }
+  }
+  const char* env = getenv("MLR_GRAM_SPLITS");
+  return env ? std::max(1, atoi(env)) : best;
+}
+
 static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t m_global, int f32, int max_iters) {
   p = PcpPlan{};
   p.ch = ch;
@@ -141,7 +163,7 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   int64_t splits = ceil_div(2 * sms, tiles);
   if (gram128_ok(ch.np)) {  // blocked Gram (gemm_f64.cu): about one CTA per SM
     const int64_t b128 = (int64_t)(ch.np / 128) * (ch.np / 128 + 1) / 2;
-    splits = std::max<int64_t>(1, sms / b128);  // one wave (1 CTA per SM: 512 threads x 100 registers)
+    splits = gram128_splits(b128, sms, m_local);
   }
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);
@@ -225,7 +247,7 @@ static void cpcp_params(CpcpPlan& p, const ChainDev& ch, int64_t m_local, int64_
   int64_t splits = ceil_div(2 * sms, tiles);
   if (gram128_ok(ch.np)) {  // blocked Gram (gemm_f64.cu): about one CTA per SM
     const int64_t b128 = (int64_t)(ch.np / 128) * (ch.np / 128 + 1) / 2;
-    splits = std::max<int64_t>(1, sms / b128);  // one wave (1 CTA per SM: 512 threads x 100 registers)
+    splits = gram128_splits(b128, sms, m_local);
   }
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, m_local / 64));
   p.gram_splits = (int)std::max<int64_t>(1, splits);

@@ -3,28 +3,82 @@ conversion, and the collective wrapper used for row-sharded runs."""
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
 
-class Comm:
-    """Collectives over a torch.distributed group (NCCL on GPUs, gloo on CPU);
-    a world of one makes every call a no-op."""
+_NATIVE = {}  # (group, device) -> native NCCL communicator handle (one per process group)
 
-    def __init__(self, group=None, enabled=None):
+
+def _native_comm(group, world, rank):
+    """The library's own NCCL communicator for this group (mlr_comm_create),
+    built once: rank 0's unique id travels by ONE torch.distributed broadcast,
+    after which every per-iteration collective is a direct ncclAllReduce /
+    ncclAllGather call on the plan stream (include/mlr_b200.h)."""
+    from . import _lib
+    dev = torch.cuda.current_device()
+    key = (id(group) if group is not None else None, dev)
+    if key in _NATIVE:
+        return _NATIVE[key]
+    lib = _lib.load()
+    if not lib.mlr_comm_available():
+        _NATIVE[key] = None
+        return None
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        _lib.check(lib.mlr_comm_unique_id(ctypes.c_void_p(uid.data_ptr())))
+    t = uid.cuda()
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    uid.copy_(t.cpu())
+    h = ctypes.c_void_p()
+    _lib.check(lib.mlr_comm_create(ctypes.c_void_p(uid.data_ptr()), world, rank, dev, ctypes.byref(h)))
+    _NATIVE[key] = h
+    return h
+
+
+class Comm:
+    """Collectives of the row-sharded solvers.  On GPUs over an NCCL process
+    group they run on the library's own NCCL communicator (ctypes ->
+    mlr_comm_allreduce / mlr_comm_allgather on the current stream; torch.
+    distributed only carries the one-time unique-id exchange).  Over gloo
+    (CPU tests, ranks sharing one device) they go through torch.distributed,
+    staging CUDA tensors through host memory.  A world of one makes every
+    call a no-op."""
+
+    def __init__(self, group=None, enabled=None, force_native=None):
+        if force_native is None:  # tests: run a one-rank NCCL group through the native collectives
+            force_native = os.environ.get("MLR_FORCE_NATIVE_NCCL") == "1"
         if enabled is None:
             enabled = dist.is_available() and dist.is_initialized()
         self.enabled = bool(enabled)
         self.group = group
         self.world = dist.get_world_size(group) if self.enabled else 1
         self.rank = dist.get_rank(group) if self.enabled else 0
+        self.native = None
+        if (self.world > 1 or force_native) and self.enabled and torch.cuda.is_available() \
+                and dist.get_backend(group) == "nccl" and os.environ.get("MLR_NATIVE_NCCL", "1") != "0":
+            self.native = _native_comm(group, self.world, self.rank)  # force_native: one-rank NCCL (tests)
 
     def _host(self, t):
         """gloo works on host tensors: stage CUDA tensors through host memory."""
         return self.world > 1 and t.is_cuda and dist.get_backend(self.group) != "nccl"
 
+    def _nat(self, t):
+        return self.native is not None and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+
+    def _native_reduce(self, t, op):
+        from . import _lib
+        _lib.check(_lib.load().mlr_comm_allreduce(self.native, ctypes.c_void_p(t.data_ptr()), t.numel(), 8, op,
+                                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return t
+
     def sum(self, t):
+        if self._nat(t):
+            return self._native_reduce(t, 0)
         if self.world > 1:
             if self._host(t):
                 h = t.cpu()
@@ -35,6 +89,8 @@ class Comm:
         return t
 
     def max(self, t):
+        if self._nat(t):
+            return self._native_reduce(t, 2)
         if self.world > 1:
             if self._host(t):
                 h = t.cpu()
@@ -46,7 +102,12 @@ class Comm:
 
     def gather(self, out, t):
         """out (world * t.numel()) <- concatenation of every rank's t."""
-        if self.world > 1:
+        if self._nat(t) and self._nat(out):
+            from . import _lib
+            _lib.check(_lib.load().mlr_comm_allgather(
+                self.native, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(out.data_ptr()), t.numel(), 8,
+                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        elif self.world > 1:
             if dist.get_backend(self.group) == "nccl":
                 dist.all_gather_into_tensor(out, t, group=self.group)
             else:

@@ -126,3 +126,40 @@ def test_cli_bridge_rebinds_and_restores():
     cli_bridge.uninstall(mod, prev)
     assert mod.ialm_solve is cpu and mod.ml_ialm_solve is cpu and mod.fwt_solve is cpu and mod.ml_fwt_solve is cpu
     assert mod._numerical_rank is cpu and mod.io is io
+
+
+def test_cli_compare_cpu_vs_gpu_names(reference, tmp_path, capsys):
+    """`mlrpca compare --solver-a ml-ialm --solver-b ml-ialm-gpu` (cli.py:336-361)
+    runs the reference solver for 'a' and the bound GPU solver for 'b'; the
+    GPU solvers are stand-ins here (no device), counting their calls."""
+    import numpy as np
+    import mlrpca.cli as cli
+    from mlrpca import io as rio
+    from paper_2206_13369_b200 import cli_bridge
+    calls = []
+
+    def fake(name, fn):
+        def run(*a, **k):
+            calls.append(name)
+            return fn(*a, **k)
+        return run
+
+    gpu = {"ml_ialm_solve": fake("ml_ialm_solve", reference.ml_ialm_solve),
+           "ialm_solve": fake("ialm_solve", reference.ialm_solve),
+           "ml_fwt_solve": fake("ml_fwt_solve", reference.ml_fwt_solve),
+           "fwt_solve": fake("fwt_solve", reference.fwt_solve)}
+    d = np.random.default_rng(3).standard_normal((40, 32))
+    rio.save_matrix(d, tmp_path / "d.lrml")
+    prev = cli_bridge.install_side_by_side(cli, gpu)
+    try:
+        rc = cli.main(["compare", "--input", str(tmp_path / "d.lrml"), "--solver-a", "ml-ialm",
+                       "--solver-b", "ml-ialm-gpu", "--levels", "8", "--out", str(tmp_path / "out")])
+        assert rc in (0, 1)
+        assert calls == ["ml_ialm_solve"]  # only 'b' ran on the (stand-in) GPU solver
+        assert (tmp_path / "out" / "metrics_a.csv").exists() and (tmp_path / "out" / "metrics_b.csv").exists()
+        assert cli.ml_ialm_solve is not gpu["ml_ialm_solve"]  # bindings restored after the GPU call
+        out = capsys.readouterr().out
+        assert "ml-ialm-gpu" in out and "ml-ialm," in out
+    finally:
+        for k, v in prev.items():
+            setattr(cli, k, v)

@@ -100,3 +100,48 @@ def test_cpcp_rows_two_ranks_match_one():
     assert abs(obj[0] - one.objective_history[0]) <= 1e-9 * one.objective_history[0]
     assert abs(res[0][4] - one.iter) <= max(2, int(0.05 * one.iter))
     assert abs(obj[-1] - one.objective_history[-1]) / one.objective_history[-1] <= 1e-3
+
+
+def test_native_nccl_communicator_one_rank():
+    """The library's own NCCL communicator (mlr_comm_*: dlopen'd NCCL, unique
+    id exchanged through torch.distributed once) drives every collective of
+    the row-sharded loops; on the one-GPU box a one-rank NCCL group runs the
+    same calls (all-reduce in place, all-gather) and must reproduce the
+    single-GPU solves bit for bit."""
+    import ctypes
+    import paper_2206_13369_b200 as pkg
+    from oracle import mlrpca_oracle as O
+    from paper_2206_13369_b200 import _lib, runtime
+
+    lib = _lib.load()
+    assert lib.mlr_comm_available() == 1
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    os.environ["MLR_FORCE_NATIVE_NCCL"] = "1"
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        c = runtime.Comm()
+        assert c.native is not None and lib.mlr_comm_size(c.native) == 1
+        x = torch.arange(10, dtype=torch.float64, device="cuda")
+        c.sum(x)
+        c.max(x)
+        out = torch.zeros(10, dtype=torch.float64, device="cuda")
+        c.gather(out, x)
+        torch.cuda.synchronize()
+        assert torch.equal(x, torch.arange(10, dtype=torch.float64, device="cuda")) and torch.equal(out, x)
+        d, _ = O.gaussian_rpca(150, 120, 5, 0.1, 31)
+        one = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=30, tol_feasibility=1e-7))
+        st = pkg.ml_ialm_solve_rows(torch.from_numpy(d).cuda(), pkg.PcpOptions(levels=30, tol_feasibility=1e-7), 150)
+        assert st.iter == one.iter and np.array_equal(st.l.cpu().numpy(), one.l)
+        d2, mask = O.gaussian_rpca(150, 120, 4, 0.1, 32, observe=0.8)
+        lam = 1 / np.sqrt(150)
+        opts = pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(150), tol=1e-6, max_iters=300, levels=30,
+                               collect_rank=False)
+        one2 = pkg.ml_fwt_solve(d2, pkg.ObservationMask(mask), opts)
+        st2 = pkg.ml_fwt_solve_rows(torch.from_numpy(d2).cuda(), pkg.ObservationMask(mask), opts, 150, 0)
+        assert st2.iter == one2.iter and st2.objective_history == one2.objective_history
+    finally:
+        os.environ.pop("MLR_FORCE_NATIVE_NCCL", None)
+        runtime._NATIVE.clear()
+        dist.destroy_process_group()
