@@ -97,6 +97,14 @@ int mlr_comm_allgather(void* comm, const void* in, void* out, int64_t count, int
 int mlr_comm_rank(void* comm);
 int mlr_comm_size(void* comm);
 
+/* ---------------------------------------------------------------- tensor cores
+ * Test entry of the reconstruction kernel FP32 plans use for Z = A W~ (the
+ * L_H = U_r diag(sigma_r - tau) V_r^T step, pcp.py:258-266): 3xTF32
+ * tcgen05.mma with TMEM accumulators and TMA operand loads (tc_gemm.cu).
+ * Z (m x np FP32, ld np) = A (m x np FP32, ld np) W (np x np FP64, row-major);
+ * np % 64 == 0; work: np^2 doubles + 2 np^2 floats.  Synchronous. */
+int mlr_tc_gemm_tf32x3(int64_t m, int np, const float* A, const double* W, float* Z, void* work, void* stream);
+
 /* ---------------------------------------------------------------- ML-PCP */
 int64_t mlr_pcp_workspace_bytes(void* chain, int64_t m_local, int f32, int max_iters);
 int mlr_pcp_create(void* chain, int64_t m_local, int64_t m_global, int f32, int max_iters, void* workspace,

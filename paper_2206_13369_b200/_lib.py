@@ -44,6 +44,8 @@ _SIGS = {
     "mlr_comm_allgather": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "mlr_comm_rank": (c_int, [c_void_p]),
     "mlr_comm_size": (c_int, [c_void_p]),
+    # 3xTF32 tcgen05 reconstruction GEMM (test entry)
+    "mlr_tc_gemm_tf32x3": (c_int, [c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     # ML-PCP
     "mlr_pcp_workspace_bytes": (c_int64, [c_void_p, c_int64, c_int, c_int]),
     "mlr_pcp_create": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_void_p, POINTER(c_void_p)]),

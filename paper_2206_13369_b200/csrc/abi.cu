@@ -114,6 +114,10 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
   p.Xm = c.take<double>(8 * nn);
   p.Vm = c.take<double>(8 * nn);
   p.Wm = c.take<double>(8 * nn);
+  if (p.tc_recon) {
+    p.w_hi = c.take<float>(4 * nn);
+    p.w_lo = c.take<float>(4 * nn);
+  }
   p.sig = c.take<double>(8 * np);
   p.fw = c.take<double>(8 * np);
   p.qbuf = c.take<double>(8 * (size_t)jacobi2_qbuf_elems(np));
@@ -134,7 +138,7 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
 // 440 CTAs = 2.97 waves of 148; the old one-wave rule gave 2 slices -> 110
 // CTAs on 148 SMs).
 static int64_t gram128_splits(int64_t b128, int sms, int64_t m_local) {
-  if (2 * b128 <= sms) return std::max<int64_t>(1, sms / b128);
+  if (4 * b128 <= sms) return std::max<int64_t>(1, sms / b128);
   int64_t best = 1;
   double best_e = 0.0;
   for (int64_t s = 1; s <= 16; ++s) {
@@ -185,8 +189,8 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
     p.lz_fused_ctas = fused ? (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(m_local, 1), 8), sms))
                             : 0;
     const char* lg = getenv("MLR_LZ_LONG");
-    // n <= 2 CTAs x 512 threads x 6 float4 groups; seg x 4 B per stage, >= 4 stages
-    p.lz_long_clusters = (f32 && ch.n > 2048 && ch.n % 4 == 0 && ch.n <= 24576 && !(lg && lg[0] == '0'))
+    // n <= 2 CTAs x 512 threads x 5 float4 groups (20480); seg x 4 B per stage, >= 4 stages
+    p.lz_long_clusters = (f32 && ch.n > 2048 && ch.n % 4 == 0 && ch.n <= 20480 && !(lg && lg[0] == '0'))
                              ? sms / 2 : 0;
     const char* r = getenv("MLR_LZ_RUN");
     p.lz_run_ctas = (ch.n <= 4096 && m_local > 0 && !(r && r[0] == '0')) ? sms : 0;
@@ -194,6 +198,10 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
     if (p.lz_run_ctas && rc) p.lz_run_ctas = std::max(1, std::min(sms, atoi(rc)));
   }
   p.lz_kmax = std::min(500, std::max(8, ch.n));
+  {
+    const char* e = getenv("MLR_TC_RECON");
+    p.tc_recon = f32 && tc_recon_bn(ch.np) > 0 && !(e && e[0] == '0');
+  }
   {
     const char* e = getenv("MLR_EIG_SORT");
     p.eig_sort = e ? atoi(e) : 1;  // measured: C2 Jacobi -7%, C5 -6%
@@ -494,6 +502,13 @@ int mlr_pcp_create(void* chain, int64_t m_local, int64_t m_global, int f32, int 
   pcp_params(*p, ((Chain*)chain)->d, m_local, m_global, f32, max_iters);
   Carver c(workspace);
   carve_pcp(*p, c);
+  if (p->tc_recon && m_local > 0) {
+    const int rc = tc_recon_setup(&p->tc, (const float*)p->A, m_local, p->ch.np, p->w_hi, p->w_lo);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+  }
   eye_kernel<<<256, 256>>>(p->Vm, p->ch.np);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {

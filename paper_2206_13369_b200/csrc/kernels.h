@@ -1,5 +1,6 @@
 // Internal (C++) interfaces between the ABI layer and the kernel files.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,6 +36,19 @@ int matrix_to_frames(const void* x, int64_t ldx, bool f32, int count, int H, int
                      cudaStream_t st);
 int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st,
                const int* skip = nullptr);
+
+// 3xTF32 tcgen05 reconstruction Z = A W~ (tc_gemm.cu): TMA tensor maps of A
+// and the TF32 hi / lo parts of W~^T, built once per plan
+struct TcRecon {
+  CUtensorMap mapA, mapBhi, mapBlo;
+  int64_t M;
+  int np, bn;
+  bool ready;
+};
+int tc_recon_bn(int np);
+int tc_recon_setup(TcRecon* r, const float* A, int64_t M, int np, const float* Whi, const float* Wlo);
+int tc_recon_run(const TcRecon* r, float* Z, int64_t ldz, const int* skip, cudaStream_t st);
+int tc_split_w(const double* Wt, float* hi, float* lo, int np, const int* skip, cudaStream_t st);
 
 // ---------------------------------------------------------------- jacobi
 

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(LZ_FW * 32, 1) lz_dtdv_kernel(const LanczosDev
 // FP64 partial of w goes to wpart[cluster]; sum_slices adds the clusters in
 // a fixed order (deterministic).  D is read once per Lanczos step instead of
 // twice (lz_dv_kernel + lz_dtv_kernel).
-constexpr int LZL_T = 512, LZL_CL = 2, LZL_R = 2, LZL_NG = 6;  // NG float4 groups per thread: seg <= 12288
+constexpr int LZL_T = 512, LZL_CL = 2, LZL_R = 2, LZL_NG = 5;  // NG float4 groups per thread: seg <= 10240
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
   extern __shared__ __align__(128) unsigned char lzl_smem[];
   __shared__ __align__(8) uint64_t full[16];
   __shared__ double xch[2][LZL_R][LZL_CL];
-  __shared__ double red[LZL_T / 32][LZL_R];
+  __shared__ double red[2][LZL_T / 32][LZL_R];
   uint32_t cr, cid, ncl;
   asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
   asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
@@ -402,13 +402,13 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
   cluster_sync_all();  // both CTAs started: exchange slots may be written
   if (!skip) {
     const int64_t nb = (nrows + LZL_R - 1) / LZL_R;
-    for (int64_t b = 0; b < nb; ++b) {
+    // partial dots of batch b over this CTA's segment -> red[b & 1]
+    auto dots = [&](int64_t b) {
       const int64_t j0 = b * LZL_R;
       const int rr = (int)(nrows - j0 < LZL_R ? nrows - j0 : LZL_R);
-      double part[LZL_R];
 #pragma unroll
       for (int r = 0; r < LZL_R; ++r) {
-        part[r] = 0.0;
+        double pr = 0.0;
         if (r < rr) {
           const int64_t j = j0 + r;
           const int s = (int)(j % stages);
@@ -426,23 +426,33 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
               a1 = fma((double)x.w, qv[g][3], a1);
             }
           }
-          part[r] = warp_sum(a0 + a1);
+          pr = warp_sum(a0 + a1);
         }
+        if (lane == 0) red[b & 1][warp][r] = pr;
       }
-      if (lane == 0)
-#pragma unroll
-        for (int r = 0; r < LZL_R; ++r) red[warp][r] = part[r];
+    };
+    // warp 0: the CTA's partial of each row of batch b (fixed order) -> both
+    // CTAs' exchange slots, then this thread's half of cluster barrier b
+    auto post = [&](int64_t b) {
+      if (warp == 0 && lane < LZL_R) {
+        double v = 0.0;
+        for (int w = 0; w < LZL_T / 32; ++w) v += red[b & 1][w][lane];
+        for (uint32_t c = 0; c < LZL_CL; ++c) dsmem_st_f64(&xch[b & 1][lane][cr], c, v);
+      }
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    };
+    if (nb > 0) {
+      dots(0);
       __syncthreads();
-      if (warp == 0) {
-        // lanes 0..R-1 sum the warps' partials of row r in a fixed order and
-        // post them to both CTAs of the pair
-        if (lane < LZL_R) {
-          double v = 0.0;
-          for (int w = 0; w < LZL_T / 32; ++w) v += red[w][lane];
-          for (uint32_t c = 0; c < LZL_CL; ++c) dsmem_st_f64(&xch[b & 1][lane][cr], c, v);
-        }
-      }
-      cluster_sync_all();
+      post(0);
+    }
+    // Software pipeline: the dots of batch b + 1 run while cluster barrier b
+    // completes; then t(b) and the accumulation of batch b.
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t j0 = b * LZL_R;
+      const int rr = (int)(nrows - j0 < LZL_R ? nrows - j0 : LZL_R);
+      if (b + 1 < nb) dots(b + 1);
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
       double t[LZL_R];
 #pragma unroll
       for (int r = 0; r < LZL_R; ++r) {
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
           }
         }
       }
-      __syncthreads();  // every thread is done with this batch's stages
+      __syncthreads();  // batch b's stages are consumed; red[(b + 1) & 1] is complete
       if (tid == 0 && bytes > 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int r = 0; r < rr; ++r) {
@@ -481,6 +491,7 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
           }
         }
       }
+      if (b + 1 < nb) post(b + 1);
     }
   }
   double* o = wpart + (int64_t)cid * n + col0;
@@ -1825,12 +1836,25 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   // rank-0 iteration has W~ = 0 and Z = 0: the products are skipped
   // (jac_skip) and Z is cleared instead.
   skip = &p->dev->jac_skip;
+  const bool tc = p->tc_recon && p->m_local > 0;
   if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;
-  if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw))) return rc;
+  if (tc) {
+    // W~^T = V diag(f) U'^T (the tcgen05 B operand is K-major), then its TF32 hi / lo parts
+    if ((rc = mm(p->Vm, false, p->T1, true, p->Wm, p->fw))) return rc;
+    if ((rc = tc_split_w(p->Wm, p->w_hi, p->w_lo, np, skip, st))) return rc;
+  } else if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw))) {
+    return rc;
+  }
   p->timer.end(kPhPost, st);
   // Z = A W~
   p->timer.begin(st);
-  if (p->m_local > 0) {
+  if (tc) {
+    if ((rc = tc_recon_run(&p->tc, (float*)p->Z, np, skip, st))) return rc;
+    const int64_t zn = p->m_local * np;
+    pcp_zero_if_rank0<<<(int)std::min<int64_t>(ceil_div(zn, 1024), 1184), 256, 0, st>>>(
+        p->dev, reinterpret_cast<uint32_t*>(p->Z), zn);
+    MLR_LAUNCH_CHECK("pcp_zero_if_rank0");
+  } else if (p->m_local > 0) {
     GemmSpec z{};
     z.M = (int)p->m_local; z.N = np; z.K = np;
     z.A = p->A; z.lda = np; z.a_f32 = p->f32; z.trans_a = false;

@@ -63,7 +63,10 @@ struct PcpPlan {
   void* Z;             // m_local x np (T)
   double* gram_part;   // gram_splits x np x np
   double* row_part;    // row_blocks x 4
-  double *T1, *Bm, *Xm, *Vm, *Wm;   // np x np: U, T, B~ (Jacobi), V (eigenvectors), W~
+  double *T1, *Bm, *Xm, *Vm, *Wm;   // np x np: U, T, B~ (Jacobi), V (eigenvectors), W~ (W~^T on the tcgen05 path)
+  bool tc_recon;                    // FP32: Z = A W~ by the 3xTF32 tcgen05 kernel (tc_gemm.cu)
+  float *w_hi, *w_lo;               // np x np: TF32 hi / lo parts of W~^T
+  TcRecon tc;
   double* qbuf;        // Jacobi per-pair rotations
   int* qflag;
   double *sig, *fw;    // np

@@ -348,3 +348,31 @@ def test_lanczos_long_rows_sigma1(m, n):
     st = pkg.ml_ialm_solve(d32, opts)
     s1 = np.linalg.norm(d32.astype(np.float64), 2)
     assert np.isclose(st.mu_history[0], 1.25 / s1, rtol=1e-8)
+
+
+# ------------------------------------------------------------------ tcgen05 3xTF32 GEMM
+@pytest.mark.parametrize("m,np_", [(300, 256), (1000, 1280), (129, 320), (64, 384)])
+def test_tcgen05_tf32x3_gemm_vs_fp64(m, np_):
+    """Z = A W on the tensor cores (kind::tf32, 3 products, TMEM accumulator,
+    TMA-loaded 128B-swizzled tiles) against an FP64 product: FP32-class
+    error relative to |A| |W| (the partial last 128-row tile included)."""
+    import ctypes
+    import torch
+    from paper_2206_13369_b200 import _lib
+    rng = np.random.default_rng(np_ + m)
+    a = rng.standard_normal((m, np_)).astype(np.float32)
+    w = rng.standard_normal((np_, np_)) / np.sqrt(np_)
+    A = torch.from_numpy(a).cuda()
+    W = torch.from_numpy(w).cuda()
+    Z = torch.full((m, np_), float("nan"), dtype=torch.float32, device="cuda")
+    work = torch.empty(np_ * np_ * 2, dtype=torch.float64, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.mlr_tc_gemm_tf32x3(m, np_, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(W.data_ptr()),
+                                      ctypes.c_void_p(Z.data_ptr()), ctypes.c_void_p(work.data_ptr()),
+                                      ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    z = Z.cpu().numpy().astype(np.float64)
+    ref = a.astype(np.float64) @ w
+    scale = np.abs(a).astype(np.float64) @ np.abs(w)
+    err = np.abs(z - ref) / scale
+    assert np.isfinite(z).all()
+    assert err.max() <= 4e-6, err.max()  # ~2^-21 per product + FP32 accumulation over K
