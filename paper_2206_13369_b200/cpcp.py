@@ -10,6 +10,7 @@ and the 5-iteration convergence window all run on the device.
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import numpy as np
 import torch
@@ -22,6 +23,7 @@ from .runtime import SINGLE, Comm, as_device_matrix, give_back, give_back_all
 
 # When set to a list, solves record per-phase CUDA-event timings into it.
 TIMING_SINK = None
+VERIFY_REPLICATED = os.environ.get("MLR_VERIFY_REPLICATED") == "1"  # see pcp.VERIFY_REPLICATED
 # When set to a list, solves append their final device state (dict of
 # mlr_cpcp_state: k, corner flags, the l1 arg-max (i_s, j_s), ...): tests.
 STATE_SINK = None
@@ -96,6 +98,9 @@ def run_fwt(be, comm, D, maskbits, m_global, opts, radius, check_every, probe=No
             be.gram()
             comm.sum(be.red[:ns])
             comm.gather(be.amax_all, be.amax)
+            if VERIFY_REPLICATED:
+                comm.check_replicated(be.red[:ns], "K_g + stats")
+                comm.check_replicated(be.amax_all, "arg-max records")
             be.finalize()
         # pipelined polling (see pcp.run_ialm)
         token = be.snapshot()

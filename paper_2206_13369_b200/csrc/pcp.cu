@@ -668,7 +668,8 @@ __device__ __forceinline__ double lz_cluster_sum(cg::cluster_group& cl, double* 
 }
 
 __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double* __restrict__ Q,
-                                                           const double* __restrict__ w_in, int n, double tol) {
+                                                           const double* __restrict__ w_in, int n, double tol,
+                                                           int passes) {
   if (lz->done) return;
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
@@ -712,8 +713,10 @@ __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double
     w[j] = v;
   }
   __syncthreads();
-  // full reorthogonalisation, twice (classical Gram-Schmidt)
-  for (int pass = 0; pass < 2; ++pass) {
+  // full reorthogonalisation, `passes` times (classical Gram-Schmidt); one
+  // pass by default, as in lz_run_kernel: only the top Ritz value is used,
+  // and it is insensitive to the residual non-orthogonality
+  for (int pass = 0; pass < passes; ++pass) {
     double* ph = part + 2 + pass * K;
     for (int c = wid; c < K; c += LZ_T / 32) {
       const double* qc = Q + (int64_t)c * n + j0;
@@ -1362,7 +1365,12 @@ int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStre
   MLR_CUDA(cudaFuncSetAttribute(lz_update_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   MLR_CUDA(cudaFuncSetAttribute(lz_update_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   p->timer.begin(st);
-  MLR_CUDA(cudaLaunchKernelEx(&cfg, lz_update_cluster, p->lz, p->lzQ, w_reduced, n, tol));
+  static int passes = -1;
+  if (passes < 0) {
+    const char* pe = getenv("MLR_LZ_CL_REORTH");
+    passes = pe ? std::max(0, std::min(2, atoi(pe))) : 1;
+  }
+  MLR_CUDA(cudaLaunchKernelEx(&cfg, lz_update_cluster, p->lz, p->lzQ, w_reduced, n, tol, passes));
   p->timer.end(kPhLanczos, st);
   return kOk;
 }

@@ -10,6 +10,8 @@ never idle waiting for Python.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -19,6 +21,9 @@ from .chain import build_chain, resolve_coarse_width
 from .runtime import SINGLE, Comm, as_device_matrix, give_back, give_back_all
 
 LANCZOS_TOL = 1e-15
+# Debug: check that the all-reduced Gram every rank feeds its replicated
+# Jacobi is bitwise identical across ranks (runtime.Comm.check_replicated).
+VERIFY_REPLICATED = os.environ.get("MLR_VERIFY_REPLICATED") == "1"
 
 # When set to a list, solves record per-phase CUDA-event timings into it
 # (one dict per solve; used by bench.py for the roofline figures).
@@ -103,6 +108,8 @@ def run_ialm(be, comm, D, m_global, n, opts, lam, check_every, coarse=None):
             calls += 1
             be.gram(1)
             comm.sum(be.red[:ns])
+            if VERIFY_REPLICATED:
+                comm.check_replicated(be.red[:ns], "coarse Gram + stats")
             be.finalize()
         # pipelined polling: the next batch is queued before this one's state
         # is read; once done, every further step is a no-op on the device

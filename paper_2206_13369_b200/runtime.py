@@ -100,6 +100,28 @@ class Comm:
                 dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return t
 
+    def check_replicated(self, t, what):
+        """Debug (MLR_VERIFY_REPLICATED=1): the all-reduced buffer every rank
+        feeds its replicated eigensolver / LMO must be bitwise identical on
+        all ranks (NCCL's all-reduce guarantees it; this checks it).  Raises
+        RuntimeError naming the first rank that differs."""
+        if self.world <= 1:
+            return
+        bits = t.contiguous().view(torch.int64)
+        h = torch.stack([bits.sum(), (bits * torch.arange(1, bits.numel() + 1, device=bits.device)).sum()])
+        hd = h
+        out = torch.zeros(2 * self.world, dtype=torch.int64, device=h.device)
+        if self._host(h) or not h.is_cuda or self.native is None:
+            parts = [torch.empty_like(hd.cpu()) for _ in range(self.world)]
+            dist.all_gather(parts, hd.cpu() if self._host(h) else hd, group=self.group)
+            out = torch.cat([x.to(out.device) for x in parts])
+        else:
+            dist.all_gather_into_tensor(out, hd, group=self.group)
+        got = out.view(self.world, 2).cpu()
+        for r in range(1, self.world):
+            if not torch.equal(got[r], got[0]):
+                raise RuntimeError(f"replicated {what} differs between rank 0 and rank {r}")
+
     def gather(self, out, t):
         """out (world * t.numel()) <- concatenation of every rank's t."""
         if self._nat(t) and self._nat(out):

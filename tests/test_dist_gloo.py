@@ -123,3 +123,13 @@ def test_time_budget_decision_is_collective(kind):
     same iteration (no hang, no mismatched collective counts)."""
     two = _run(kind + "_budget", 2)
     assert two[0][4] == two[1][4] == 1
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("kind", ["pcp", "cpcp"])
+def test_replicated_inputs_bitwise_equal(kind, monkeypatch):
+    """MLR_VERIFY_REPLICATED=1: every iteration all-gathers a hash of the
+    all-reduced Gram (+ arg-max records) and raises if any rank differs."""
+    monkeypatch.setenv("MLR_VERIFY_REPLICATED", "1")
+    two = _run(kind, 2)
+    assert two[0][4] == two[1][4]

@@ -45,21 +45,25 @@ def launch_table(path, title):
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active",
-           "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+           "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+           "launch__grid_size", "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "smsp__issue_active.avg.pct_of_peak_sustained_active"]
 
 
 def full_table(rep, title):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                         capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
-    lines = [f"# {title}", "", f"source: `{rep}` (ncu --set full --clock-control none)", ""]
+    lines = [f"## {title}", "", f"source: `{rep}` (ncu --set full --clock-control none)", ""]
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         u = dict(zip(hdr, units))
-        lines.append(f"## `{d.get('Kernel Name', '?').split('(')[0]}` grid {d.get('Grid Size')} block {d.get('Block Size')}")
+        lines.append(f"### `{d.get('Kernel Name', '?').split('(')[0]}` grid {d.get('Grid Size')} block {d.get('Block Size')}")
         lines.append("")
         lines.append("| metric | value |")
         lines.append("|---|---|")
@@ -71,5 +75,10 @@ def full_table(rep, title):
 
 
 if __name__ == "__main__":
-    mode, path, title = sys.argv[1], sys.argv[2], sys.argv[3]
-    print(launch_table(path, title) if mode == "launches" else full_table(path, title))
+    mode, title, paths = sys.argv[1], sys.argv[2], sys.argv[3:]
+    if mode == "launches":
+        print(launch_table(paths[0], title))
+    else:
+        print(f"# {title}\n")
+        for p in paths:
+            print(full_table(p, p.rsplit("/", 1)[-1]))
