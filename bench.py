@@ -74,7 +74,7 @@ def _peaks():
     p = _json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {"hbm_gbs": 6650.0, "_fallback": True}
     own = _json(os.path.join(ROOT, "profiles", "peaks_b200.json")) or {}
     p = dict(p)
-    for k in ("fp64_mma_tflops", "fp32_ffma_tflops", "tf32_mma_tflops"):
+    for k in ("fp64_mma_tflops", "fp32_ffma_tflops", "tf32_tc_tflops"):
         if k in own:
             p[k] = own[k]
     return p
@@ -331,12 +331,21 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic, 
         "hbm", b * (3 * m * n + 2 * m * npad), "GB/s", hbm, "b (3 m n + 2 m n_p) bytes")
     add("gram", "gram128_kernel (K = A^T A, FP64 DMMA, symmetric)", "tensor", m * npad * npad, "TFLOP/s", fp64,
         "m n_p^2 flops (symmetric half of 2 m n_p^2)", peak_source=fp64_src)
-    add("recon", "gemm_f64_kernel (Z = A W~, FP64 DMMA)", "tensor", 2.0 * m * npad * npad, "TFLOP/s", fp64,
-        "2 m n_p^2 flops", peak_source=fp64_src)
+    if b == 4:  # FP32 plans: 3xTF32 on tcgen05 (tc_gemm.cu)
+        add("recon", "tc_recon_kernel (Z = A W~, 3xTF32 tcgen05.mma kind::tf32, TMEM accumulator, TMA operands)",
+            "tensor", 3 * 2.0 * m * npad * npad, "TFLOP/s", peaks.get("tf32_tc_tflops", 1100.0),
+            "3 products x 2 m n_p^2 TF32 flops",
+            peak_source="nominal dense TF32 tensor peak, 1100 TF/s (not measured)")
+    else:
+        add("recon", "gemm_f64_kernel (Z = A W~, FP64 DMMA)", "tensor", 2.0 * m * npad * npad, "TFLOP/s", fp64,
+            "2 m n_p^2 flops", peak_source=fp64_src)
     if sweeps:
-        flops = 12.0 * npad ** 3 * statistics.mean(sweeps)
+        # per sweep: B~ <- J^T B~ J on the symmetric half (n_p/32 (n_p/32 - 1)/2 block pairs per step,
+        # 2 x 2 x 32^3 flops each, n_p/16 steps: 4 n_p^3) + V <- V J (4 n_p^3)
+        flops = 8.0 * npad ** 3 * statistics.mean(sweeps)
         add("jacobi", "jacobi2_kernel + j2_vapply_kernel (FP64 two-sided block Jacobi on B~)", "tensor", flops,
-            "TFLOP/s", fp64, "12 n_p^3 flops per sweep x mean sweeps", tkey="jacobi2_kernel", peak_source=fp64_src)
+            "TFLOP/s", fp64, "8 n_p^3 flops per sweep (4 n_p^3 symmetric B~ update + 4 n_p^3 V update) x mean "
+            "sweeps", tkey="jacobi2_kernel", peak_source=fp64_src)
     return out
 
 
@@ -457,6 +466,13 @@ def gpu_arm(args, name, cfg, world, rank, local):
     roof = rl.get(dominant) or rl.get("update")
     per_iter = {k: round(v / k_solve, 4) for k, v in phase_ms.items()}
 
+    secondary = {}
+    if world == 1 and not args.no_secondary:
+        del D, d_pin
+        torch.cuda.empty_cache()
+        if name != "C2":
+            secondary["C2"] = pcp_secondary(dev, args.seed, flush)
+        secondary.update(cpcp_secondary(dev, args.seed, flush))
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = len(os.sched_getaffinity(0))
@@ -468,13 +484,6 @@ def gpu_arm(args, name, cfg, world, rank, local):
                          f"FP64 on the FP32-rounded input), {secs:.1f} s; sigma_1 by an untimed 30-step Lanczos "
                          f"({setup:.1f} s setup)", **host_info()}
 
-    secondary = {}
-    if world == 1 and not args.no_secondary:
-        del D, d_pin
-        torch.cuda.empty_cache()
-        if name != "C2":
-            secondary["C2"] = pcp_secondary(dev, args.seed, flush)
-        secondary.update(cpcp_secondary(dev, args.seed, flush))
     mode = (f"row-sharded x{world} (gloo on one shared device: functional run, NOT a scaling number)" if shared
             else (f"row-sharded x{world}, NCCL all-reduce of the coarse Gram" if world > 1 else "1 GPU"))
     line = {

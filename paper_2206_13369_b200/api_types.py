@@ -22,14 +22,27 @@ class SvdError(RuntimeError):
         self.iterations = iterations
 
 
+PRECISIONS = ("auto", "float64", "float32")
+
+
+def check_precision(p):
+    if p not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}, got {p!r}")
+
+
 @dataclass
 class PcpOptions:
     """pcp.py:20-54.  ``levels`` is the coarse WIDTH n_H (pcp.py:200-210).
 
     GPU-only extras: ``jacobi_tol`` (relative off-diagonal stopping level of
-    the coarse eigensolver; default 64*eps for float64 input, 1e-10 for
-    float32) and ``check_every`` (iterations between host polls of the
-    device-side stopping flag; 1 when ``time_budget`` is set)."""
+    the coarse eigensolver; default 64*eps for float64 data, 1e-6 for
+    float32), ``check_every`` (iterations between host polls of the
+    device-side stopping flag; 1 when ``time_budget`` is set) and
+    ``precision``: "auto" (default) computes and returns in the input's
+    floating type (float32 stays float32, anything else float64);
+    "float64" reproduces the reference exactly in that respect (every input
+    is coerced to float64, linalg.py:48-57, and results are float64);
+    "float32" computes in FP32 for any input."""
 
     lam: float | None = None
     mu0: float | None = None
@@ -43,8 +56,10 @@ class PcpOptions:
     time_budget: float | None = None
     jacobi_tol: float | None = None
     check_every: int | None = None
+    precision: str = "auto"
 
     def validate(self):
+        check_precision(self.precision)
         if self.lam is not None and self.lam <= 0:
             raise ValueError("lam must be positive")
         if self.mu0 is not None and self.mu0 <= 0:
@@ -156,8 +171,10 @@ class CpcpOptions:
     collect_rank: bool = True
     track_oracle_atoms: bool = False
     check_every: int | None = None
+    precision: str = "auto"  # as PcpOptions.precision
 
     def validate(self):
+        check_precision(self.precision)
         if self.lambda_l <= 0 or self.lambda_s <= 0:
             raise ValueError("penalty weights must be positive")
         if self.tol <= 0:

@@ -165,7 +165,7 @@ def ml_fwt_solve(d, mask=None, opts=None):
     """Multilevel Frank-Wolfe thresholding (drop-in for mlrpca.ml_fwt_solve)."""
     if opts is None:
         raise ValueError("CpcpOptions with penalty weights is required")
-    D, kind = as_device_matrix(d, "d")
+    D, kind = as_device_matrix(d, "d", opts.precision)
     m, n = D.shape
     with torch.cuda.device(D.device):
         nh = resolve_coarse_width(n, m, opts.levels, opts.rank_guess)
@@ -213,7 +213,7 @@ def ml_fwt_solve_rows(d_local, mask_local, opts, m_global, row0, group=None):
     over ``group``."""
     if opts is None:
         raise ValueError("CpcpOptions with penalty weights is required")
-    D, kind = as_device_matrix(d_local, "d")
+    D, kind = as_device_matrix(d_local, "d", opts.precision)
     m, n = D.shape
     comm = Comm(group)
     with torch.cuda.device(D.device):

@@ -181,9 +181,9 @@ def ml_ialm_solve(d, opts=None):
     input's side).  ``opts.levels`` is the coarse width n_H, as in the
     reference.  Raises ValueError / LevelError / SvdError like the reference.
     """
-    D, kind = as_device_matrix(d, "d")
-    m, n = D.shape
     opts = opts if opts is not None else PcpOptions()
+    D, kind = as_device_matrix(d, "d", opts.precision)
+    m, n = D.shape
     lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m, n))
     diag = None
     with torch.cuda.device(D.device):
@@ -224,9 +224,9 @@ def ialm_solve(d, opts=None):
     shrinkages are), so a wide ``d`` is solved as its transpose and the
     Gram stays min(m, n) square.
     """
-    D, kind = as_device_matrix(d, "d")
-    m, n = D.shape
     opts = opts if opts is not None else PcpOptions()
+    D, kind = as_device_matrix(d, "d", opts.precision)
+    m, n = D.shape
     lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m, n))
     wide = n > m
     if wide:
@@ -274,7 +274,7 @@ def ml_ialm_solve_rows(d_local, opts, m_global, group=None):
     """Row-sharded ML-IALM: this rank holds rows of the global m_global x n
     iterate; K = A^T A and the per-iteration reductions are all-reduced over
     ``group`` (NCCL).  Returns a PcpState whose arrays are this rank's rows."""
-    D, kind = as_device_matrix(d_local, "d")
+    D, kind = as_device_matrix(d_local, "d", opts.precision)
     m, n = D.shape
     comm = Comm(group)
     lam = opts.lam if opts.lam is not None else 1.0 / np.sqrt(max(m_global, n))

@@ -150,7 +150,7 @@ def require_cuda():
         raise RuntimeError("paper_2206_13369_b200 requires a CUDA (sm_100a) device; no CPU fallback exists")
 
 
-def as_device_matrix(x, name="d"):
+def as_device_matrix(x, name="d", precision="auto"):
     """Validate like as_matrix (linalg.py:48-57, finiteness is checked on the
     device) and return (tensor on GPU, kind) where kind records how to give
     results back: "numpy", "torch-cpu" or "torch-cuda"."""
@@ -166,7 +166,7 @@ def as_device_matrix(x, name="d"):
             raise ValueError(f"{name} must have positive dimensions, got {tuple(t.shape)}")
         if not t.is_cuda:
             t = t.to(torch.device("cuda", torch.cuda.current_device()), non_blocking=t.is_pinned())
-        return t.contiguous(), kind
+        return _with_precision(t.contiguous(), precision), kind
     a = np.asarray(x)
     if a.dtype != np.float32:
         a = np.asarray(a, dtype=np.float64)
@@ -175,7 +175,19 @@ def as_device_matrix(x, name="d"):
     if a.shape[0] < 1 or a.shape[1] < 1:
         raise ValueError(f"{name} must have positive dimensions, got {a.shape}")
     t = torch.from_numpy(np.ascontiguousarray(a)).to(torch.device("cuda", torch.cuda.current_device()))
-    return t, "numpy"
+    return _with_precision(t, precision), "numpy"
+
+
+def _with_precision(t, precision):
+    """PcpOptions / CpcpOptions.precision: "auto" keeps the input's type
+    (float32 or float64), "float64" / "float32" convert on the device."""
+    if precision not in ("auto", "float64", "float32"):
+        raise ValueError(f"precision must be one of ('auto', 'float64', 'float32'), got {precision!r}")
+    if precision == "float64" and t.dtype != torch.float64:
+        return t.to(torch.float64)
+    if precision == "float32" and t.dtype != torch.float32:
+        return t.to(torch.float32)
+    return t
 
 
 def give_back_all(ts, kind):

@@ -376,3 +376,22 @@ def test_tcgen05_tf32x3_gemm_vs_fp64(m, np_):
     err = np.abs(z - ref) / scale
     assert np.isfinite(z).all()
     assert err.max() <= 4e-6, err.max()  # ~2^-21 per product + FP32 accumulation over K
+
+
+# ------------------------------------------------------------------ precision option
+def test_precision_option_is_explicit():
+    """precision="auto" follows the input type; "float64" is the reference's
+    behaviour (coerce to float64, return float64) for any input; "float32"
+    forces the FP32 path."""
+    d, _ = O.gaussian_rpca(200, 160, 8, 0.1, 4)
+    d32 = d.astype(np.float32)
+    auto = pkg.ml_ialm_solve(d32, pkg.PcpOptions(levels=40, tol_feasibility=1e-6))
+    assert auto.l.dtype == np.float32
+    f64 = pkg.ml_ialm_solve(d32, pkg.PcpOptions(levels=40, tol_feasibility=1e-6, precision="float64"))
+    ref = pkg.ml_ialm_solve(d32.astype(np.float64), pkg.PcpOptions(levels=40, tol_feasibility=1e-6))
+    assert f64.l.dtype == np.float64 and f64.iter == ref.iter and np.array_equal(f64.l, ref.l)
+    f32 = pkg.ml_ialm_solve(d32.astype(np.float64), pkg.PcpOptions(levels=40, tol_feasibility=1e-6,
+                                                                   precision="float32"))
+    assert f32.l.dtype == np.float32 and f32.iter == auto.iter and np.array_equal(f32.l, auto.l)
+    with pytest.raises(ValueError, match="precision"):
+        pkg.ml_ialm_solve(d32, pkg.PcpOptions(levels=40, precision="fp16"))
