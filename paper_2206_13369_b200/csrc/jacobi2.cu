@@ -322,6 +322,24 @@ __device__ __forceinline__ void j2_quadrant(Smem& S, const double* __restrict__ 
 // phase B, barrier 2, steps) — read with mlr_debug_j2prof.
 __device__ unsigned long long g_j2prof[16];
 
+// the same for the last CTA (a phase-B worker in split mode): slot 12 barrier
+// wait, 13 ticket grabs / setup, 14 item compute, 15 items processed
+__device__ unsigned long long g_j2prof2[8];
+__device__ __forceinline__ void j2_wmark2(int slot, long long& t0) {
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    const long long t = clock64();
+    atomicAdd(&g_j2prof2[slot], (unsigned long long)(t - t0));
+    t0 = t;
+  }
+}
+__device__ __forceinline__ void j2_wmark(int slot, long long& t0) {
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    const long long t = clock64();
+    atomicAdd(&g_j2prof[slot], (unsigned long long)(t - t0));
+    t0 = t;
+  }
+}
+
 __device__ __forceinline__ void j2_mark(int slot, long long& t0) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t = clock64();
@@ -343,7 +361,7 @@ __global__ void __launch_bounds__(J2_THREADS, 2)
 jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows_v, double tol,
                double abs_floor_rel, int max_sweeps, double* __restrict__ Qlog, int cap,
                int* __restrict__ qflag_log, double* __restrict__ off_slots, int* __restrict__ result,
-               const int* __restrict__ skip, int cache_q, double early_off, int vlog, int dflow) {
+               const int* __restrict__ skip, int cache_q, double early_off, int vlog, int dflow, int tickets) {
   if (skip && *skip) return;
   if (result[7] != 0) return;  // converged or out of sweeps in an earlier launch
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -380,6 +398,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   __shared__ int qf_all[64];
   __shared__ short cur_pair[J2_DF_MAXB], nxt_pair[J2_DF_MAXB], nxt_partner[J2_DF_MAXB];
   __shared__ int s_ticket;
+  __shared__ int s_cand[J2_DF_MAXB / 2], s_ccnt[2];
   const double tol2 = tol * tol;
 
   for (int e = tid; e < nb * npairs; e += J2_THREADS) {
@@ -441,6 +460,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       const int slot = g % cap;
       double* Qbuf = Qlog + (int64_t)slot * npairs * J2_PW * J2_PW;
       int* qflag = qflag_log + slot * npairs;
+      long long tw = clock64();
       long long t0 = clock64();
       if (blockIdx.x == 0 && tid == 0) atomicAdd(&g_j2prof[5], 1ull);
       const int* srow = sched + step * npairs;
@@ -814,9 +834,12 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       }
       if (!CLUSTER) __threadfence();  // barrier.cluster.arrive/wait are release/acquire
       j2_mark(6, t0);
+      if (blockIdx.x == gridDim.x - 1 && tid == 0) tw = clock64();
       j2_sync<CLUSTER>();
       j2_mark(2, t0);
+      j2_wmark(12, tw);
       // ------------------------------------------------ phase B: apply
+      long long tw2 = tw;
       if (!dflow || widx >= 0)
         for (int k = tid; k < npairs; k += J2_THREADS) qf_all[k] = qflag[k];
       const bool last_step = step == nb - 1;
@@ -948,29 +971,41 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         // (see phase A).  Worker w's first ticket is w, the rest come from an
         // atomic counter offset by nworkers; each worker ends with exactly
         // one failing grab and the grab completing the count resets it.
+        j2_wmark2(0, tw2);
         unsigned char* dmark = reinterpret_cast<unsigned char*>(items);
         short* dcrit = reinterpret_cast<short*>(dmark + ((nbitems + 15) & ~15));  // critical items, first in the queue
         int* ctr = tctr + (g & 1);
         for (int it = tid; it < nbitems; it += J2_THREADS) dmark[it] = 0;
         __syncthreads();
-        if (tid == 0) {
-          int nc = 0;
-          if (!last_step)
-            for (int k2 = 0; k2 < npairs; ++k2) {
-              const int nx = sched[(step + 1) * npairs + k2];
-              const int ka = cur_pair[nx & 0xffff], kb = cur_pair[nx >> 16];
-              if (ka != kb) {
-                const int lo = min(ka, kb), hi = max(ka, kb);
-                const int it = lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1);
-                if (!dmark[it]) {
-                  dmark[it] = 1;
-                  dcrit[nc++] = (short)it;
-                }
-              }
+        // Critical items (those holding a next-step pair's off-diagonal block),
+        // in next-step pair order, each once: thread k2 < npairs (<= 64) takes
+        // next-step pair k2, drops duplicates of an earlier pair's item, and
+        // two ballots compact the list.  (A serial thread-0 loop with its
+        // dependent shared loads and integer divisions cost ~8k cycles per
+        // step on every worker at C5.)
+        {
+          int itk = -1;
+          if (tid < npairs && !last_step) {
+            const int nx = sched[(step + 1) * npairs + tid];
+            const int ka = cur_pair[nx & 0xffff], kb = cur_pair[nx >> 16];
+            if (ka != kb) {
+              const int lo = min(ka, kb), hi = max(ka, kb);
+              itk = lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1);
             }
-          s_ticket = nc;
+          }
+          if (tid < J2_DF_MAXB / 2) s_cand[tid] = itk;
+          __syncthreads();
+          bool keep = itk >= 0;
+          for (int j = 0; keep && j < tid; ++j) keep = s_cand[j] != itk;
+          if (keep) dmark[itk] = 1;
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (tid < J2_DF_MAXB / 2 && (tid & 31) == 0) s_ccnt[tid >> 5] = __popc(bal);
+          __syncthreads();
+          if (keep) dcrit[((tid >> 5) ? s_ccnt[0] : 0) + __popc(bal & ((1u << (tid & 31)) - 1u))] = (short)itk;
+          if (tid == 0) s_ticket = s_ccnt[0] + s_ccnt[1];
         }
         __syncthreads();
+        j2_wmark2(1, tw2);
         const int ncrit = s_ticket;
         __syncthreads();
         const int total = ncrit + nbitems;
@@ -982,10 +1017,15 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
           __syncthreads();
           return v;
         };
+        // Static round-robin (default): worker w takes tickets w, w + nworkers, ...
+        // (the critical items are tickets 0 .. ncrit-1, so they still come
+        // first); items cost the same, and the contended atomic ticket counter
+        // (~3 grabs per worker per step, 256 workers on one address) measured
+        // ~12k cycles per step on a worker at C5.  tickets != 0: the queue.
         int tk = widx, last_v = -1;
         for (;;) {
           if (tk >= total) {
-            if (last_v < 0) {  // the pre-assigned ticket was past the end: make the failing grab
+            if (tickets && last_v < 0) {  // the pre-assigned ticket was past the end: make the failing grab
               last_v = grab();
               tk = nworkers + last_v;
               continue;
@@ -1028,9 +1068,13 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
                       }
                     }
               }
+              j2_wmark(13, tw);
+              j2_wmark2(2, tw2);
               j2_item(S, B, np, a1, b1, a2, b2, Qbuf + (int64_t)kA * J2_PW * J2_PW,
                       Qbuf + (int64_t)kB * J2_PW * J2_PW, qf_all[kA] != 0, qf_all[kB] != 0, true, skipmask, w0,
                       w1, g + 1, l0, l1);
+              j2_wmark(14, tw);
+              if (blockIdx.x == gridDim.x - 1 && tid == 0) atomicAdd(&g_j2prof[15], 1ull);
             } else if (split && dmark[it] && tid == 0) {
               // identity critical item: nothing to read, release its owners
               const int xs[2] = {srow[kA] & 0xffff, srow[kA] >> 16};
@@ -1040,10 +1084,14 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
               }
             }
           }
-          last_v = grab();
-          tk = nworkers + last_v;
+          if (tickets) {
+            last_v = grab();
+            tk = nworkers + last_v;
+          } else {
+            tk += nworkers;
+          }
         }
-        if (tid == 0 && last_v == grabs - 1) atomicExch(ctr, 0);
+        if (tickets && tid == 0 && last_v == grabs - 1) atomicExch(ctr, 0);
       }
       if (!CLUSTER && (!dflow || last_step)) __threadfence();
       j2_mark(3, t0);
@@ -1195,6 +1243,8 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   int dflow = 0;
   if (vlog && nb <= J2_DF_MAXB) dflow = 1;
   if (const char* e = getenv("MLR_J2_DFLOW")) dflow = !dflow ? 0 : (e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1));
+  int tickets = 0;  // 1: dynamic phase-B item queue (atomic counter) instead of static round-robin
+  if (const char* e = getenv("MLR_J2_TICKETS")) tickets = e[0] == '1';
   const int max_items = dflow ? 0 : (nitems + nctas - 1) / nctas;
   const size_t item_bytes = dflow ? (size_t)nitems + 2 * (size_t)npairs + 32 : (size_t)max_items * 8;
   const size_t sched = (size_t)nb * npairs * sizeof(int) + item_bytes + (size_t)npairs * sizeof(int) + 64;
@@ -1253,10 +1303,12 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   for (int l = 0; l < std::max(launches, 1); ++l) {
     if (cluster)
       MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<true>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
-                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow));
+                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow,
+                                  tickets));
     else
       MLR_CUDA(cudaLaunchKernelEx(&cfg, jacobi2_kernel<false>, B, V, np, nrows_v, tol, abs_floor_rel, max_sweeps,
-                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow));
+                                  Qlog, cap, qflag_log, off_slots, result, skip, cache_q, early_off, vlog, dflow,
+                                  tickets));
     if (vlog) {
       if (var == 16)
         j2_vapply_kernel<16><<<(nrows_v + 15) / 16, VA_THREADS, vsm, st>>>(V, np, nrows_v, Qlog, cap, qflag_log,
@@ -1267,6 +1319,13 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
       MLR_LAUNCH_CHECK("j2_vapply_kernel");
     }
   }
+  return kOk;
+}
+
+int jacobi2_debug_prof2(unsigned long long* out8) {
+  MLR_CUDA(cudaMemcpyFromSymbol(out8, g_j2prof2, sizeof(unsigned long long) * 8));
+  unsigned long long z[8] = {};
+  MLR_CUDA(cudaMemcpyToSymbol(g_j2prof2, z, sizeof(z)));
   return kOk;
 }
 
