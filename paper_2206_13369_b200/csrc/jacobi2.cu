@@ -184,6 +184,12 @@ __device__ __forceinline__ void tile_mm(const double (*A)[J2_LD], const double (
   }
 }
 
+template <typename Smem>
+__device__ __forceinline__ void j2_item_compute(Smem& S, double* __restrict__ B, int np, int a1, int b1, int a2,
+                                                int b2, bool ra, bool rb, bool store, int skipmask,
+                                                const int* wait0, const int* wait1, int waitval, int* loaded0,
+                                                int* loaded1);
+
 // One off-diagonal pair-block item: out = Q_A^T X Q_B with X = B[pair
 // (a1, b1) columns, pair (a2, b2) columns]; ra / rb say whether Q_A / Q_B are
 // non-identity.  Leaves out in S.X (and its transpose in S.Q2); writes both
@@ -213,6 +219,17 @@ __device__ __forceinline__ void j2_item(Smem& S, double* __restrict__ B, int np,
     if (rb) S.Q2[e >> 5][e & 31] = qb[u];
   }
   __syncthreads();
+  j2_item_compute(S, B, np, a1, b1, a2, b2, ra, rb, store, skipmask, wait0, wait1, waitval, loaded0, loaded1);
+}
+
+// Second half of j2_item: X (and Q_A in S.Q, Q_B in S.Q2 when rotated) are in
+// shared memory, visible to all threads.
+template <typename Smem>
+__device__ __forceinline__ void j2_item_compute(Smem& S, double* __restrict__ B, int np, int a1, int b1, int a2,
+                                                int b2, bool ra, bool rb, bool store, int skipmask,
+                                                const int* wait0, const int* wait1, int waitval, int* loaded0,
+                                                int* loaded1) {
+  const int tid = threadIdx.x;
   if (tid == 0) {  // X is read: its next-step owners may now overwrite their quadrants
     if (loaded0) st_release(loaded0, waitval);
     if (loaded1) st_release(loaded1, waitval);
