@@ -713,9 +713,8 @@ __global__ void __launch_bounds__(LZ_T) lz_update_cluster(LanczosDev* lz, double
     w[j] = v;
   }
   __syncthreads();
-  // full reorthogonalisation, `passes` times (classical Gram-Schmidt); one
-  // pass by default, as in lz_run_kernel: only the top Ritz value is used,
-  // and it is insensitive to the residual non-orthogonality
+  // full reorthogonalisation, `passes` times (classical Gram-Schmidt; none by
+  // default, see pcp_lanczos_update): only the top Ritz value is used
   for (int pass = 0; pass < passes; ++pass) {
     double* ph = part + 2 + pass * K;
     for (int c = wid; c < K; c += LZ_T / 32) {
@@ -1368,7 +1367,13 @@ int pcp_lanczos_update(PcpPlan* p, const double* w_reduced, double tol, cudaStre
   static int passes = -1;
   if (passes < 0) {
     const char* pe = getenv("MLR_LZ_CL_REORTH");
-    passes = pe ? std::max(0, std::min(2, atoi(pe))) : 1;
+    // default 0: the plain three-term recurrence.  Only the top Ritz value
+    // is used (sigma_1 for mu_0 and Y_0); Paige's analysis shows it converges
+    // to the extreme eigenvalue to working accuracy without reorthogonalising
+    // (lost orthogonality only duplicates converged Ritz values).  Measured:
+    // the same 107 steps on C5 and sigma_1 equal to the exact 2-norm to the
+    // tests' 1e-8 (mu); Lanczos 72 -> 60 ms per C5 solve.
+    passes = pe ? std::max(0, std::min(2, atoi(pe))) : 0;
   }
   MLR_CUDA(cudaLaunchKernelEx(&cfg, lz_update_cluster, p->lz, p->lzQ, w_reduced, n, tol, passes));
   p->timer.end(kPhLanczos, st);
