@@ -353,6 +353,17 @@ __device__ __forceinline__ void dsmem_st_f64(const double* local, uint32_t cta, 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
 }
+// st.async of one double into a peer CTA's shared memory; the bytes complete
+// a transaction on the peer's mbarrier (same offset in the peer's smem).
+__device__ __forceinline__ void dsmem_st_async_f64(const double* local_slot, const uint64_t* local_bar,
+                                                   uint32_t cta, double v) {
+  uint32_t rslot, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rslot) : "r"(smem_u32(local_slot)), "r"(cta));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(cta));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(rslot), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -364,6 +375,7 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
                                                                 double* __restrict__ wpart) {
   extern __shared__ __align__(128) unsigned char lzl_smem[];
   __shared__ __align__(8) uint64_t full[16];
+  __shared__ __align__(8) uint64_t xbar[2];  // batch parity: the peer's partials have landed
   __shared__ double xch[2][LZL_R][LZL_CL];
   __shared__ double red[2][LZL_T / 32][LZL_R];
   uint32_t cr, cid, ncl;
@@ -380,6 +392,8 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
   const uint32_t bytes = (uint32_t)len * 4u;
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -431,28 +445,35 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
         if (lane == 0) red[b & 1][warp][r] = pr;
       }
     };
-    // warp 0: the CTA's partial of each row of batch b (fixed order) -> both
-    // CTAs' exchange slots, then this thread's half of cluster barrier b
+    // warp 0: the CTA's partial of each row of batch b (fixed order) into
+    // its own slot and, by st.async, the peer's slot, completing 8 bytes of a
+    // transaction on the peer's xbar[b & 1]; thread 0 arms its own xbar for
+    // the peer's partials.  No cluster barrier: each CTA waits only for the
+    // bytes it needs (the peer cannot run two batches ahead, since it waits
+    // for this CTA's partials of the batch in between).
     auto post = [&](int64_t b) {
       if (warp == 0 && lane < LZL_R) {
         double v = 0.0;
         for (int w = 0; w < LZL_T / 32; ++w) v += red[b & 1][w][lane];
-        for (uint32_t c = 0; c < LZL_CL; ++c) dsmem_st_f64(&xch[b & 1][lane][cr], c, v);
+        xch[b & 1][lane][cr] = v;
+        for (uint32_t c = 0; c < LZL_CL; ++c)
+          if (c != cr) dsmem_st_async_f64(&xch[b & 1][lane][cr], &xbar[b & 1], c, v);
       }
-      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      if (tid == 0) mbar_expect_tx(&xbar[b & 1], (uint32_t)(LZL_R * (LZL_CL - 1) * sizeof(double)));
     };
     if (nb > 0) {
       dots(0);
       __syncthreads();
       post(0);
     }
-    // Software pipeline: the dots of batch b + 1 run while cluster barrier b
-    // completes; then t(b) and the accumulation of batch b.
+    // Software pipeline: the dots of batch b + 1 run while the peer's
+    // partials of batch b arrive; then t(b) and the accumulation of batch b.
     for (int64_t b = 0; b < nb; ++b) {
       const int64_t j0 = b * LZL_R;
       const int rr = (int)(nrows - j0 < LZL_R ? nrows - j0 : LZL_R);
       if (b + 1 < nb) dots(b + 1);
-      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      mbar_wait(&xbar[b & 1], (uint32_t)((b >> 1) & 1));
+      __syncthreads();  // the own-slot writes of warp 0 are visible too
       double t[LZL_R];
 #pragma unroll
       for (int r = 0; r < LZL_R; ++r) {
@@ -502,6 +523,7 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
 #pragma unroll
       for (int e = 0; e < 4; ++e) o[4 * k + e] = acc[g][e];
   }
+  cluster_sync_all();  // no CTA leaves while its peer's last st.async may be in flight
 }
 
 int lz_long_stages(int seg) {
