@@ -339,6 +339,12 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic, 
     else:
         add("recon", "gemm_f64_kernel (Z = A W~, FP64 DMMA)", "tensor", 2.0 * m * npad * npad, "TFLOP/s", fp64,
             "2 m n_p^2 flops", peak_source=fp64_src)
+    lz_steps = real_launches.get("lanczos_steps")
+    if lz_steps and b == 4 and n > 4096:
+        real_launches["lanczos"] = lz_steps
+        add("lanczos", "lz_dtdq_long_kernel + lz_update_cluster (sigma_1: one pass over D per Lanczos step, "
+            "TMA-staged rows, 2-CTA clusters)", "hbm", float(b) * m * n, "GB/s", hbm,
+            "b m n bytes per Lanczos step (D read once)")
     if sweeps:
         # per sweep: B~ <- J^T B~ J on the symmetric half (n_p/32 (n_p/32 - 1)/2 block pairs per step,
         # 2 x 2 x 32^3 flops each, n_p/16 steps: 4 n_p^3) + V <- V J (4 n_p^3)
@@ -460,7 +466,8 @@ def gpu_arm(args, name, cfg, world, rank, local):
     sweeps_all = [x for s in sink for x in s.get("jac_sweeps", [])]
     sweeps = [x for x in sweeps_all if x > 0]
     k_solve = sum(s.get("iters", 0) for s in sink) or 1
-    real = {"update": k_solve, "gram": k_solve + 1, "jacobi": len(sweeps), "recon": len(sweeps)}
+    real = {"update": k_solve, "gram": k_solve + 1, "jacobi": len(sweeps), "recon": len(sweeps),
+            "lanczos_steps": sink[0].get("lanczos_steps") if sink else None}
     rl = roofline_entries(name, cfg, phases, sweeps, r1 - r0, world, peaks, _traffic(name), real)
     dominant = max(phase_ms, key=phase_ms.get) if phase_ms else None
     roof = rl.get(dominant) or rl.get("update")
