@@ -97,6 +97,13 @@ int mlr_comm_allgather(void* comm, const void* in, void* out, int64_t count, int
 int mlr_comm_rank(void* comm);
 int mlr_comm_size(void* comm);
 
+/* ---------------------------------------------------------------- box QP
+ * Test entry of the device box QP of every FW-T step (_solve_box_qp and
+ * _coord_min, cpcp.py:195-231, evaluated in the reference's operation order):
+ * for i < count, (out2[2i], out2[2i+1]) = (ga, gb) of in6[6i..6i+5] =
+ * (aa, bb, ab, la, lb, fallback_gamma; NaN = None).  Device pointers. */
+int mlr_box_qp_batch(const double* in6, double* out2, int count, void* stream);
+
 /* ---------------------------------------------------------------- tensor cores
  * Test entry of the reconstruction kernel FP32 plans use for Z = A W~ (the
  * L_H = U_r diag(sigma_r - tau) V_r^T step, pcp.py:258-266): 3xTF32

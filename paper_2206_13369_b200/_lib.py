@@ -44,6 +44,8 @@ _SIGS = {
     "mlr_comm_allgather": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "mlr_comm_rank": (c_int, [c_void_p]),
     "mlr_comm_size": (c_int, [c_void_p]),
+    # exact box QP of the FW-T step (test entry)
+    "mlr_box_qp_batch": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
     # 3xTF32 tcgen05 reconstruction GEMM (test entry)
     "mlr_tc_gemm_tf32x3": (c_int, [c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     # ML-PCP

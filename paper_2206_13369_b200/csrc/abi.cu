@@ -278,6 +278,9 @@ int mlr_version(void) { return 1; }
 
 // debug: cycle breakdown of the Jacobi kernel (CTA 0); resets the counters
 int mlr_debug_j2prof(unsigned long long* out8) { return mlr::jacobi2_debug_prof(out8); }
+int mlr_box_qp_batch(const double* in6, double* out2, int count, void* stream) {
+  return mlr::box_qp_batch(in6, out2, count, (cudaStream_t)stream);
+}
 int mlr_debug_j2prof2(unsigned long long* out8) { return mlr::jacobi2_debug_prof2(out8); }
 const char* mlr_last_error(void) { return g_err.c_str(); }
 int mlr_device_count(void) {

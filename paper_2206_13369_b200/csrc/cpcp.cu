@@ -841,19 +841,29 @@ __global__ void __launch_bounds__(256) cp_dots_reduce(const double* __restrict__
   }
 }
 
-// _solve_box_qp / _coord_min (cpcp.py:195-231), FP64.
+// _solve_box_qp / _coord_min (cpcp.py:195-231), FP64, evaluated in the
+// reference's operation order with non-contractible intrinsics (no FMA
+// fusion), so the step sizes are bit-identical to numpy's for the same
+// inputs (tests/test_gpu_large.py::test_box_qp_bitwise).
 __device__ double coord_min(double quad, double lin) {
   if (quad <= 0.0) return lin < 0.0 ? 1.0 : 0.0;
-  return fmin(fmax(-lin / quad, 0.0), 1.0);
+  return fmin(fmax(__ddiv_rn(-lin, quad), 0.0), 1.0);
 }
 
 __device__ void box_qp(double aa, double bb, double ab, double la, double lb, double fb, double& ga, double& gb) {
-  auto q = [&](double x, double y) { return 0.5 * (aa * x * x + 2 * ab * x * y + bb * y * y) + la * x + lb * y; };
-  const double det = aa * bb - ab * ab;
+  // value(ga, gb) = .5*(aa*ga*ga + 2*ab*ga*gb + bb*gb*gb) + la*ga + lb*gb, left to right
+  auto q = [&](double x, double y) {
+    double s = __dadd_rn(__dmul_rn(__dmul_rn(aa, x), x), __dmul_rn(__dmul_rn(__dmul_rn(2.0, ab), x), y));
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(bb, y), y));
+    s = __dmul_rn(0.5, s);
+    s = __dadd_rn(s, __dmul_rn(la, x));
+    return __dadd_rn(s, __dmul_rn(lb, y));
+  };
+  const double det = __dsub_rn(__dmul_rn(aa, bb), __dmul_rn(ab, ab));
   bool have = false;
   if (det > 0.0) {
-    const double x = (-la * bb + lb * ab) / det;
-    const double y = (-lb * aa + la * ab) / det;
+    const double x = __ddiv_rn(__dadd_rn(__dmul_rn(-la, bb), __dmul_rn(lb, ab)), det);
+    const double y = __ddiv_rn(__dadd_rn(__dmul_rn(-lb, aa), __dmul_rn(la, ab)), det);
     if (x >= 0.0 && x <= 1.0 && y >= 0.0 && y <= 1.0) {
       ga = x;
       gb = y;
@@ -863,9 +873,9 @@ __device__ void box_qp(double aa, double bb, double ab, double la, double lb, do
   if (!have) {
     double x = 0.0, y = 0.0;
     for (int it = 0; it < 200; ++it) {
-      const double xn = coord_min(aa, la + ab * y);
-      const double yn = coord_min(bb, lb + ab * xn);
-      const bool stop = fabs(xn - x) <= 1e-12 && fabs(yn - y) <= 1e-12;
+      const double xn = coord_min(aa, __dadd_rn(la, __dmul_rn(ab, y)));
+      const double yn = coord_min(bb, __dadd_rn(lb, __dmul_rn(ab, xn)));
+      const bool stop = fabs(__dsub_rn(xn, x)) <= 1e-12 && fabs(__dsub_rn(yn, y)) <= 1e-12;
       x = xn;
       y = yn;
       if (stop) break;
@@ -873,11 +883,31 @@ __device__ void box_qp(double aa, double bb, double ab, double la, double lb, do
     ga = x;
     gb = y;
   }
-  const double gf = fmin(fmax(fb, 0.0), 1.0);
-  if (q(gf, gf) < q(ga, gb)) {
-    ga = gf;
-    gb = gf;
+  if (fb >= 0.0 || fb < 0.0) {  // fallback given (NaN = none, as the reference's None)
+    const double gf = fmin(fmax(fb, 0.0), 1.0);
+    if (q(gf, gf) < q(ga, gb)) {
+      ga = gf;
+      gb = gf;
+    }
   }
+}
+
+// Test entry: out[2i], out[2i+1] = box_qp(in[6i .. 6i+5]) (aa, bb, ab, la, lb, fallback or NaN)
+__global__ void box_qp_batch_kernel(const double* __restrict__ in, double* __restrict__ out, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double* c = in + 6 * (int64_t)i;
+  double ga = 0.0, gb = 0.0;
+  box_qp(c[0], c[1], c[2], c[3], c[4], c[5], ga, gb);
+  out[2 * (int64_t)i] = ga;
+  out[2 * (int64_t)i + 1] = gb;
+}
+
+int box_qp_batch(const double* in, double* out, int count, cudaStream_t st) {
+  if (count <= 0) return kOk;
+  box_qp_batch_kernel<<<(count + 127) / 128, 128, 0, st>>>(in, out, count);
+  MLR_LAUNCH_CHECK("box_qp_batch_kernel");
+  return kOk;
 }
 
 __global__ void cp_qp_kernel(CpcpDev* st, const double* __restrict__ dots) {

@@ -71,6 +71,7 @@ int cpcp_finalize(CpcpPlan* p, const double* red, cudaStream_t st);
 int cpcp_outputs(CpcpPlan* p, void* L, int64_t ldl, cudaStream_t st);
 int cpcp_rank_shadow(CpcpPlan* p, double* L64, int64_t ld, cudaStream_t st);
 int cpcp_atom_copy(CpcpPlan* p, double* u_out, double* v_out, cudaStream_t st);
+int box_qp_batch(const double* in, double* out, int count, cudaStream_t st);
 int cpcp_atom_dense(CpcpPlan* p, const double* u, const double* v, double* out, int64_t ldo, cudaStream_t st);
 
 }  // namespace mlr

@@ -395,3 +395,25 @@ def test_precision_option_is_explicit():
     assert f32.l.dtype == np.float32 and f32.iter == auto.iter and np.array_equal(f32.l, auto.l)
     with pytest.raises(ValueError, match="precision"):
         pkg.ml_ialm_solve(d32, pkg.PcpOptions(levels=40, precision="fp16"))
+
+
+# ------------------------------------------------------------------ box QP
+def test_box_qp_bitwise():
+    """The device box QP (cp_qp_kernel's solver) equals the reference's
+    _solve_box_qp (cpcp.py:202-231; via the pinned oracle) bit for bit on
+    every branch: interior point, det <= 0, point outside the box, quad <= 0,
+    fallback winning / clipped / absent."""
+    import ctypes
+    import torch
+    from box_qp_cases import cases
+    from paper_2206_13369_b200 import _lib
+    c = cases()
+    inp = torch.from_numpy(c.copy()).cuda()
+    out = torch.zeros((len(c), 2), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.load().mlr_box_qp_batch(ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                            len(c), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    got = out.cpu().numpy()
+    for i, row in enumerate(c):
+        fb = None if np.isnan(row[5]) else float(row[5])
+        want = O.box_qp(*[float(x) for x in row[:5]], fallback=fb)
+        assert (got[i, 0], got[i, 1]) == want, (row, got[i], want)

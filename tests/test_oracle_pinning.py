@@ -235,3 +235,15 @@ def test_oracle_loop_generator_matches_ml_ialm():
     assert [g[1] for g in got] == [h.feasibility_gap for h in ref.history]
     assert [g[2] for g in got] == [h.rank_l for h in ref.history]
     assert abs(O.lanczos_sigma1(d) - np.linalg.norm(d, 2)) <= 1e-12 * np.linalg.norm(d, 2)
+
+
+def test_box_qp_oracle_bitwise_vs_reference(reference):
+    """oracle.box_qp reproduces the reference's _solve_box_qp bit for bit on
+    every branch (the device test compares the GPU against the oracle)."""
+    from box_qp_cases import cases
+    import mlrpca.cpcp as RC
+    for c in cases():
+        fb = None if np.isnan(c[5]) else float(c[5])
+        want = RC._solve_box_qp(*[float(x) for x in c[:5]], fallback_gamma=fb)
+        got = O.box_qp(*[float(x) for x in c[:5]], fallback=fb)
+        assert got == want, (c, got, want)
