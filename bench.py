@@ -210,7 +210,7 @@ def run_reference(args, name, cfg):
     line = {
         "impl": "reference", "metric": metric_for(name, cfg), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded generator with BASELINE {name} shapes/distributions)",
         "config": {"workload": workload_for(name, cfg), "seed": args.seed, "step": "one ML-IALM loop iteration",
                    "last_gap": last[1] if last else None},
