@@ -86,7 +86,7 @@ int mlr_eigh_psd(int np, const double* B, double* V, double* lam, double tol, in
  * red buffer (mlr_pcp_gram / mlr_cpcp_gram layouts), all-gather the CPCP
  * arg-max records and all-reduce the QP dots / Lanczos vectors on the
  * plan's stream.  NCCL is dlopen'd at the first call (mlr_comm_available()
- * reports whether it could be).  dtype: 8 = float64, 5 = int64; op: 0 = sum,
+ * reports whether it could be).  dtype: 8 = float64, 4 = int64; op: 0 = sum,
  * 2 = max (NCCL's enum values). */
 int mlr_comm_available(void);
 int mlr_comm_unique_id(void* out128);

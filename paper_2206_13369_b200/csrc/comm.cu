@@ -27,7 +27,7 @@ typedef struct {
 } ncclUniqueId;
 typedef enum { ncclSuccess = 0 } ncclResult_t;
 typedef enum { ncclSum = 0, ncclProd = 1, ncclMax = 2, ncclMin = 3 } ncclRedOp_t;
-typedef enum { ncclInt64 = 5, ncclFloat64 = 8 } ncclDataType_t;
+typedef enum { ncclInt64 = 4, ncclFloat64 = 8 } ncclDataType_t;
 
 struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*);
@@ -125,7 +125,7 @@ int mlr_comm_destroy(void* comm) {
   return kOk;
 }
 
-/* op: 0 sum, 2 max; dtype: 8 float64, 5 int64 (NCCL's enum values) */
+/* op: 0 sum, 2 max; dtype: 8 float64, 4 int64 (NCCL enum values) */
 int mlr_comm_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream) {
   MlrComm* c = (MlrComm*)comm;
   if (!c || (op != ncclSum && op != ncclMax) || (dtype != ncclFloat64 && dtype != ncclInt64)) {

@@ -21,7 +21,10 @@ def _native_comm(group, world, rank):
     ncclAllGather call on the plan stream (include/mlr_b200.h)."""
     from . import _lib
     dev = torch.cuda.current_device()
-    key = (id(group) if group is not None else None, dev)
+    # keyed by the process group object as well as its shape: a destroyed and
+    # re-created group gets a new communicator
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    key = (id(pg), dev, world, rank)
     if key in _NATIVE:
         return _NATIVE[key]
     lib = _lib.load()
