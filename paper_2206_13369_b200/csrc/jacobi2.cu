@@ -415,7 +415,6 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   __shared__ int qf_all[64];
   __shared__ short cur_pair[J2_DF_MAXB], nxt_pair[J2_DF_MAXB], nxt_partner[J2_DF_MAXB];
   __shared__ int s_ticket;
-  __shared__ int s_cand[J2_DF_MAXB / 2], s_ccnt[2];
   const double tol2 = tol * tol;
 
   for (int e = tid; e < nb * npairs; e += J2_THREADS) {
@@ -470,6 +469,36 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
   const int g_applied = result[6];
   const int g_start = g;
   const double abs_floor = g_start == 0 ? abs_floor_rel * S.red[0] : off_slots[2];
+  // dflow: the critical items of every step (see phase B), once per launch:
+  // thread st builds step st's list in next-step pair order, each item once
+  short* crit_count = reinterpret_cast<short*>(items);
+  short* crit_list = crit_count + ((nb + 7) & ~7);
+  if (dflow) {
+    __syncthreads();  // qslot (which shares this region) is no longer read
+    for (int st = tid; st < nb; st += J2_THREADS) {
+      int cnt = 0;
+      if (st + 1 < nb) {
+        short bp[J2_DF_MAXB];
+        for (int k = 0; k < npairs; ++k) {
+          const int x = sched[st * npairs + k];
+          bp[x & 0xffff] = (short)k;
+          bp[x >> 16] = (short)k;
+        }
+        for (int k2 = 0; k2 < npairs; ++k2) {
+          const int nx = sched[(st + 1) * npairs + k2];
+          const int ka = bp[nx & 0xffff], kb = bp[nx >> 16];
+          if (ka == kb) continue;
+          const int lo = min(ka, kb), hi = max(ka, kb);
+          const int it = lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1);
+          bool dup = false;
+          for (int j = 0; j < cnt; ++j) dup |= crit_list[st * npairs + j] == it;
+          if (!dup) crit_list[st * npairs + cnt++] = (short)it;
+        }
+      }
+      crit_count[st] = (short)cnt;
+    }
+    __syncthreads();
+  }
   bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
     if (vlog && g + nb > g_applied + cap) break;  // rotation log full: pause, V catches up, resume
@@ -989,38 +1018,19 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
         // atomic counter offset by nworkers; each worker ends with exactly
         // one failing grab and the grab completing the count resets it.
         j2_wmark2(0, tw2);
-        unsigned char* dmark = reinterpret_cast<unsigned char*>(items);
-        short* dcrit = reinterpret_cast<short*>(dmark + ((nbitems + 15) & ~15));  // critical items, first in the queue
+        // Critical items (those holding a next-step pair's off-diagonal
+        // block; computed for every step of the schedule at kernel start):
+        // tickets 0 .. ncrit-1, in next-step pair order, each once.  An item
+        // is critical iff a next-step pair joins one of its row blocks with
+        // one of its column blocks (checked on the fly with nxt_partner).
+        const short* dcrit = crit_list + (int64_t)step * npairs;
         int* ctr = tctr + (g & 1);
-        for (int it = tid; it < nbitems; it += J2_THREADS) dmark[it] = 0;
-        __syncthreads();
-        // Critical items (those holding a next-step pair's off-diagonal block),
-        // in next-step pair order, each once: thread k2 < npairs (<= 64) takes
-        // next-step pair k2, drops duplicates of an earlier pair's item, and
-        // two ballots compact the list.  (A serial thread-0 loop with its
-        // dependent shared loads and integer divisions cost ~8k cycles per
-        // step on every worker at C5.)
-        {
-          int itk = -1;
-          if (tid < npairs && !last_step) {
-            const int nx = sched[(step + 1) * npairs + tid];
-            const int ka = cur_pair[nx & 0xffff], kb = cur_pair[nx >> 16];
-            if (ka != kb) {
-              const int lo = min(ka, kb), hi = max(ka, kb);
-              itk = lo * (2 * npairs - lo - 1) / 2 + (hi - lo - 1);
-            }
-          }
-          if (tid < J2_DF_MAXB / 2) s_cand[tid] = itk;
-          __syncthreads();
-          bool keep = itk >= 0;
-          for (int j = 0; keep && j < tid; ++j) keep = s_cand[j] != itk;
-          if (keep) dmark[itk] = 1;
-          const unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if (tid < J2_DF_MAXB / 2 && (tid & 31) == 0) s_ccnt[tid >> 5] = __popc(bal);
-          __syncthreads();
-          if (keep) dcrit[((tid >> 5) ? s_ccnt[0] : 0) + __popc(bal & ((1u << (tid & 31)) - 1u))] = (short)itk;
-          if (tid == 0) s_ticket = s_ccnt[0] + s_ccnt[1];
-        }
+        auto is_crit = [&](int a1, int b1, int a2, int b2) {
+          if (last_step) return false;
+          const int p1 = nxt_partner[a1], p2 = nxt_partner[b1];
+          return p1 == a2 || p1 == b2 || p2 == a2 || p2 == b2;
+        };
+        if (tid == 0) s_ticket = crit_count[step];
         __syncthreads();
         j2_wmark2(1, tw2);
         const int ncrit = s_ticket;
@@ -1050,16 +1060,17 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             break;
           }
           const int it = tk < ncrit ? dcrit[tk] : tk - ncrit;
-          if (tk >= ncrit && dmark[it]) {  // already taken as a critical item
+          int kA = 0, rem = it;
+          while (rem >= npairs - 1 - kA) {
+            rem -= npairs - 1 - kA;
+            ++kA;
+          }
+          const int kB = kA + 1 + rem;
+          const bool crit = is_crit(srow[kA] & 0xffff, srow[kA] >> 16, srow[kB] & 0xffff, srow[kB] >> 16);
+          if (tk >= ncrit && crit) {  // already taken as a critical item
           } else {
-            int kA = 0, rem = it;
-            while (rem >= npairs - 1 - kA) {
-              rem -= npairs - 1 - kA;
-              ++kA;
-            }
-            const int kB = kA + 1 + rem;
             // non-split: a next-step owner computes the whole item itself
-            if ((qf_all[kA] || qf_all[kB]) && !(dmark[it] && !split)) {
+            if ((qf_all[kA] || qf_all[kB]) && !(crit && !split)) {
               const int a1 = srow[kA] & 0xffff, b1 = srow[kA] >> 16;
               const int a2 = srow[kB] & 0xffff, b2 = srow[kB] >> 16;
               // quadrants that are a next-step pair's off-diagonal block are
@@ -1069,7 +1080,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
               const int* w1 = nullptr;
               int* l0 = nullptr;
               int* l1 = nullptr;
-              if (dmark[it]) {
+              if (crit) {
                 const int xs[2] = {a1, b1}, ys[2] = {a2, b2};
                 for (int qx = 0; qx < 2; ++qx)
                   for (int qy = 0; qy < 2; ++qy)
@@ -1092,7 +1103,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
                       w1, g + 1, l0, l1);
               j2_wmark(14, tw);
               if (blockIdx.x == gridDim.x - 1 && tid == 0) atomicAdd(&g_j2prof[15], 1ull);
-            } else if (split && dmark[it] && tid == 0) {
+            } else if (split && crit && tid == 0) {
               // identity critical item: nothing to read, release its owners
               const int xs[2] = {srow[kA] & 0xffff, srow[kA] >> 16};
               for (int qx = 0; qx < 2; ++qx) {
@@ -1263,7 +1274,9 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
   int tickets = 0;  // 1: dynamic phase-B item queue (atomic counter) instead of static round-robin
   if (const char* e = getenv("MLR_J2_TICKETS")) tickets = e[0] == '1';
   const int max_items = dflow ? 0 : (nitems + nctas - 1) / nctas;
-  const size_t item_bytes = dflow ? (size_t)nitems + 2 * (size_t)npairs + 32 : (size_t)max_items * 8;
+  // dflow: per-step critical-item counts and lists (shorts); else the item list
+  const size_t item_bytes =
+      dflow ? 2 * (size_t)((nb + 7) & ~7) + 2 * (size_t)nb * npairs + 64 : (size_t)max_items * 8;
   const size_t sched = (size_t)nb * npairs * sizeof(int) + item_bytes + (size_t)npairs * sizeof(int) + 64;
   const size_t qcache = (size_t)npairs * J2_PW * J2_LD * sizeof(double);
   const int cache_q = (!dflow && sizeof(J2Smem) + qcache + sched <= 200 * 1024) ? 1 : 0;
