@@ -282,6 +282,7 @@ int mlr_box_qp_batch(const double* in6, double* out2, int count, void* stream) {
   return mlr::box_qp_batch(in6, out2, count, (cudaStream_t)stream);
 }
 int mlr_debug_j2prof2(unsigned long long* out8) { return mlr::jacobi2_debug_prof2(out8); }
+int mlr_debug_j2trace(unsigned long long* buf, int g0, int n) { return mlr::jacobi2_debug_trace(buf, g0, n); }
 const char* mlr_last_error(void) { return g_err.c_str(); }
 int mlr_device_count(void) {
   int n = 0;

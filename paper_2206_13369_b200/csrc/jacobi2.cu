@@ -342,6 +342,22 @@ __device__ unsigned long long g_j2prof[16];
 // the same for the last CTA (a phase-B worker in split mode): slot 12 barrier
 // wait, 13 ticket grabs / setup, 14 item compute, 15 items processed
 __device__ unsigned long long g_j2prof2[8];
+// Debug trace (mlr_debug_j2trace, tools/gpu/jacobi_trace.py): for global
+// steps [g0, g0 + n), per CTA, %globaltimer at [0] the step barrier arrival,
+// [1] its release, [3] the step start, [4] an owner's tile / quadrant
+// loaded, [5] its rounds + Q done, [6] its wflag wait done; [2] phase-B
+// items processed.  Off unless a buffer is set.
+__device__ unsigned long long* g_j2trace = nullptr;
+__device__ int g_j2trace_g0 = 0, g_j2trace_n = 0;
+__device__ __forceinline__ unsigned long long j2_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void j2_trace(int g, int me, int nctas, int slot, unsigned long long v) {
+  if (g_j2trace && g >= g_j2trace_g0 && g < g_j2trace_g0 + g_j2trace_n)
+    g_j2trace[(((int64_t)(g - g_j2trace_g0) * nctas) + me) * 8 + slot] = v;
+}
 __device__ __forceinline__ void j2_wmark2(int slot, long long& t0) {
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
     const long long t = clock64();
@@ -508,6 +524,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       int* qflag = qflag_log + slot * npairs;
       long long tw = clock64();
       long long t0 = clock64();
+      if (tid == 0) j2_trace(g, me, nctas, 3, j2_gtime());
       if (blockIdx.x == 0 && tid == 0) atomicAdd(&g_j2prof[5], 1ull);
       const int* srow = sched + step * npairs;
       // ------------------------------------------------ phase A: pair owners
@@ -633,6 +650,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
           if ((tid & 31) == 0 && mx > tol) S.active = 1;
         }
         __syncthreads();
+        if (tid == 0) j2_trace(g, me, nctas, 4, j2_gtime());
         j2_mark(0, t0);
         const int rounds = !S.active ? 0 : (step == 0 ? J2_PW - 1 : J2_BW);
         // pair k of inner round rnd: circle method on 32 players for step 0,
@@ -862,12 +880,14 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
             for (int e = sub; e < J2_PW; e += 8) qo[r * J2_PW + e] = S.Q[r][e];
           }
         }
+        if (tid == 0) j2_trace(g, me, nctas, 5, j2_gtime());
         j2_mark(1, t0);
         // split mode: the worker taking my critical item must have read its X
         // (which contains my off-diagonal block) before I overwrite that block
         if (rot && crit_quad) {
           if (tid == 0)
             while (ld_acquire(wflag + k) < g) __nanosleep(20);
+          if (tid == 0) j2_trace(g, me, nctas, 6, j2_gtime());
           __syncthreads();
         }
         // the rotated diagonal block goes straight back into B
@@ -881,7 +901,9 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       if (!CLUSTER) __threadfence();  // barrier.cluster.arrive/wait are release/acquire
       j2_mark(6, t0);
       if (blockIdx.x == gridDim.x - 1 && tid == 0) tw = clock64();
+      if (tid == 0) j2_trace(g, me, nctas, 0, j2_gtime());
       j2_sync<CLUSTER>();
+      if (tid == 0) j2_trace(g, me, nctas, 1, j2_gtime());
       j2_mark(2, t0);
       j2_wmark(12, tw);
       // ------------------------------------------------ phase B: apply
@@ -1103,6 +1125,8 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
                       w1, g + 1, l0, l1);
               j2_wmark(14, tw);
               if (blockIdx.x == gridDim.x - 1 && tid == 0) atomicAdd(&g_j2prof[15], 1ull);
+              if (tid == 0 && g_j2trace && g >= g_j2trace_g0 && g < g_j2trace_g0 + g_j2trace_n)
+                g_j2trace[(((int64_t)(g - g_j2trace_g0) * nctas) + me) * 8 + 2] += 1;
             } else if (split && crit && tid == 0) {
               // identity critical item: nothing to read, release its owners
               const int xs[2] = {srow[kA] & 0xffff, srow[kA] >> 16};
@@ -1349,6 +1373,13 @@ static int launch_j2(double* B, double* V, int np, int nrows_v, double tol, doub
       MLR_LAUNCH_CHECK("j2_vapply_kernel");
     }
   }
+  return kOk;
+}
+
+int jacobi2_debug_trace(unsigned long long* buf, int g0, int n) {
+  MLR_CUDA(cudaMemcpyToSymbol(g_j2trace, &buf, sizeof(buf)));
+  MLR_CUDA(cudaMemcpyToSymbol(g_j2trace_g0, &g0, sizeof(int)));
+  MLR_CUDA(cudaMemcpyToSymbol(g_j2trace_n, &n, sizeof(int)));
   return kOk;
 }
 

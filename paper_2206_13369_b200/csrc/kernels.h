@@ -80,6 +80,7 @@ int64_t jacobi2_qbuf_elems(int np);   // rotation log (doubles)
 int64_t jacobi2_qflag_elems(int np);  // rotation-log flags (ints)
 int jacobi2_debug_prof(unsigned long long* out8);
 int jacobi2_debug_prof2(unsigned long long* out8);
+int jacobi2_debug_trace(unsigned long long* buf, int g0, int n);
 int jacobi2_eig(bool f32, void* B, void* V, int np, int nrows_v, double tol, double abs_floor_rel, int max_sweeps,
                 void* Qbuf, int* qflag, double* off_slots, int* result, const int* skip, cudaStream_t st);
 
