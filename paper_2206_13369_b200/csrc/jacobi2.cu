@@ -358,6 +358,14 @@ __device__ __forceinline__ void j2_trace(int g, int me, int nctas, int slot, uns
   if (g_j2trace && g >= g_j2trace_g0 && g < g_j2trace_g0 + g_j2trace_n)
     g_j2trace[(((int64_t)(g - g_j2trace_g0) * nctas) + me) * 8 + slot] = v;
 }
+// slot 7: the SM the CTA runs on (placement of owners vs workers)
+__device__ __forceinline__ void j2_trace_sm(int g, int me, int nctas) {
+  if (g_j2trace && g >= g_j2trace_g0 && g < g_j2trace_g0 + g_j2trace_n) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_j2trace[(((int64_t)(g - g_j2trace_g0) * nctas) + me) * 8 + 7] = smid;
+  }
+}
 __device__ __forceinline__ void j2_wmark2(int slot, long long& t0) {
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
     const long long t = clock64();
@@ -525,6 +533,7 @@ jacobi2_kernel(double* __restrict__ B, double* __restrict__ V, int np, int nrows
       long long tw = clock64();
       long long t0 = clock64();
       if (tid == 0) j2_trace(g, me, nctas, 3, j2_gtime());
+      if (tid == 0) j2_trace_sm(g, me, nctas);
       if (blockIdx.x == 0 && tid == 0) atomicAdd(&g_j2prof[5], 1ull);
       const int* srow = sched + step * npairs;
       // ------------------------------------------------ phase A: pair owners

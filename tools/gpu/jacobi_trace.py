@@ -68,3 +68,26 @@ for s_ in range(1, n):
     seg["wflag wait"].append(np.median(o[w, 6] - o[w, 5]) if w.any() else 0.0)
     seg["publish->arrive"].append(np.median(o[:, 0] - np.where(w, o[:, 6], o[:, 5])))
 print("owner segments (us):", {k: round(np.mean(v) / 1e3, 2) for k, v in seg.items() if v})
+
+sm = t[1, :, 7].astype(int)
+owner_sms = sm[owners]
+others = sm[~owners]
+shared = sum(1 for x in owner_sms if x in set(others))
+print(f"SM placement: {len(set(sm))} distinct SMs for {nctas} CTAs; owners on SMs shared with a worker: {shared} of {owners.sum()}")
+if os.environ.get("SMDUMP"):
+    for c in range(nctas):
+        mates = [int(x) for x in np.nonzero(sm == sm[c])[0] if x != c]
+        print(f"cta {c} sm {sm[c]} mates {mates}")
+
+# per-owner rounds+Q time, split by what shares the owner's SM
+rq = []
+for s_ in range(1, n):
+    if t[s_ - 1, :, 1].min() == 0:
+        continue
+    o = t[s_, obase:obase + 40]
+    rq.append(o[:, 5] - o[:, 4])
+rq = np.mean(rq, axis=0) / 1e3
+own_idx = np.arange(obase, obase + 40)
+dbl = np.array([any(owners[x] for x in np.nonzero(sm == sm[c])[0] if x != c) for c in own_idx])
+print(f"rounds+Q per owner: owner-mate {rq[dbl].mean() if dbl.any() else float('nan'):.2f} us ({dbl.sum()}), "
+      f"worker-mate {rq[~dbl].mean() if (~dbl).any() else float('nan'):.2f} us ({(~dbl).sum()}); max {rq.max():.2f}")
