@@ -130,6 +130,7 @@ static void carve_pcp(PcpPlan& p, Carver& c) {
                          std::max(std::max(std::max(p.lz_splits, p.lz_fused_ctas), p.lz_run_ctas), p.lz_long_clusters));
   p.lzRed = c.take<double>(8 * (size_t)std::max(p.lz_run_ctas, 1) * (2 * ((size_t)p.lz_kmax + 1) + 4));
   p.lzWork = c.take<double>(8 * (size_t)n);
+  if (p.trd_on) trd_carve(&p.trd, c.take<char>(trd_bytes(p.ch.nh)), p.ch.nh);
 }
 
 // K slices of the blocked 128x128 Gram (one CTA per SM).  Small Grams (few
@@ -208,6 +209,17 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   }
   p.jac_tol_host = 1e-14;
   p.jac_max_sweeps = 60;
+  {
+    // coarse eigensolver: "trd" (tridiagonal, trd.cu), "jacobi" (warm-started
+    // block Jacobi), default by size: measured on B200, the cluster Jacobi
+    // matches the tridiagonal solver for 192 < n_H <= 512 (C2: 29 vs 31 ms
+    // per solve), the tridiagonal solver wins below (C1: 20.5 vs 24.9 ms) and
+    // above (C5: 172 vs 257 ms)
+    const char* e = getenv("MLR_EIG");
+    const std::string ev = e ? e : "";
+    const bool want = ev == "trd" || (ev != "jacobi" && (ch.nh <= 192 || ch.nh > 512));
+    p.trd_on = want && trd_supported(ch.nh);
+  }
 }
 
 static void carve_cpcp(CpcpPlan& p, Carver& c) {

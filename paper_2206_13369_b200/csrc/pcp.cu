@@ -1071,9 +1071,9 @@ __global__ void pcp_finalize_kernel(PcpDev* st, const double* __restrict__ red, 
   }
 }
 
-__global__ void pcp_after_jacobi(PcpDev* st, const int* __restrict__ jac_result) {
+__global__ void pcp_after_jacobi(PcpDev* st, const int* __restrict__ jac_result, int trd) {
   if (st->done) return;
-  if (st->jac_skip) {  // rank 0 certified: no eigensolve this iteration
+  if (st->jac_skip || (trd && st->trd_ok)) {  // rank 0 certified, or the tridiagonal solver succeeded
     st->jac_sweeps = 0;
     return;
   }
@@ -1835,20 +1835,32 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
     if (rc || ksplit <= 1) return rc;
     return sum_slices(p->gram_part, (int64_t)np * np, (int64_t)np * np, ksplit, C, st, skip);
   };
-  if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;   // U = G^-1 V
-  if ((rc = mm(red, false, p->T1, false, p->Xm, nullptr))) return rc;        // T = K U
-  if ((rc = mm(p->T1, true, p->Xm, false, p->Bm, nullptr))) return rc;       // B~ = U^T T
+  // tridiagonal eigensolver (trd.cu): no warm start, B = G^-1 K G^-1 directly
+  const bool use_trd = p->trd_on && p->trunc_sv0 == 0;
+  if (use_trd) {
+    if ((rc = mm(red, false, p->ch.gi, false, p->Xm, nullptr))) return rc;    // X = K G^-1
+    if ((rc = mm(p->ch.gi, false, p->Xm, false, p->Bm, nullptr))) return rc;  // B = G^-1 X
+  } else {
+    if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;   // U = G^-1 V
+    if ((rc = mm(red, false, p->T1, false, p->Xm, nullptr))) return rc;        // T = K U
+    if ((rc = mm(p->T1, true, p->Xm, false, p->Bm, nullptr))) return rc;       // B~ = U^T T
+  }
   p->timer.end(kPhPre, st);
   p->timer.begin(st);
   if ((rc = pcp_rank0(p, st))) return rc;
+  if (use_trd &&
+      (rc = trd_eig(p->dev, &p->trd, p->Bm, p->Vm, p->ch.nh, np, &p->dev->tau, &p->dev->jac_skip, st)))
+    return rc;
+  // the Jacobi: the eigensolver (warm started), or on the trd path the
+  // fallback for a failed tridiagonal solve (V = I then), skipped otherwise
   if ((rc = jacobi2_eig(false, p->Bm, p->Vm, np, np, p->jac_tol_host, p->jac_floor_rel, p->jac_max_sweeps, p->qbuf,
-                        p->qflag, p->jac_off, p->jac_result, &p->dev->jac_skip, st)))
+                        p->qflag, p->jac_off, p->jac_result, use_trd ? &p->dev->eig_skip : &p->dev->jac_skip, st)))
     return rc;
   p->timer.end(kPhJacobi, st);
   p->timer.begin(st);
-  pcp_after_jacobi<<<1, 1, 0, st>>>(p->dev, p->jac_result);
+  pcp_after_jacobi<<<1, 1, 0, st>>>(p->dev, p->jac_result, use_trd ? 1 : 0);
   MLR_LAUNCH_CHECK("pcp_after_jacobi");
-  if (p->eig_sort) {
+  if (p->eig_sort && !use_trd) {
     // sort the eigenpairs (warm start of the next iteration); fw is free until svt_weights
     int* perm = reinterpret_cast<int*>(p->fw);
     const int nh = p->ch.nh;

@@ -29,6 +29,8 @@ struct PcpDev {
   int jac_sweeps;
   int trunc, sv, sv_cap;  // ialm_solve: keep only the top-sv triplets, adapt sv (pcp.py:157-165)
   int jac_skip;     // Jacobi not needed this iteration: done, or rank 0 certified (pcp_rank0_test)
+  int eig_skip;     // trd path: the Jacobi fallback is not needed (trd solved it, or jac_skip)
+  int trd_ok;       // trd path: this iteration's eigenpairs came from the tridiagonal solver
 };
 
 struct LanczosDev {
@@ -36,6 +38,16 @@ struct LanczosDev {
   double theta, theta_prev, sigma1;
   double alpha[512];
   double beta[512];
+};
+
+// Scratch of the tridiagonal coarse eigensolver (trd.cu)
+struct TrdBuf {
+  double* hv;     // n x ldh (ldh = n rounded up to even): row j = Householder vector v_j (entries j+1..n-1)
+  double* z;      // n x n: eigenvectors of T, vector c at z[c * n + i]
+  double *beta, *dd, *ee, *lam;  // n each: reflector scalars, diag / off-diag of T, eigenvalues (descending)
+  uint4 *pll, *rowll, *sll;      // flag-carrying publication buffers (2 x n, 2 x n, 2 x 256 records)
+  double* scale;                 // power-of-two scale of T used by the bisection / vectors
+  int* info;                     // [0] = k (eigenvalues above tau^2), [1] = failure
 };
 
 struct PcpPlan {
@@ -50,6 +62,8 @@ struct PcpPlan {
   int coarse_ksplit;  // split-K of the n_p^3 coarse products (<= gram_splits)
   int lz_run_ctas;    // > 0: the whole Lanczos run in one cooperative kernel (one rank, n <= 4096)
   int eig_sort;       // sort the eigenpairs after each Jacobi (warm start of the next)
+  int trd_on;         // coarse eigensolver: tridiagonal (trd.cu) with the Jacobi as fallback
+  TrdBuf trd;
   double* lzRed;      // lz_run_ctas x (2 (kmax + 1) + 4) dot partials
   double jac_tol_host;
   double jac_floor_rel;
@@ -74,6 +88,13 @@ struct PcpPlan {
   int* jac_result;     // 4
   double *lzQ, *lzT, *lzW, *lzWork;
 };
+
+int trd_max_n();
+bool trd_supported(int n);
+size_t trd_bytes(int n);
+void trd_carve(TrdBuf* b, char* base, int n);
+int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const double* tau, const int* skip,
+            cudaStream_t s);
 
 int pcp_input_stats(PcpPlan* p, const void* D, int64_t ldd, double* out2, cudaStream_t st);
 int matrix_stats(int64_t m, int n, bool f32, const void* D, int64_t ldd, double* part, int blocks, double* out3,

@@ -1,0 +1,791 @@
+// Coarse symmetric eigensolver by Householder tridiagonalisation (sm_100a).
+//
+// Replaces the two-sided Jacobi for the ML-PCP coarse SVT (reference
+// pcp.py:257-258, svd_full = LAPACK gesdd, linalg.py:86-99): only the
+// eigenpairs of B = M_H^T M_H above tau^2 enter the SVT, and the Jacobi had
+// to diagonalise the whole noise bulk below tau^2 as well (6-12 sweeps per
+// warm-started iteration at C5).  Here:
+//
+//   1. trd_reduce_kernel   B = Q T Q^T (T tridiagonal), one cooperative grid.
+//      Row i of B lives in the shared memory of CTA i mod G (C5: 16 rows of
+//      1250 doubles in each of 79 CTAs), so the n - 2 reflector steps never
+//      touch HBM.  Every CTA keeps a replica of the next row, so it builds
+//      the reflector v_j itself; per step it computes p_i = beta A_i v for its
+//      rows (one warp per row) and publishes them with its partial p^T v,
+//      then (after the one grid-wide exchange of the step) applies
+//      A -= v w^T + w v^T, w = p - (beta/2)(p^T v) v, to its rows and to the
+//      replica; the owner of row j + 2 publishes it for the next-but-one
+//      step.  Publication is fence-free: every double travels in a 16-byte
+//      record {lo, tag, hi, tag} written and polled with single 16-byte
+//      volatile accesses (the NCCL LL protocol), the tag being the step.
+//      Fixed-order sums: bitwise reproducible, so replicated ranks agree.
+//   2. trd_bisect_kernel   eigenvalues of T above tau^2: Sturm counts give
+//      k = #{lambda > tau^2} exactly; one warp per eigenvalue refines it by
+//      32-point multisection to full FP64 accuracy (division-free Sturm
+//      sequences: one FMA on the dependency chain per step).
+//   3. trd_vectors_kernel  eigenvector of T per eigenvalue from the twisted
+//      factorisation T - lambda I = N_r D_r N_r^T (one warp per vector, the
+//      pivots from the forward / backward Sturm sequences so the divisions
+//      stay off the dependency chain, twist index r at the smallest
+//      |gamma_r|, then two products; scratch in shared memory).
+//   4. trd_back_kernel     V = Q Z: the reflectors applied in reverse order to
+//      the k vectors (one warp per vector, the vector in registers, the
+//      reflector rows staged in shared memory by TMA bulk copies).
+//   5. trd_commit_kernel   eigenvalues to diag(B~) (what svt_weights reads),
+//      zero V outside the k columns; on any non-finite result V = I and the
+//      Jacobi (launched after, skipped on success) solves the iteration.
+//
+// Accuracy: the reduction is backward stable (T = Q^T (B + E) Q with
+// |E| ~ eps |B|) and the twisted vectors have residual ~ eps |T|, like
+// LAPACK dsytrd + dstebz + dstein; a numpy restatement of exactly these steps
+// reproduces the reference's C1 / C2 solves (same iterations and rank
+// column, relF(L) 1e-12 / 3e-13).
+
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "pcp.h"
+
+namespace mlr {
+
+namespace {
+
+constexpr int TRD_T = 512;
+constexpr int TRD_W = TRD_T / 32;  // one local row per warp
+constexpr int TRD_MAXG = 256;
+constexpr int TRD_LL = 4;  // publication records per thread and step: n <= 4 x 512
+
+// flag-carrying 16-byte records (NCCL LL): {lo32, tag, hi32, tag}
+__device__ __forceinline__ void ll_store(uint4* p, double v, uint32_t tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.relaxed.gpu.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((uint32_t)u), "r"(tag),
+               "r"((uint32_t)(u >> 32)), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ll_ld(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ double ll_val(uint4 v) {
+  return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
+}
+__device__ __forceinline__ double ll_load(const uint4* p, uint32_t tag) {
+  uint32_t a, f1, c, f2;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(f1), "=r"(c), "=r"(f2)
+                 : "l"(p)
+                 : "memory");
+  } while (f1 != tag || f2 != tag);
+  return __longlong_as_double((long long)(((unsigned long long)c << 32) | a));
+}
+
+// a / b to ~1 ulp: approximate reciprocal and two Newton steps (normal
+// inputs of moderate exponent: T is pre-scaled to |T| ~ 1)
+__device__ __forceinline__ double trd_div(double a, double bb) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(bb));
+  double e = fma(-bb, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-bb, r, 1.0);
+  r = fma(r, e, r);
+  return a * r;
+}
+
+// The reflector that zeroes row[j+2..n) of the (replicated) row j + 1
+// (Householder, LAPACK dlarfg convention): beta, the new off-diagonal e and
+// the scale of v = row / (alpha - e).  s = sum of row[k]^2, k >= j + 2.
+// Computed redundantly by every thread: identical inputs, identical ops.
+__device__ __forceinline__ void trd_reflector(double alpha, double s, double& bet, double& ej, double& scale) {
+  bet = 0.0;
+  ej = alpha;
+  scale = 0.0;
+  if (s != 0.0) {
+    const double nx = sqrt(fma(alpha, alpha, s));
+    ej = alpha >= 0.0 ? -nx : nx;
+    bet = trd_div(ej - alpha, ej);
+    scale = trd_div(1.0, alpha - ej);
+  }
+}
+
+// Step j uses v_j (vsb[j & 1], built at the end of step j - 1 from the
+// replica of row j) and keeps the rank-2 update of step j - 1 pending on the
+// local rows: the matvec corrects for it with two scalars,
+//   (A - v' w'^T - w' v'^T)_i . v = A_i . v - v'_i (w' . v) - w'_i (v' . v),
+// and the update itself is applied after p is published, while the
+// exchange is in flight.  The exchange carries p only: every CTA has v and
+// all of p, so K = beta/2 p . v needs no separate partial sums.
+__global__ void __launch_bounds__(TRD_T, 1)
+trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const int* __restrict__ skip, int trace, int slp) {
+  if (skip && *skip) return;
+  long long tr[8];
+  const bool tron = trace && threadIdx.x == 0;
+  extern __shared__ double trd_sm[];
+  const int G = gridDim.x, g = blockIdx.x;
+  const int R = (n + G - 1) / G;  // <= TRD_W (host checks)
+  const int ldh = (n + 1) & ~1;
+  double* rows = trd_sm;          // R x n: rows g, g + G, g + 2G, ...
+  double* vsb = rows + (size_t)R * n;  // 2 x n: v_j by step parity
+  double* wpv = vsb + 2 * (size_t)n;   // w of the pending update
+  double* ps = wpv + n;
+  double* cur = ps + n;                // the replica of row j + 1
+  __shared__ double kpart[TRD_W], sqpart[TRD_W], s1part[TRD_W], s2part[TRD_W], s_bs[2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int r = 0; r < R; ++r) {
+    const int i = g + r * G;
+    if (i < n)
+      for (int k = tid; k < n; k += TRD_T) rows[(size_t)r * n + k] = B[(int64_t)i * ldb + k];
+  }
+  {
+    double q = 0.0;
+    for (int k = tid; k < n; k += TRD_T) {
+      const double x = B[k];
+      cur[k] = x;
+      if (k >= 2) q = fma(x, x, q);
+    }
+    q = warp_sum(q);
+    if (lane == 0) sqpart[wid] = q;
+  }
+  __syncthreads();
+  double bet;
+  {
+    double s = 0.0;
+    for (int w = 0; w < TRD_W; ++w) s += sqpart[w];
+    double ej, scale;
+    trd_reflector(cur[1], s, bet, ej, scale);
+    if (g == 0 && tid == 0) {
+      b.beta[0] = bet;
+      b.dd[0] = cur[0];
+      b.ee[0] = ej;
+    }
+    for (int k = 1 + tid; k < n; k += TRD_T) {
+      const double v = k == 1 ? 1.0 : cur[k] * scale;
+      vsb[k] = v;
+      if (g == 0) b.hv[k] = v;
+    }
+  }
+  __syncthreads();
+  const int my_i = g + wid * G;  // the row this warp owns (if < n and wid < R)
+  const bool has_row = wid < R && my_i < n;
+  double* my_row = rows + (size_t)wid * n;
+  for (int j = 0; j < n - 2; ++j) {
+    const int m1 = j + 1;
+    const uint32_t tag = (uint32_t)j + 1u;
+    const double* vc = vsb + (size_t)(j & 1) * n;         // v_j
+    const double* vp = vsb + (size_t)((j + 1) & 1) * n;   // v_{j-1} (pending)
+    const bool trs = tron && j == n / 2;
+    if (trs) {
+      tr[0] = clock64();
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[7]));
+    }
+    // (1) p_i = beta (A_i . v - v'_i s1 - w'_i s2) for the local rows i >= j + 1
+    if (has_row && my_i >= m1) {
+      double s1 = 0.0, s2 = 0.0;
+      if (j > 0) {
+        s1 = warp_sum(lane < TRD_W ? s1part[lane] : 0.0);
+        s2 = warp_sum(lane < TRD_W ? s2part[lane] : 0.0);
+      }
+      double a0 = 0.0, a1 = 0.0;
+      int k = m1 + lane;
+      for (; k + 32 < n; k += 64) {
+        a0 = fma(my_row[k], vc[k], a0);
+        a1 = fma(my_row[k + 32], vc[k + 32], a1);
+      }
+      if (k < n) a0 = fma(my_row[k], vc[k], a0);
+      double raw = warp_sum(a0 + a1);
+      if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
+      if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
+    }
+    if (trace) __syncthreads();
+    if (trs) tr[1] = clock64();
+    // (2) the pending update of step j - 1 on the local rows (k >= j + 1);
+    //     the owner of row j + 1 publishes it (through step j - 1)
+    if (j > 0 && has_row && my_i >= m1) {
+      const double vi = vp[my_i], wi = wpv[my_i];
+      uint4* pub = my_i == m1 ? b.rowll + (size_t)(m1 & 1) * n : nullptr;
+      int k = m1 + lane;
+      for (; k + 32 < n; k += 64) {
+        const double x0 = fma(-vi, wpv[k], fma(-wi, vp[k], my_row[k]));
+        const double x1 = fma(-vi, wpv[k + 32], fma(-wi, vp[k + 32], my_row[k + 32]));
+        my_row[k] = x0;
+        my_row[k + 32] = x1;
+        if (pub) {
+          ll_store(pub + k, x0, tag);
+          ll_store(pub + k + 32, x1, tag);
+        }
+      }
+      if (k < n) {
+        const double x0 = fma(-vi, wpv[k], fma(-wi, vp[k], my_row[k]));
+        my_row[k] = x0;
+        if (pub) ll_store(pub + k, x0, tag);
+      }
+    }
+    if (trace) __syncthreads();
+    if (trs) tr[2] = clock64();
+    // (3) the exchange: all of p and the replica of row j + 1; K partials
+    {
+      const uint4* pl = b.pll + (size_t)(j & 1) * n;
+      const uint4* rl = b.rowll + (size_t)(m1 & 1) * n;
+      uint4 pr[TRD_LL], cr[TRD_LL];
+#pragma unroll
+      for (int u = 0; u < TRD_LL; ++u) {
+        const int k = m1 + tid + u * TRD_T;
+        if (k < n) {
+          pr[u] = ll_ld(pl + k);
+          if (j > 0) cr[u] = ll_ld(rl + k);
+        }
+      }
+      double q = 0.0;
+#pragma unroll
+      for (int u = 0; u < TRD_LL; ++u) {
+        const int k = m1 + tid + u * TRD_T;
+        if (k < n) {
+          while (pr[u].y != tag || pr[u].w != tag) {
+            if (slp) __nanosleep(slp);
+            pr[u] = ll_ld(pl + k);
+          }
+          const double p = ll_val(pr[u]);
+          ps[k] = p;
+          q = fma(p, vc[k], q);
+          if (j > 0) {
+            while (cr[u].y != tag || cr[u].w != tag) {
+              if (slp) __nanosleep(slp);
+              cr[u] = ll_ld(rl + k);
+            }
+            cur[k] = ll_val(cr[u]);
+          } else {
+            cur[k] = B[ldb + k];
+          }
+        }
+      }
+      q = warp_sum(q);
+      if (lane == 0) kpart[wid] = q;
+    }
+    if (trs) {
+      tr[3] = clock64();
+      long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      tr[7] = gt - tr[7];
+    }
+    __syncthreads();
+    if (trs) tr[4] = clock64();
+    // (4) w_j = p - K v_j (the new pending update); the replica row j + 1
+    //     through step j and its sum of squares beyond j + 2
+    {
+      const double K = 0.5 * bet * warp_sum(lane < TRD_W ? kpart[lane] : 0.0);
+      const double vi = vc[m1];
+      const double wi = fma(-K, vi, ps[m1]);
+      double q = 0.0;
+      for (int k = m1 + tid; k < n; k += TRD_T) {
+        const double wk = fma(-K, vc[k], ps[k]);
+        wpv[k] = wk;
+        const double c2 = fma(-vi, wk, fma(-wi, vc[k], cur[k]));
+        cur[k] = c2;
+        if (k >= j + 3) q = fma(c2, c2, q);
+      }
+      q = warp_sum(q);
+      if (lane == 0) sqpart[wid] = q;
+    }
+    __syncthreads();
+    // (5) the reflector of step j + 1 from the replica (warp 0), v_{j+1} and
+    //     the two correction dots of the next matvec
+    if (j + 1 < n - 2) {
+      if (wid == 0) {
+        const double s = warp_sum(lane < TRD_W ? sqpart[lane] : 0.0);
+        if (lane == 0) {
+          double bt, ej, sc;
+          trd_reflector(cur[j + 2], s, bt, ej, sc);
+          s_bs[0] = bt;
+          s_bs[1] = sc;
+          if (g == 0) {
+            b.beta[j + 1] = bt;
+            b.dd[j + 1] = cur[j + 1];
+            b.ee[j + 1] = ej;
+          }
+        }
+      }
+      __syncthreads();
+      const double scale = s_bs[1];
+      double* vn = vsb + (size_t)((j + 1) & 1) * n;  // overwrites v_{j-1}: no longer needed
+      double* hrow = b.hv + (int64_t)(j + 1) * ldh;
+      double q1 = 0.0, q2 = 0.0;
+      for (int k = j + 2 + tid; k < n; k += TRD_T) {
+        const double v = k == j + 2 ? 1.0 : cur[k] * scale;
+        vn[k] = v;
+        if (g == 0) hrow[k] = v;
+        q1 = fma(wpv[k], v, q1);
+        q2 = fma(vc[k], v, q2);
+      }
+      q1 = warp_sum(q1);
+      q2 = warp_sum(q2);
+      if (lane == 0) {
+        s1part[wid] = q1;
+        s2part[wid] = q2;
+      }
+    }
+    if (trs) tr[5] = clock64();
+    __syncthreads();
+    bet = s_bs[0];
+    if (trs) {
+      tr[6] = clock64();
+      printf("trd g=%d j=%d: matvec %lld upd %lld xchg %lld bar %lld w %lld refl %lld total %lld startns %lld\n", g, j,
+             tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4], tr[6] - tr[5],
+             tr[6] - tr[0], tr[7]);
+    }
+  }
+  // the trailing 2 x 2 block: the replica is row n - 2 through step n - 3;
+  // row n - 1 still has the update of step n - 3 pending
+  if (g == 0 && tid == 0) {
+    b.dd[n - 2] = cur[n - 2];
+    b.ee[n - 2] = cur[n - 1];
+    b.beta[n - 2] = 0.0;
+    b.beta[n - 1] = 0.0;
+    b.ee[n - 1] = 0.0;
+  }
+  if (has_row && lane == 0 && my_i == n - 1) {
+    const double* vl = vsb + (size_t)((n - 3) & 1) * n;
+    const double vi = vl[n - 1], wi = wpv[n - 1];
+    b.dd[n - 1] = fma(-vi, wi, fma(-wi, vi, my_row[n - 1]));
+  }
+}
+
+// Number of eigenvalues of T greater than x: sign changes of the Sturm
+// sequence p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, p_{-1} = 1 (the
+// negative pivots q_i = p_i / p_{i-1} of T - x I).  One FMA on the
+// dependency chain per step; every 8 steps the pair is rescaled by an exact
+// power of two (T is pre-scaled so |d - x|, e^2 <= 4: 8 steps grow it by
+// at most 8^8).  A zero p_i counts as non-negative: the number of sign
+// changes over (p_{i-1}, 0, p_{i+1} = -e^2 p_{i-1}) is the same either way.
+__device__ __forceinline__ int trd_count_gt(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                            double x) {
+  double pm = 1.0, pc = d[0] - x;
+  int neg = pc < 0.0;
+  int i = 1;
+  for (; i + 8 <= n; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double pn = fma(d[i + u] - x, pc, -e2[i + u - 1] * pm);
+      neg += (pn < 0.0) != (pc < 0.0);
+      pm = pc;
+      pc = pn;
+    }
+    const int hc = __double2hiint(pc) & 0x7fffffff, hm = __double2hiint(pm) & 0x7fffffff;
+    const int ex = (max(hc, hm) >> 20) - 1023;
+    const double f = __hiloint2double((1023 - ex) << 20, 0);
+    pc *= f;
+    pm *= f;
+  }
+  for (; i < n; ++i) {
+    const double pn = fma(d[i] - x, pc, -e2[i - 1] * pm);
+    neg += (pn < 0.0) != (pc < 0.0);
+    pm = pc;
+    pc = pn;
+  }
+  return n - neg;
+}
+
+// T scaled by the power of two that brings its Gershgorin bound into [1, 2)
+__device__ __forceinline__ double trd_scale_of(double hi) { return hi > 0.0 ? scalbn(1.0, -ilogb(hi)) : 1.0; }
+
+// One warp per eigenvalue index c (c-th largest, 0-based) among those above
+// t = tau^2; all warps first agree on k = count(> t).  lam holds the
+// unscaled eigenvalues, scale the factor for the vector kernel.
+__global__ void __launch_bounds__(256) trd_bisect_kernel(TrdBuf b, int n, const double* __restrict__ tau_p,
+                                                         const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double bs_sm[];
+  double* d = bs_sm;
+  double* e2 = d + n;
+  __shared__ double s_lo, s_hi, s_sc;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (wid == 0) {
+    double hi = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double el = i > 0 ? fabs(b.ee[i - 1]) : 0.0, er = i < n - 1 ? fabs(b.ee[i]) : 0.0;
+      hi = fmax(hi, fabs(b.dd[i]) + el + er);
+    }
+    hi = warp_max(hi);
+    if (lane == 0) {
+      const double sc = trd_scale_of(hi);
+      s_sc = sc;
+      s_hi = hi * sc * (1.0 + 4.0 * DBL_EPSILON);
+      const double tau = *tau_p;
+      s_lo = tau * tau * sc;
+      if (blockIdx.x == 0) b.scale[0] = sc;
+    }
+  }
+  __syncthreads();
+  const double sc = s_sc;
+  for (int i = tid; i < n; i += blockDim.x) {
+    d[i] = b.dd[i] * sc;
+    const double e = i < n - 1 ? b.ee[i] * sc : 0.0;
+    e2[i] = fmax(e * e, 0x1p-900);  // an exact zero coupling would stall the sequence
+  }
+  __syncthreads();
+  const double t = s_lo;
+  const int c = blockIdx.x * (blockDim.x >> 5) + wid;
+  int k = 0;
+  if (lane == 0) k = trd_count_gt(d, e2, n, t);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  if (blockIdx.x == 0 && tid == 0) b.info[0] = k;
+  if (c >= k) return;
+  // lambda_c in (lo, hi]: count(lo) >= c + 1 > count(hi)
+  double lo = t, hi = s_hi;
+  for (int round = 0; round < 40; ++round) {
+    const double w = hi - lo;
+    if (w <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 0x1p-1000) break;
+    const double x = lo + w * (double)(lane + 1) / 33.0;
+    const int cnt = trd_count_gt(d, e2, n, x);
+    const unsigned above = __ballot_sync(0xffffffffu, cnt >= c + 1);  // a prefix of lanes
+    const int na = __popc(above);
+    const double nlo = na > 0 ? __shfl_sync(0xffffffffu, x, na - 1) : lo;
+    const double nhi = na < 32 ? __shfl_sync(0xffffffffu, x, na & 31) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) b.lam[c] = 0.5 * (lo + hi) / sc;
+}
+
+__device__ __forceinline__ double trd_rescale_pair(double& pc, double& pm) {
+  const int hc = __double2hiint(pc) & 0x7fffffff, hm = __double2hiint(pm) & 0x7fffffff;
+  const int ex = (max(hc, hm) >> 20) - 1023;
+  const double f = __hiloint2double((1023 - ex) << 20, 0);
+  pc *= f;
+  pm *= f;
+  return f;
+}
+
+// Twisted factorisation eigenvector of T for lambda_c, one warp per c, on T
+// scaled by the bisection's power of two.  Lane 0 runs the recurrences:
+//   forward Sturm sequence p -> pivots D+_i = p_i / p_{i-1} (T - lam I =
+//   L+ D+ L+^T), backward sequence r -> R-_i = r_i / r_{i+1} (= U- R- U-^T),
+//   gamma_i = D+_i + R-_i - (d_i - lam), twist r = argmin |gamma_i|,
+//   z_r = 1, z_i = -(e_i / D+_i) z_{i+1} above, z_{i+1} = -(e_i / R-_{i+1}) z_i
+//   below.  The chains are one FMA (sequences) or one multiply (z) per step;
+// the divisions are off the chain.  Output z[c * n + i], unit 2-norm.
+constexpr int TRD_VW = 6;
+
+__global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int n, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ double vsm[];  // TRD_VW x 3 n
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int k = b.info[0];
+  const int c = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (c >= k) return;
+  double* __restrict__ dps = vsm + (size_t)wid * 3 * n;  // D+_i
+  double* __restrict__ rms = dps + n;                     // R-_i
+  double* __restrict__ zz = rms + n;
+  const double sc = b.scale[0];
+  const double lam = b.lam[c] * sc;
+  const double* __restrict__ d = b.dd;
+  const double* __restrict__ e = b.ee;
+  const double piv = 0x1p-900, big = 0x1p+900;
+  if (lane == 0) {
+    // forward: p_i = (d_i - lam) p_{i-1} - e_{i-1}^2 p_{i-2}
+    double pm = 1.0, pc = fma(__ldg(d), sc, -lam);
+    dps[0] = pc;
+#pragma unroll 4
+    for (int i = 1; i < n; ++i) {
+      const double ei = __ldg(e + i - 1) * sc;
+      const double pn = fma(fma(__ldg(d + i), sc, -lam), pc, -(ei * ei) * pm);
+      dps[i] = trd_div(pn, pc);
+      pm = pc;
+      pc = pn;
+      if ((i & 7) == 0) trd_rescale_pair(pc, pm);
+    }
+    // backward: r_i = (d_i - lam) r_{i+1} - e_i^2 r_{i+2}; gamma on the fly
+    double rn = 1.0, rc = fma(__ldg(d + n - 1), sc, -lam);
+    rms[n - 1] = rc;
+    auto clampd = [&](double x) { return fabs(x) < piv ? -piv : fmin(fmax(x, -big), big); };
+    int r = n - 1;
+    double best = fabs(clampd(dps[n - 1]));
+#pragma unroll 4
+    for (int i = n - 2; i >= 0; --i) {
+      const double ei = __ldg(e + i) * sc;
+      const double di = fma(__ldg(d + i), sc, -lam);
+      const double rp = fma(di, rc, -(ei * ei) * rn);
+      const double rmi = trd_div(rp, rc);
+      rms[i] = rmi;
+      rn = rc;
+      rc = rp;
+      if ((i & 7) == 0) trd_rescale_pair(rc, rn);
+      const double gam = clampd(dps[i]) + clampd(rmi) - di;
+      if (fabs(gam) < best) {
+        best = fabs(gam);
+        r = i;
+      }
+    }
+    // z
+    double ss = 1.0, zi = 1.0;
+    zz[r] = 1.0;
+#pragma unroll 4
+    for (int i = r - 1; i >= 0; --i) {
+      zi = -trd_div(__ldg(e + i) * sc, clampd(dps[i])) * zi;
+      zz[i] = zi;
+      ss = fma(zi, zi, ss);
+    }
+    zi = 1.0;
+#pragma unroll 4
+    for (int i = r; i < n - 1; ++i) {
+      zi = -trd_div(__ldg(e + i) * sc, clampd(rms[i + 1])) * zi;
+      zz[i + 1] = zi;
+      ss = fma(zi, zi, ss);
+    }
+    const double inv = 1.0 / sqrt(ss);
+    if (!(isfinite(inv) && inv > 0.0)) atomicExch(b.info + 1, 1);
+    rms[0] = inv;  // hand the norm to the warp
+  }
+  __syncwarp();
+  const double inv = rms[0];
+  double* __restrict__ out = b.z + (size_t)c * n;
+  for (int i = lane; i < n; i += 32) out[i] = zz[i] * inv;
+}
+
+// V = Q Z = H_0 H_1 ... H_{n-3} Z, one warp per column c < k with the column
+// in registers (NQ = ceil(n / 32) per lane).  The reflector rows stream
+// through shared memory by TMA bulk copies (cp.async.bulk, one mbarrier per
+// stage of TRD_BCH rows, TRD_BST stages, thread 0 the producer), shared by
+// the CTA's TRD_BW warps.  Output V[i * ldv + c].
+constexpr int TRD_BW = 8, TRD_BCH = 4, TRD_BST = 3;
+__device__ __forceinline__ uint32_t trd_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int NQ>
+__global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int n, int K, double* __restrict__ V,
+                                                                   int ldv, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) double bk_sm[];  // TRD_BST x TRD_BCH x ldh
+  __shared__ __align__(8) uint64_t bars[TRD_BST];
+  const int k = b.info[0];
+  const int lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * TRD_BW;
+  if (c0 >= k) return;
+  const int c = c0 + (threadIdx.x >> 5);
+  const bool active = c < k;
+  const int ldh = (n + 1) & ~1;
+  const int nref = n - 2;  // reflectors 0 .. n-3, applied from the top
+  const int nch = (nref + TRD_BCH - 1) / TRD_BCH;
+  auto issue = [&](int ch) {  // thread 0
+    const int st = ch % TRD_BST;
+    const int jtop = nref - 1 - ch * TRD_BCH;
+    uint32_t bytes = 0;
+    for (int r = 0; r < TRD_BCH; ++r) {
+      const int j = jtop - r;
+      if (j < 0) break;
+      bytes += (uint32_t)(ldh - ((j + 1) & ~1)) * 8u;
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(trd_smem_u32(bars + st)), "r"(bytes)
+                 : "memory");
+    for (int r = 0; r < TRD_BCH; ++r) {
+      const int j = jtop - r;
+      if (j < 0) break;
+      const int a0 = (j + 1) & ~1;
+      double* dst = bk_sm + ((size_t)st * TRD_BCH + r) * ldh + a0;
+      const double* src = b.hv + (int64_t)j * ldh + a0;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              trd_smem_u32(dst)),
+          "l"(src), "r"((uint32_t)(ldh - a0) * 8u), "r"(trd_smem_u32(bars + st))
+          : "memory");
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < TRD_BST; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(trd_smem_u32(bars + st)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int ch = 0; ch < TRD_BST && ch < nch; ++ch) issue(ch);
+  }
+  double z[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int i = lane + 32 * q;
+    z[q] = (active && i < n) ? b.z[(size_t)c * n + i] : 0.0;
+  }
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch % TRD_BST;
+    const uint32_t parity = (uint32_t)(ch / TRD_BST) & 1u;
+    asm volatile(
+        "{\n.reg .pred p;\nTRD_W_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra TRD_W_%=;\n}\n" ::"r"(
+            trd_smem_u32(bars + st)),
+        "r"(parity)
+        : "memory");
+    const int jtop = nref - 1 - ch * TRD_BCH;
+    for (int r = 0; r < TRD_BCH; ++r) {
+      const int j = jtop - r;
+      if (j < 0) break;
+      const double bet = __ldg(b.beta + j);
+      if (bet == 0.0) continue;
+      const double* h = bk_sm + ((size_t)st * TRD_BCH + r) * ldh;
+      const int q0 = (j + 1) >> 5;  // lower q hold only rows <= j for every lane
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        if (q >= q0 && i > j && i < n) {
+          if (q & 1) acc1 = fma(h[i], z[q], acc1);
+          else acc0 = fma(h[i], z[q], acc0);
+        }
+      }
+      const double s = bet * warp_sum(acc0 + acc1);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        if (q >= q0 && i > j && i < n) z[q] = fma(-s, h[i], z[q]);
+      }
+    }
+    __syncthreads();  // stage st consumed by every warp
+    if (threadIdx.x == 0 && ch + TRD_BST < nch) issue(ch + TRD_BST);
+  }
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      if (i < n) V[(int64_t)i * ldv + c] = z[q];
+    }
+  }
+}
+
+// Eigenvalues onto diag(B~) (svt_weights), V zero outside the k computed
+// columns; a failed solve hands V = I to the Jacobi fallback.
+__global__ void trd_commit_kernel(PcpDev* st, TrdBuf b, int n, int np, double* __restrict__ Bm,
+                                  double* __restrict__ V) {
+  if (st->done || st->jac_skip) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->eig_skip = 1;
+    return;
+  }
+  const int k = b.info[0];
+  bool ok = b.info[1] == 0;
+  for (int c = 0; c < k && ok; ++c) ok = isfinite(b.lam[c]);
+  const int64_t tot = (int64_t)np * np;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / np), c = (int)(e % np);
+    if (!ok) V[e] = i == c ? 1.0 : 0.0;
+    else if (c >= k || i >= n) V[e] = 0.0;
+  }
+  if (ok)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+      Bm[(int64_t)i * (np + 1)] = i < k ? b.lam[i] : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->trd_ok = ok;
+    st->eig_skip = ok;
+    if (ok && k == 0) st->jac_skip = 1;  // rank 0: no W~ / Z products, Z cleared
+  }
+}
+
+}  // namespace
+
+int trd_max_n() { return TRD_LL * TRD_T; }
+
+size_t trd_bytes(int n) {
+  const size_t nn = (size_t)n * n;
+  // hv (n x ldh), z: 2 n^2 + n; beta, dd, ee, lam: 4 n; pll, rowll: 4 n records; sll; scale, info
+  return 8 * (2 * nn + 5 * (size_t)n) + 16 * (4 * (size_t)n + 2 * TRD_MAXG) + 8 * 4 + 4 * 16 + 12 * 256;
+}
+
+void trd_carve(TrdBuf* b, char* base, int n) {
+  const size_t nn = (size_t)n * n;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    char* p = base + off;
+    off += bytes;
+    return p;
+  };
+  b->hv = (double*)take(8 * (size_t)n * ((n + 1) & ~1));
+  b->z = (double*)take(8 * nn);
+  b->beta = (double*)take(8 * (size_t)n);
+  b->dd = (double*)take(8 * (size_t)n);
+  b->ee = (double*)take(8 * (size_t)n);
+  b->lam = (double*)take(8 * (size_t)n);
+  b->pll = (uint4*)take(16 * 2 * (size_t)n);
+  b->rowll = (uint4*)take(16 * 2 * (size_t)n);
+  b->sll = (uint4*)take(16 * 2 * (size_t)TRD_MAXG);
+  b->scale = (double*)take(8 * 4);
+  b->info = (int*)take(4 * 16);
+}
+
+static int trd_grid(int n) {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int G = std::min(std::min(sms, TRD_MAXG), std::max(1, (n + TRD_W - 1) / TRD_W));
+  const char* e = getenv("MLR_TRD_G");
+  if (e) G = std::max(1, std::min(std::min(sms, TRD_MAXG), atoi(e)));
+  if ((n + G - 1) / G > TRD_W) G = (n + TRD_W - 1) / TRD_W;
+  return G;
+}
+
+bool trd_supported(int n) {
+  if (n < 3 || n > trd_max_n()) return false;
+  const int G = trd_grid(n);
+  if (G > TRD_MAXG) return false;
+  const int R = (n + G - 1) / G;
+  const size_t smem = 8 * ((size_t)R * n + 5 * (size_t)n);
+  return smem <= 224 * 1024 && 8 * 12 * (size_t)(n + 1) <= 200 * 1024 && 24 * (size_t)n <= 200 * 1024;
+}
+
+// Eigenpairs of B (n x n in the leading block of an np x np buffer) above
+// tau^2 into V (np x np, columns 0..k-1) and diag(B); Jacobi fallback flag in
+// st->eig_skip.  skip: device flag (done or rank-0 certified).
+int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const double* tau, const int* skip,
+            cudaStream_t s) {
+  const int G = trd_grid(n);
+  const int R = (n + G - 1) / G;
+  const size_t smem = 8 * ((size_t)R * n + 5 * (size_t)n);
+  // the publication records carry step tags >= 1: clear them (and info)
+  MLR_CUDA(cudaMemsetAsync(b->pll, 0, 16 * 2 * (size_t)n, s));
+  MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
+  MLR_CUDA(cudaMemsetAsync(b->sll, 0, 16 * 2 * (size_t)TRD_MAXG, s));
+  MLR_CUDA(cudaMemsetAsync(b->info, 0, 4 * 16, s));
+  MLR_CUDA(cudaFuncSetAttribute(trd_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  {
+    const double* bp = Bm;
+    int ld = np, nn = n;
+    TrdBuf bb = *b;
+    static const int trace = getenv("MLR_TRD_TRACE") ? 1 : 0;
+    int tr = trace;
+    static const int slp0 = getenv("MLR_TRD_SLEEP") ? atoi(getenv("MLR_TRD_SLEEP")) : 0;
+    int slp = slp0;
+    void* args[] = {(void*)&bp, &ld, &nn, &bb, (void*)&skip, &tr, &slp};
+    MLR_CUDA(cudaLaunchCooperativeKernel((void*)trd_reduce_kernel, dim3(G), dim3(TRD_T), args, smem, s));
+  }
+  const int wpb = 8;  // warps per bisection CTA
+  MLR_CUDA(cudaFuncSetAttribute(trd_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 * n)));
+  trd_bisect_kernel<<<(n + wpb - 1) / wpb, 32 * wpb, 16 * (size_t)n, s>>>(*b, n, tau, skip);
+  MLR_LAUNCH_CHECK("trd_bisect_kernel");
+  {
+    const int vw = (int)std::max<size_t>(1, std::min<size_t>(TRD_VW, (200 * 1024) / (24 * (size_t)n)));
+    const size_t vsm = 24 * (size_t)n * vw;
+    MLR_CUDA(cudaFuncSetAttribute(trd_vectors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
+    trd_vectors_kernel<<<(n + vw - 1) / vw, 32 * vw, vsm, s>>>(*b, n, skip);
+  }
+  MLR_LAUNCH_CHECK("trd_vectors_kernel");
+  const int nq = (n + 31) / 32;
+  const int bg = (n + TRD_BW - 1) / TRD_BW;
+  const size_t bsm = 8 * (size_t)TRD_BST * TRD_BCH * ((n + 1) & ~1);
+#define TRD_BACK(NQ)                                                                                \
+  if (nq <= NQ) {                                                                                   \
+    MLR_CUDA(cudaFuncSetAttribute(trd_back_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  (int)bsm));                                                       \
+    trd_back_kernel<NQ><<<bg, TRD_BW * 32, bsm, s>>>(*b, n, n, V, np, skip);                        \
+    MLR_LAUNCH_CHECK("trd_back_kernel");                                                            \
+  } else
+  TRD_BACK(4) TRD_BACK(8) TRD_BACK(16) TRD_BACK(24) TRD_BACK(32) TRD_BACK(40) TRD_BACK(48) TRD_BACK(64) {
+    set_error("trd_eig: n too large");
+    return kErrArg;
+  }
+#undef TRD_BACK
+  trd_commit_kernel<<<std::min<int>(ceil_div((int64_t)np * np, 256), 592), 256, 0, s>>>(st, *b, n, np, Bm, V);
+  MLR_LAUNCH_CHECK("trd_commit_kernel");
+  return kOk;
+}
+
+}  // namespace mlr

@@ -258,6 +258,13 @@ def test_time_budget_zero_stops_after_first_iteration():
 def test_time_budget_stops_at_first_iteration_past_budget(solver):
     d, mask = make_config("C2", 0)
     budget = 0.02
+    # warm-up (lazy kernel loading would otherwise land in the first timed iteration)
+    lam = 1 / np.sqrt(2000)
+    if solver == "pcp":
+        pkg.ml_ialm_solve(d, pkg.PcpOptions(lam=lam, tol_feasibility=1e-12, max_iters=2, levels=250))
+    else:
+        pkg.ml_fwt_solve(d, None, pkg.CpcpOptions(lambda_l=lam, lambda_s=lam / np.sqrt(2000), tol=1e-12, max_iters=2,
+                                                  levels=250, collect_rank=False))
     if solver == "pcp":
         st = pkg.ml_ialm_solve(d, pkg.PcpOptions(lam=1 / np.sqrt(2000), tol_feasibility=1e-12, max_iters=500,
                                                  levels=250, time_budget=budget))

@@ -406,12 +406,13 @@ def test_jacobi_eigensolver_vs_lapack(n):
 # --------------------------------------------- rank-0 certificate (pcp.cu)
 @pytest.mark.parametrize("m,n,rank,levels", [(600, 600, 30, 150),     # one-CTA register Cholesky
                                              (1200, 1200, 60, 300)])  # grid panel Cholesky (n_H > 268)
-def test_rank0_certificate_matches_oracle(m, n, rank, levels):
+def test_rank0_certificate_matches_oracle(m, n, rank, levels, monkeypatch):
     """Iterations whose SVT keeps nothing (rank 0, pcp.py:258-262) skip the
     eigensolve after the Cholesky certificate; the per-iteration rank column
     and the iterates must still match the oracle, and the skipped iterations
     must be exactly the rank-0 ones."""
     from paper_2206_13369_b200 import pcp as P
+    monkeypatch.setenv("MLR_EIG", "jacobi")  # the sweep count tells which iterations skipped the eigensolve
     d, _ = O.gaussian_rpca(m, n, rank, 0.10, 0)
     ref = O.ml_ialm(d, levels=levels, tol=1e-7)
     sink = []
@@ -429,3 +430,26 @@ def test_rank0_certificate_matches_oracle(m, n, rank, levels):
     assert relf(st.l, ref.l) <= 1e-10 and relf(st.s, ref.s) <= 1e-10
     sweeps = sink[0]["jac_sweeps"][:len(ranks)]
     assert [s == 0 for s in sweeps] == [r == 0 for r in ranks]
+
+
+# ---------------------------------------- coarse eigensolvers (trd.cu / jacobi2.cu)
+@pytest.mark.parametrize("eig", ["trd", "jacobi"])
+@pytest.mark.parametrize("m,n,rank,levels,dtype", [(600, 600, 30, 150, np.float64),
+                                                   (1200, 1200, 60, 300, np.float64),
+                                                   (1400, 1300, 40, 650, np.float32)])
+def test_coarse_eigensolvers_match_oracle(eig, m, n, rank, levels, dtype, monkeypatch):
+    """Both coarse eigensolvers -- the tridiagonal one (Householder reduction,
+    Sturm bisection, twisted-factorisation vectors, trd.cu) and the warm-started
+    block Jacobi -- reproduce the reference's SVT (pcp.py:257-262) through the
+    whole solve: same iterations and rank column, iterates to 1e-10 (FP64) /
+    1e-4 (FP32, the reference computing in FP64 on the FP32-rounded input)."""
+    monkeypatch.setenv("MLR_EIG", eig)
+    d, _ = O.gaussian_rpca(m, n, rank, 0.10, 1)
+    d = d.astype(dtype)
+    ref = O.ml_ialm(d.astype(np.float64), levels=levels, tol=1e-6)
+    st = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=levels, tol_feasibility=1e-6))
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    assert abs(st.iter - ref.iter) <= (0 if dtype == np.float64 else 1)
+    n_cmp = min(st.iter, ref.iter)
+    assert [h.rank_l for h in st.history][:n_cmp] == [h.rank_l for h in ref.history][:n_cmp]
+    assert relf(st.l, ref.l) <= tol and relf(st.s, ref.s) <= tol
