@@ -210,14 +210,12 @@ static void pcp_params(PcpPlan& p, const ChainDev& ch, int64_t m_local, int64_t 
   p.jac_tol_host = 1e-14;
   p.jac_max_sweeps = 60;
   {
-    // coarse eigensolver: "trd" (tridiagonal, trd.cu), "jacobi" (warm-started
-    // block Jacobi), default by size: measured on B200, the cluster Jacobi
-    // matches the tridiagonal solver for 192 < n_H <= 512 (C2: 29 vs 31 ms
-    // per solve), the tridiagonal solver wins below (C1: 20.5 vs 24.9 ms) and
-    // above (C5: 172 vs 257 ms)
+    // coarse eigensolver: the tridiagonal solver (trd.cu) unless MLR_EIG=jacobi
+    // (the warm-started block Jacobi).  Measured on B200 (eigensolve phase per
+    // solve, trd vs Jacobi): C1 17.8 vs 24.9 ms, C2 26.7 vs 29.5 ms, C5 145 vs
+    // 257 ms
     const char* e = getenv("MLR_EIG");
-    const std::string ev = e ? e : "";
-    const bool want = ev == "trd" || (ev != "jacobi" && (ch.nh <= 192 || ch.nh > 512));
+    const bool want = !(e && std::string(e) == "jacobi");
     p.trd_on = want && trd_supported(ch.nh);
   }
 }

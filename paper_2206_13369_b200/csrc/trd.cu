@@ -201,7 +201,10 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
       if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
       if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
     }
-    if (trace) __syncthreads();
+    // this CTA's sentinel (one 128-byte line per CTA): readers poll it
+    // instead of every p record, so each line has G pollers, not G x 8
+    __syncthreads();
+    if (tid == 0) ll_store(b.sent + ((size_t)(j & 1) * TRD_MAXG + g) * 8, 0.0, tag);
     if (trs) tr[1] = clock64();
     // (2) the pending update of step j - 1 on the local rows (k >= j + 1);
     //     the owner of row j + 1 publishes it (through step j - 1)
@@ -224,10 +227,27 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         my_row[k] = x0;
         if (pub) ll_store(pub + k, x0, tag);
       }
+      if (pub) {
+        __syncwarp();
+        if (lane == 0) ll_store(b.sent + ((size_t)2 * TRD_MAXG + (m1 & 1)) * 8, 0.0, tag);
+      }
     }
     if (trace) __syncthreads();
     if (trs) tr[2] = clock64();
-    // (3) the exchange: all of p and the replica of row j + 1; K partials
+    // (3) the exchange: all of p and the replica of row j + 1; K partials.
+    //     The sentinels first (one poller per source line), then every record
+    //     is read and its tag checked (a relaxed store may still be in
+    //     flight: those are polled again)
+    if (tid < G) {
+      const uint4* sp = b.sent + ((size_t)(j & 1) * TRD_MAXG + tid) * 8;
+      while (ll_ld(sp).y != tag) {
+      }
+    } else if (tid == TRD_T - 1 && j > 0) {
+      const uint4* sp = b.sent + ((size_t)2 * TRD_MAXG + (m1 & 1)) * 8;
+      while (ll_ld(sp).y != tag) {
+      }
+    }
+    __syncthreads();
     {
       const uint4* pl = b.pll + (size_t)(j & 1) * n;
       const uint4* rl = b.rowll + (size_t)(m1 & 1) * n;
@@ -684,7 +704,8 @@ int trd_max_n() { return TRD_LL * TRD_T; }
 size_t trd_bytes(int n) {
   const size_t nn = (size_t)n * n;
   // hv (n x ldh), z: 2 n^2 + n; beta, dd, ee, lam: 4 n; pll, rowll: 4 n records; sll; scale, info
-  return 8 * (2 * nn + 5 * (size_t)n) + 16 * (4 * (size_t)n + 2 * TRD_MAXG) + 8 * 4 + 4 * 16 + 12 * 256;
+  return 8 * (2 * nn + 5 * (size_t)n) + 16 * (4 * (size_t)n + 2 * TRD_MAXG) + 128 * (2 * TRD_MAXG + 2) + 8 * 4 +
+         4 * 16 + 14 * 256;
 }
 
 void trd_carve(TrdBuf* b, char* base, int n) {
@@ -705,6 +726,7 @@ void trd_carve(TrdBuf* b, char* base, int n) {
   b->pll = (uint4*)take(16 * 2 * (size_t)n);
   b->rowll = (uint4*)take(16 * 2 * (size_t)n);
   b->sll = (uint4*)take(16 * 2 * (size_t)TRD_MAXG);
+  b->sent = (uint4*)take(16 * 8 * (2 * (size_t)TRD_MAXG + 2));
   b->scale = (double*)take(8 * 4);
   b->info = (int*)take(4 * 16);
 }
@@ -744,6 +766,7 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
   MLR_CUDA(cudaMemsetAsync(b->pll, 0, 16 * 2 * (size_t)n, s));
   MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
   MLR_CUDA(cudaMemsetAsync(b->sll, 0, 16 * 2 * (size_t)TRD_MAXG, s));
+  MLR_CUDA(cudaMemsetAsync(b->sent, 0, 16 * 8 * (2 * (size_t)TRD_MAXG + 2), s));
   MLR_CUDA(cudaMemsetAsync(b->info, 0, 4 * 16, s));
   MLR_CUDA(cudaFuncSetAttribute(trd_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
