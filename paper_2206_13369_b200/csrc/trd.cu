@@ -120,27 +120,36 @@ __device__ __forceinline__ void trd_reflector(double alpha, double s, double& be
 // and the update itself is applied after p is published, while the
 // exchange is in flight.  The exchange carries p only: every CTA has v and
 // all of p, so K = beta/2 p . v needs no separate partial sums.
+// NQ > 0: each warp keeps its row in registers (element k = lane + 32 q),
+// which halves the shared-memory traffic of the matvec and the update;
+// NQ = 0: rows in shared memory (any n up to the limits).
+template <int NQ>
 __global__ void __launch_bounds__(TRD_T, 1)
 trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const int* __restrict__ skip, int trace, int slp) {
   if (skip && *skip) return;
+#ifdef TRD_TRACE
   long long tr[8];
   const bool tron = trace && threadIdx.x == 0;
+#else
+  trace = 0;
+#endif
   extern __shared__ double trd_sm[];
   const int G = gridDim.x, g = blockIdx.x;
   const int R = (n + G - 1) / G;  // <= TRD_W (host checks)
   const int ldh = (n + 1) & ~1;
-  double* rows = trd_sm;          // R x n: rows g, g + G, g + 2G, ...
-  double* vsb = rows + (size_t)R * n;  // 2 x n: v_j by step parity
+  double* rows = trd_sm;          // NQ = 0: R x n rows g, g + G, g + 2G, ...
+  double* vsb = rows + (NQ > 0 ? 0 : (size_t)R * n);  // 2 x n: v_j by step parity
   double* wpv = vsb + 2 * (size_t)n;   // w of the pending update
   double* ps = wpv + n;
   double* cur = ps + n;                // the replica of row j + 1
   __shared__ double kpart[TRD_W], sqpart[TRD_W], s1part[TRD_W], s2part[TRD_W], s_bs[2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int r = 0; r < R; ++r) {
-    const int i = g + r * G;
-    if (i < n)
-      for (int k = tid; k < n; k += TRD_T) rows[(size_t)r * n + k] = B[(int64_t)i * ldb + k];
-  }
+  if (NQ == 0)
+    for (int r = 0; r < R; ++r) {
+      const int i = g + r * G;
+      if (i < n)
+        for (int k = tid; k < n; k += TRD_T) rows[(size_t)r * n + k] = B[(int64_t)i * ldb + k];
+    }
   {
     double q = 0.0;
     for (int k = tid; k < n; k += TRD_T) {
@@ -173,16 +182,26 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
   const int my_i = g + wid * G;  // the row this warp owns (if < n and wid < R)
   const bool has_row = wid < R && my_i < n;
   double* my_row = rows + (size_t)wid * n;
+  double rr[NQ > 0 ? NQ : 1];
+  if constexpr (NQ > 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = lane + 32 * q;
+      rr[q] = (has_row && k < n) ? B[(int64_t)my_i * ldb + k] : 0.0;
+    }
+  }
   for (int j = 0; j < n - 2; ++j) {
     const int m1 = j + 1;
     const uint32_t tag = (uint32_t)j + 1u;
     const double* vc = vsb + (size_t)(j & 1) * n;         // v_j
     const double* vp = vsb + (size_t)((j + 1) & 1) * n;   // v_{j-1} (pending)
+#ifdef TRD_TRACE
     const bool trs = tron && j == n / 2;
     if (trs) {
       tr[0] = clock64();
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[7]));
     }
+#endif
     // (1) p_i = beta (A_i . v - v'_i s1 - w'_i s2) for the local rows i >= j + 1
     if (has_row && my_i >= m1) {
       double s1 = 0.0, s2 = 0.0;
@@ -191,12 +210,29 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         s2 = warp_sum(lane < TRD_W ? s2part[lane] : 0.0);
       }
       double a0 = 0.0, a1 = 0.0;
-      int k = m1 + lane;
-      for (; k + 32 < n; k += 64) {
-        a0 = fma(my_row[k], vc[k], a0);
-        a1 = fma(my_row[k + 32], vc[k + 32], a1);
+      if constexpr (NQ > 0) {
+        double a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int k = lane + 32 * q;
+          if (k >= m1 && k < n) {
+            const double t = rr[q] * vc[k];
+            if ((q & 3) == 0) a0 += t;
+            else if ((q & 3) == 1) a1 += t;
+            else if ((q & 3) == 2) a2 += t;
+            else a3 += t;
+          }
+        }
+        a0 += a2;
+        a1 += a3;
+      } else {
+        int k = m1 + lane;
+        for (; k + 32 < n; k += 64) {
+          a0 = fma(my_row[k], vc[k], a0);
+          a1 = fma(my_row[k + 32], vc[k + 32], a1);
+        }
+        if (k < n) a0 = fma(my_row[k], vc[k], a0);
       }
-      if (k < n) a0 = fma(my_row[k], vc[k], a0);
       double raw = warp_sum(a0 + a1);
       if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
       if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
@@ -205,13 +241,25 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     // instead of every p record, so each line has G pollers, not G x 8
     __syncthreads();
     if (tid == 0) ll_store(b.sent + ((size_t)(j & 1) * TRD_MAXG + g) * 8, 0.0, tag);
+#ifdef TRD_TRACE
     if (trs) tr[1] = clock64();
+#endif
     // (2) the pending update of step j - 1 on the local rows (k >= j + 1);
     //     the owner of row j + 1 publishes it (through step j - 1)
     if (j > 0 && has_row && my_i >= m1) {
       const double vi = vp[my_i], wi = wpv[my_i];
       uint4* pub = my_i == m1 ? b.rowll + (size_t)(m1 & 1) * n : nullptr;
-      int k = m1 + lane;
+      if constexpr (NQ > 0) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int k = lane + 32 * q;
+          if (k >= m1 && k < n) {
+            rr[q] = fma(-vi, wpv[k], fma(-wi, vp[k], rr[q]));
+            if (pub) ll_store(pub + k, rr[q], tag);
+          }
+        }
+      }
+      int k = NQ > 0 ? n : m1 + lane;
       for (; k + 32 < n; k += 64) {
         const double x0 = fma(-vi, wpv[k], fma(-wi, vp[k], my_row[k]));
         const double x1 = fma(-vi, wpv[k + 32], fma(-wi, vp[k + 32], my_row[k + 32]));
@@ -232,8 +280,10 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         if (lane == 0) ll_store(b.sent + ((size_t)2 * TRD_MAXG + (m1 & 1)) * 8, 0.0, tag);
       }
     }
+#ifdef TRD_TRACE
     if (trace) __syncthreads();
     if (trs) tr[2] = clock64();
+#endif
     // (3) the exchange: all of p and the replica of row j + 1; K partials.
     //     The sentinels first (one poller per source line), then every record
     //     is read and its tag checked (a relaxed store may still be in
@@ -251,49 +301,64 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     {
       const uint4* pl = b.pll + (size_t)(j & 1) * n;
       const uint4* rl = b.rowll + (size_t)(m1 & 1) * n;
-      uint4 pr[TRD_LL], cr[TRD_LL];
+      double q = 0.0;
+      {
+        uint4 pr[TRD_LL];
 #pragma unroll
-      for (int u = 0; u < TRD_LL; ++u) {
-        const int k = m1 + tid + u * TRD_T;
-        if (k < n) {
-          pr[u] = ll_ld(pl + k);
-          if (j > 0) cr[u] = ll_ld(rl + k);
+        for (int u = 0; u < TRD_LL; ++u) {
+          const int k = m1 + tid + u * TRD_T;
+          if (k < n) pr[u] = ll_ld(pl + k);
+        }
+#pragma unroll
+        for (int u = 0; u < TRD_LL; ++u) {
+          const int k = m1 + tid + u * TRD_T;
+          if (k < n) {
+            while (pr[u].y != tag || pr[u].w != tag) {
+              if (slp) __nanosleep(slp);
+              pr[u] = ll_ld(pl + k);
+            }
+            const double p = ll_val(pr[u]);
+            ps[k] = p;
+            q = fma(p, vc[k], q);
+          }
         }
       }
-      double q = 0.0;
+      if (j > 0) {
+        uint4 cr[TRD_LL];
 #pragma unroll
-      for (int u = 0; u < TRD_LL; ++u) {
-        const int k = m1 + tid + u * TRD_T;
-        if (k < n) {
-          while (pr[u].y != tag || pr[u].w != tag) {
-            if (slp) __nanosleep(slp);
-            pr[u] = ll_ld(pl + k);
-          }
-          const double p = ll_val(pr[u]);
-          ps[k] = p;
-          q = fma(p, vc[k], q);
-          if (j > 0) {
+        for (int u = 0; u < TRD_LL; ++u) {
+          const int k = m1 + tid + u * TRD_T;
+          if (k < n) cr[u] = ll_ld(rl + k);
+        }
+#pragma unroll
+        for (int u = 0; u < TRD_LL; ++u) {
+          const int k = m1 + tid + u * TRD_T;
+          if (k < n) {
             while (cr[u].y != tag || cr[u].w != tag) {
               if (slp) __nanosleep(slp);
               cr[u] = ll_ld(rl + k);
             }
             cur[k] = ll_val(cr[u]);
-          } else {
-            cur[k] = B[ldb + k];
           }
         }
+      } else {
+        for (int k = m1 + tid; k < n; k += TRD_T) cur[k] = B[ldb + k];
       }
       q = warp_sum(q);
       if (lane == 0) kpart[wid] = q;
     }
+#ifdef TRD_TRACE
     if (trs) {
       tr[3] = clock64();
       long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
       tr[7] = gt - tr[7];
     }
+#endif
     __syncthreads();
+#ifdef TRD_TRACE
     if (trs) tr[4] = clock64();
+#endif
     // (4) w_j = p - K v_j (the new pending update); the replica row j + 1
     //     through step j and its sum of squares beyond j + 2
     {
@@ -348,15 +413,19 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         s2part[wid] = q2;
       }
     }
+#ifdef TRD_TRACE
     if (trs) tr[5] = clock64();
+#endif
     __syncthreads();
     bet = s_bs[0];
+#ifdef TRD_TRACE
     if (trs) {
       tr[6] = clock64();
       printf("trd g=%d j=%d: matvec %lld upd %lld xchg %lld bar %lld w %lld refl %lld total %lld startns %lld\n", g, j,
              tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4], tr[6] - tr[5],
              tr[6] - tr[0], tr[7]);
     }
+#endif
   }
   // the trailing 2 x 2 block: the replica is row n - 2 through step n - 3;
   // row n - 1 still has the update of step n - 3 pending
@@ -367,10 +436,20 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     b.beta[n - 1] = 0.0;
     b.ee[n - 1] = 0.0;
   }
-  if (has_row && lane == 0 && my_i == n - 1) {
-    const double* vl = vsb + (size_t)((n - 3) & 1) * n;
-    const double vi = vl[n - 1], wi = wpv[n - 1];
-    b.dd[n - 1] = fma(-vi, wi, fma(-wi, vi, my_row[n - 1]));
+  if (has_row && my_i == n - 1) {
+    double a = 0.0;
+    if constexpr (NQ > 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (lane + 32 * q == n - 1) a = rr[q];
+    } else {
+      a = my_row[n - 1];
+    }
+    if (lane == (n - 1) % 32) {
+      const double* vl = vsb + (size_t)((n - 3) & 1) * n;
+      const double vi = vl[n - 1], wi = wpv[n - 1];
+      b.dd[n - 1] = fma(-vi, wi, fma(-wi, vi, a));
+    }
   }
 }
 
@@ -761,14 +840,22 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
             cudaStream_t s) {
   const int G = trd_grid(n);
   const int R = (n + G - 1) / G;
-  const size_t smem = 8 * ((size_t)R * n + 5 * (size_t)n);
+  const int nq = (n + 31) / 32;
+  const char* re = getenv("MLR_TRD_REGROWS");
+  const bool regs = !(re && re[0] == '0') && nq <= 16;  // measured: spills above 16 (C5 at 40: 148 -> 198 ms)
+  const size_t smem = 8 * ((regs ? 0 : (size_t)R * n) + 5 * (size_t)n);
   // the publication records carry step tags >= 1: clear them (and info)
   MLR_CUDA(cudaMemsetAsync(b->pll, 0, 16 * 2 * (size_t)n, s));
   MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
   MLR_CUDA(cudaMemsetAsync(b->sll, 0, 16 * 2 * (size_t)TRD_MAXG, s));
   MLR_CUDA(cudaMemsetAsync(b->sent, 0, 16 * 8 * (2 * (size_t)TRD_MAXG + 2), s));
   MLR_CUDA(cudaMemsetAsync(b->info, 0, 4 * 16, s));
-  MLR_CUDA(cudaFuncSetAttribute(trd_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* kfn = (void*)trd_reduce_kernel<0>;
+  if (regs) {
+    if (nq <= 8) kfn = (void*)trd_reduce_kernel<8>;
+    else kfn = (void*)trd_reduce_kernel<16>;
+  }
+  MLR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
     const double* bp = Bm;
     int ld = np, nn = n;
@@ -778,7 +865,7 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     static const int slp0 = getenv("MLR_TRD_SLEEP") ? atoi(getenv("MLR_TRD_SLEEP")) : 0;
     int slp = slp0;
     void* args[] = {(void*)&bp, &ld, &nn, &bb, (void*)&skip, &tr, &slp};
-    MLR_CUDA(cudaLaunchCooperativeKernel((void*)trd_reduce_kernel, dim3(G), dim3(TRD_T), args, smem, s));
+    MLR_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(TRD_T), args, smem, s));
   }
   const int wpb = 8;  // warps per bisection CTA
   MLR_CUDA(cudaFuncSetAttribute(trd_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 * n)));
@@ -791,7 +878,6 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     trd_vectors_kernel<<<(n + vw - 1) / vw, 32 * vw, vsm, s>>>(*b, n, skip);
   }
   MLR_LAUNCH_CHECK("trd_vectors_kernel");
-  const int nq = (n + 31) / 32;
   const int bg = (n + TRD_BW - 1) / TRD_BW;
   const size_t bsm = 8 * (size_t)TRD_BST * TRD_BCH * ((n + 1) & ~1);
 #define TRD_BACK(NQ)                                                                                \
