@@ -74,15 +74,18 @@ def _peaks():
     p = _json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {"hbm_gbs": 6650.0, "_fallback": True}
     own = _json(os.path.join(ROOT, "profiles", "peaks_b200.json")) or {}
     p = dict(p)
-    for k in ("fp64_mma_tflops", "fp32_ffma_tflops", "tf32_tc_tflops"):
+    for k in ("fp64_mma_tflops", "fp64_dfma_tflops", "fp32_ffma_tflops", "tf32_tc_tflops"):
         if k in own:
             p[k] = own[k]
     return p
 
 
 def _traffic(name):
-    t = _json(os.path.join(ROOT, "profiles", f"r03_traffic_{name.lower()}.json"))
-    return (t or {}).get("kernels", {})
+    out = {}
+    for r in ("r03", "r04"):  # later captures override earlier ones
+        t = _json(os.path.join(ROOT, "profiles", f"{r}_traffic_{name.lower()}.json"))
+        out.update((t or {}).get("kernels", {}))
+    return out
 
 
 class ClockSampler:
@@ -345,6 +348,22 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic, 
         add("lanczos", "lz_dtdq_long_kernel + lz_update_cluster (sigma_1: one pass over D per Lanczos step, "
             "TMA-staged rows, 2-CTA clusters)", "hbm", float(b) * m * n, "GB/s", hbm,
             "b m n bytes per Lanczos step (D read once)")
+    trd = real_launches.get("trd_solves")
+    if trd:
+        # Householder tridiagonalisation (4/3 n_H^3, LAPACK dsytrd count) + back-transform of the k
+        # eigenvectors above tau^2 (2 n_H^2 k, dormtr count); bisection / twisted vectors are O(n_H^2)
+        ks = real_launches.get("trd_ranks") or [nh // 2]
+        flops = 4.0 / 3.0 * nh ** 3 + 2.0 * nh ** 2 * statistics.mean(ks)
+        fp64f = peaks.get("fp64_dfma_tflops") or fp64
+        add("jacobi", "trd_reduce_kernel + trd_bisect/vectors/back_kernel (FP64 Householder tridiagonalisation "
+            "in one cooperative grid, Sturm multisection, twisted-factorisation vectors, TMA-staged back-transform)",
+            "tensor", flops, "TFLOP/s", fp64f,
+            "4/3 n_H^3 (reduction) + 2 n_H^2 k (back-transform of the k kept vectors) flops per eigensolve; "
+            "latency-bound: n_H - 2 dependent column steps, one grid-wide exchange each", tkey="trd_reduce_kernel",
+            peak_source="profiles/peaks_b200.json (measured FP64 DFMA; the reduction runs on the FP64 pipe, "
+                        "not the tensor cores)")
+        if "jacobi" in out:
+            out["jacobi"]["us_per_column_step"] = out["jacobi"]["avg_us"] / max(1, nh - 2)
     if sweeps:
         # per sweep: B~ <- J^T B~ J on the symmetric half (n_p/32 (n_p/32 - 1)/2 block pairs per step,
         # 2 x 2 x 32^3 flops each, n_p/16 steps: 4 n_p^3) + V <- V J (4 n_p^3)
@@ -465,9 +484,12 @@ def gpu_arm(args, name, cfg, world, rank, local):
     phase_ms = {k: v[0] for k, v in phases.items()}
     sweeps_all = [x for s in sink for x in s.get("jac_sweeps", [])]
     sweeps = [x for x in sweeps_all if x > 0]
+    trd_solves = sum(1 for x in sweeps_all if x < 0)  # -1: the tridiagonal eigensolver ran (trd.cu)
     k_solve = sum(s.get("iters", 0) for s in sink) or 1
-    real = {"update": k_solve, "gram": k_solve + 1, "jacobi": len(sweeps), "recon": len(sweeps),
-            "lanczos_steps": sink[0].get("lanczos_steps") if sink else None}
+    ranks = [h.rank_l for h in hist]
+    real = {"update": k_solve, "gram": k_solve + 1, "jacobi": len(sweeps) + trd_solves,
+            "recon": len(sweeps) + trd_solves, "lanczos_steps": sink[0].get("lanczos_steps") if sink else None,
+            "trd_solves": trd_solves, "trd_ranks": [r for r, x in zip(ranks, sweeps_all) if x < 0]}
     rl = roofline_entries(name, cfg, phases, sweeps, r1 - r0, world, peaks, _traffic(name), real)
     dominant = max(phase_ms, key=phase_ms.get) if phase_ms else None
     roof = rl.get(dominant) or rl.get("update")

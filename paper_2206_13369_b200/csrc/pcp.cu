@@ -1073,7 +1073,11 @@ __global__ void pcp_finalize_kernel(PcpDev* st, const double* __restrict__ red, 
 
 __global__ void pcp_after_jacobi(PcpDev* st, const int* __restrict__ jac_result, int trd) {
   if (st->done) return;
-  if (st->jac_skip || (trd && st->trd_ok)) {  // rank 0 certified, or the tridiagonal solver succeeded
+  if (trd && st->trd_ok) {  // the tridiagonal solver ran (history: -1)
+    st->jac_sweeps = -1;
+    return;
+  }
+  if (st->jac_skip) {  // rank 0 certified: no eigensolve this iteration
     st->jac_sweeps = 0;
     return;
   }

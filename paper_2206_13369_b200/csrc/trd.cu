@@ -754,7 +754,10 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
 __global__ void trd_commit_kernel(PcpDev* st, TrdBuf b, int n, int np, double* __restrict__ Bm,
                                   double* __restrict__ V) {
   if (st->done || st->jac_skip) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->eig_skip = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->eig_skip = 1;
+      st->trd_ok = 0;
+    }
     return;
   }
   const int k = b.info[0];
