@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int 
 constexpr int TRD_BW = 8, TRD_BCH = 4, TRD_BST = 3;
 __device__ __forceinline__ uint32_t trd_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int NQ>
+template <int NQ, int CPW>
 __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int n, int K, double* __restrict__ V,
                                                                    int ldv, const int* __restrict__ skip) {
   if (skip && *skip) return;
@@ -661,10 +661,9 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
   __shared__ __align__(8) uint64_t bars[TRD_BST];
   const int k = b.info[0];
   const int lane = threadIdx.x & 31;
-  const int c0 = blockIdx.x * TRD_BW;
+  const int c0 = blockIdx.x * TRD_BW * CPW;
   if (c0 >= k) return;
-  const int c = c0 + (threadIdx.x >> 5);
-  const bool active = c < k;
+  const int c = c0 + (threadIdx.x >> 5) * CPW;  // this warp's columns c .. c + CPW - 1
   const int ldh = (n + 1) & ~1;
   const int nref = n - 2;  // reflectors 0 .. n-3, applied from the top
   const int nch = (nref + TRD_BCH - 1) / TRD_BCH;
@@ -698,12 +697,14 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int ch = 0; ch < TRD_BST && ch < nch; ++ch) issue(ch);
   }
-  double z[NQ];
+  double z[CPW][NQ];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int i = lane + 32 * q;
-    z[q] = (active && i < n) ? b.z[(size_t)c * n + i] : 0.0;
-  }
+  for (int u = 0; u < CPW; ++u)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      z[u][q] = (c + u < k && i < n) ? b.z[(size_t)(c + u) * n + i] : 0.0;
+    }
   __syncthreads();
   for (int ch = 0; ch < nch; ++ch) {
     const int st = ch % TRD_BST;
@@ -721,32 +722,46 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
       if (bet == 0.0) continue;
       const double* h = bk_sm + ((size_t)st * TRD_BCH + r) * ldh;
       const int q0 = (j + 1) >> 5;  // lower q hold only rows <= j for every lane
-      double acc0 = 0.0, acc1 = 0.0;
+      double acc[CPW];
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) acc[u] = 0.0;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int i = lane + 32 * q;
         if (q >= q0 && i > j && i < n) {
-          if (q & 1) acc1 = fma(h[i], z[q], acc1);
-          else acc0 = fma(h[i], z[q], acc0);
+          const double hv = h[i];
+#pragma unroll
+          for (int u = 0; u < CPW; ++u) acc[u] = fma(hv, z[u][q], acc[u]);
         }
       }
-      const double s = bet * warp_sum(acc0 + acc1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) acc[u] *= bet;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int i = lane + 32 * q;
-        if (q >= q0 && i > j && i < n) z[q] = fma(-s, h[i], z[q]);
+        if (q >= q0 && i > j && i < n) {
+          const double hv = h[i];
+#pragma unroll
+          for (int u = 0; u < CPW; ++u) z[u][q] = fma(-acc[u], hv, z[u][q]);
+        }
       }
     }
     __syncthreads();  // stage st consumed by every warp
     if (threadIdx.x == 0 && ch + TRD_BST < nch) issue(ch + TRD_BST);
   }
-  if (active) {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int i = lane + 32 * q;
-      if (i < n) V[(int64_t)i * ldv + c] = z[q];
+  for (int u = 0; u < CPW; ++u)
+    if (c + u < k) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n) V[(int64_t)i * ldv + c + u] = z[u][q];
+      }
     }
-  }
 }
 
 // Eigenvalues onto diag(B~) (svt_weights), V zero outside the k computed
@@ -885,13 +900,21 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     trd_vectors_kernel<<<(n + vw - 1) / vw, 32 * vw, vsm, s>>>(*b, n, skip);
   }
   MLR_LAUNCH_CHECK("trd_vectors_kernel");
-  const int bg = (n + TRD_BW - 1) / TRD_BW;
+  const char* cpe = getenv("MLR_TRD_BACK_CPW");
+  const int cpw = cpe ? std::max(1, std::min(2, atoi(cpe))) : 1;  // 2 measured slower at C5 (spills)
+  const int bg = (n + TRD_BW * cpw - 1) / (TRD_BW * cpw);
   const size_t bsm = 8 * (size_t)TRD_BST * TRD_BCH * ((n + 1) & ~1);
 #define TRD_BACK(NQ)                                                                                \
   if (nq <= NQ) {                                                                                   \
-    MLR_CUDA(cudaFuncSetAttribute(trd_back_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                  (int)bsm));                                                       \
-    trd_back_kernel<NQ><<<bg, TRD_BW * 32, bsm, s>>>(*b, n, n, V, np, skip);                        \
+    if (cpw == 2) {                                                                                 \
+      MLR_CUDA(cudaFuncSetAttribute(trd_back_kernel<NQ, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    (int)bsm));                                                     \
+      trd_back_kernel<NQ, 2><<<bg, TRD_BW * 32, bsm, s>>>(*b, n, n, V, np, skip);                   \
+    } else {                                                                                        \
+      MLR_CUDA(cudaFuncSetAttribute(trd_back_kernel<NQ, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    (int)bsm));                                                     \
+      trd_back_kernel<NQ, 1><<<bg, TRD_BW * 32, bsm, s>>>(*b, n, n, V, np, skip);                   \
+    }                                                                                               \
     MLR_LAUNCH_CHECK("trd_back_kernel");                                                            \
   } else
   TRD_BACK(4) TRD_BACK(8) TRD_BACK(16) TRD_BACK(24) TRD_BACK(32) TRD_BACK(40) TRD_BACK(48) TRD_BACK(64) {
