@@ -204,11 +204,8 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
 #endif
     // (1) p_i = beta (A_i . v - v'_i s1 - w'_i s2) for the local rows i >= j + 1
     if (has_row && my_i >= m1) {
-      double s1 = 0.0, s2 = 0.0;
-      if (j > 0) {
-        s1 = warp_sum(lane < TRD_W ? s1part[lane] : 0.0);
-        s2 = warp_sum(lane < TRD_W ? s2part[lane] : 0.0);
-      }
+      double s1 = (j > 0 && lane < TRD_W) ? s1part[lane] : 0.0;
+      double s2 = (j > 0 && lane < TRD_W) ? s2part[lane] : 0.0;
       double a0 = 0.0, a1 = 0.0;
       if constexpr (NQ > 0) {
         double a2 = 0.0, a3 = 0.0;
@@ -233,7 +230,15 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         }
         if (k < n) a0 = fma(my_row[k], vc[k], a0);
       }
-      double raw = warp_sum(a0 + a1);
+      // the row dot and the two correction dots reduced together (three
+      // independent shuffle chains in flight)
+      double raw = a0 + a1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        raw += __shfl_xor_sync(0xffffffffu, raw, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
       if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
       if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
     }
@@ -406,8 +411,11 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         q1 = fma(wpv[k], v, q1);
         q2 = fma(vc[k], v, q2);
       }
-      q1 = warp_sum(q1);
-      q2 = warp_sum(q2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+        q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+      }
       if (lane == 0) {
         s1part[wid] = q1;
         s2part[wid] = q2;
