@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(GTHREADS)
 gemm_f64_kernel(int M, int N, int K, const TA* __restrict__ A, int64_t lda,
                 const TB* __restrict__ B, int64_t ldb, TC* __restrict__ C, int64_t ldc,
                 int64_t c_slice, int k_chunk, double alpha, const double* __restrict__ kscale,
-                const int* __restrict__ skip, int sym_tiles) {
+                const int* __restrict__ skip, int sym_tiles, const int* __restrict__ klim,
+                const int* __restrict__ nlim) {
   if (skip && *skip) return;
   __shared__ double As[2][GBK][GBM + GPAD];
   __shared__ double Bs[2][GBK][GBN + GPAD];
@@ -49,8 +50,9 @@ gemm_f64_kernel(int M, int N, int K, const TA* __restrict__ A, int64_t lda,
     bn = bm + t;
   }
   const int m0 = bm * GBM, n0 = bn * GBN;
+  if (nlim && n0 >= *nlim) return;  // columns >= *nlim of C are not wanted (uniform per CTA)
   const int kb = blockIdx.z * k_chunk;
-  const int ke = min(K, kb + k_chunk);
+  const int ke = min(klim ? min(K, *klim) : K, kb + k_chunk);
   C += (int64_t)blockIdx.z * c_slice;
 
   double acc[4][4][2];
@@ -310,13 +312,14 @@ __global__ void sum_slices_kernel(const double* __restrict__ P, int64_t count, i
 template <typename TA, typename TB, typename TC, bool TA_, bool TB_>
 static int launch(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
                   void* C, int64_t ldc, int64_t c_slice, int splits, double alpha, const double* kscale,
-                  const int* skip, bool sym, cudaStream_t st) {
+                  const int* skip, bool sym, const int* klim, const int* nlim, cudaStream_t st) {
   const int tn = (N + GBN - 1) / GBN, tm = (M + GBM - 1) / GBM;
   const int sym_tiles = (sym && M == N) ? tn : 0;
   dim3 grid(sym_tiles ? tn * (tn + 1) / 2 : tn, sym_tiles ? 1 : tm, splits);
   int chunk = (int)round_up(ceil_div(K, splits), GBK);
   gemm_f64_kernel<TA, TB, TC, TA_, TB_><<<grid, GTHREADS, 0, st>>>(
-      M, N, K, (const TA*)A, lda, (const TB*)B, ldb, (TC*)C, ldc, c_slice, chunk, alpha, kscale, skip, sym_tiles);
+      M, N, K, (const TA*)A, lda, (const TB*)B, ldb, (TC*)C, ldc, c_slice, chunk, alpha, kscale, skip, sym_tiles,
+      klim, nlim);
   MLR_LAUNCH_CHECK("gemm_f64_kernel");
   return kOk;
 }
@@ -331,7 +334,7 @@ int gemm_f64(GemmSpec g, cudaStream_t st) {
   if (g.a_f32 == std::is_same<TA, float>::value && g.b_f32 == std::is_same<TB, float>::value && \
       g.c_f32 == std::is_same<TC, float>::value && g.trans_a == XA && g.trans_b == XB)            \
     return launch<TA, TB, TC, XA, XB>(g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.C, g.ldc,         \
-                                      g.c_slice, g.splits, g.alpha, g.kscale, g.skip, g.sym, st);
+                                      g.c_slice, g.splits, g.alpha, g.kscale, g.skip, g.sym, g.klim, g.nlim, st);
 #define MLR_G_TYPES(XA, XB)                 \
   MLR_G(float, float, float, XA, XB)        \
   MLR_G(float, float, double, XA, XB)       \

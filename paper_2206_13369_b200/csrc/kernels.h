@@ -26,6 +26,8 @@ struct GemmSpec {
   const double* kscale;  // optional: op(A)[:, k] *= kscale[k]
   const int* skip;       // optional device flag: kernel is a no-op when *skip != 0
   bool sym;              // C = op(A) op(B) is symmetric (Gram): upper-triangle tiles, mirrored
+  const int* klim;       // optional device value: only k < *klim contributes (op(A) columns beyond are zero)
+  const int* nlim;       // optional device value: columns >= *nlim of C are not computed (left as they are)
 };
 int gemm_f64(GemmSpec g, cudaStream_t st);
 bool gram128_ok(int n);  // the blocked Gram kernel handles width n (gemm_f64.cu)

@@ -1827,8 +1827,11 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   // so K is split (slices in gram_part, free between Gram passes) and the
   // slices summed in a fixed order
   const int ksplit = p->coarse_ksplit;
-  auto mm = [&](const double* A, bool ta, const double* Bp, bool tb, double* C, const double* ks) {
+  auto mm = [&](const double* A, bool ta, const double* Bp, bool tb, double* C, const double* ks,
+                const int* klim = nullptr, const int* nlim = nullptr) {
     GemmSpec g{};
+    g.klim = klim;
+    g.nlim = nlim;
     g.M = np; g.N = np; g.K = np;
     g.A = A; g.lda = np; g.a_f32 = false; g.trans_a = ta;
     g.B = Bp; g.ldb = np; g.b_f32 = false; g.trans_b = tb;
@@ -1888,12 +1891,15 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   // (jac_skip) and Z is cleared instead.
   skip = &p->dev->jac_skip;
   const bool tc = p->tc_recon && p->m_local > 0;
-  if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;
+  // tridiagonal path: V has k = info[0] nonzero columns, so U' = G^-1 V is
+  // needed only in its first k columns and the products below sum over k
+  const int* kl = use_trd ? p->trd.info + 2 : nullptr;
+  if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr, nullptr, kl))) return rc;
   if (tc) {
     // W~^T = V diag(f) U'^T (the tcgen05 B operand is K-major), then its TF32 hi / lo parts
-    if ((rc = mm(p->Vm, false, p->T1, true, p->Wm, p->fw))) return rc;
+    if ((rc = mm(p->Vm, false, p->T1, true, p->Wm, p->fw, kl))) return rc;
     if ((rc = tc_split_w(p->Wm, p->w_hi, p->w_lo, np, skip, st))) return rc;
-  } else if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw))) {
+  } else if ((rc = mm(p->T1, false, p->Vm, true, p->Wm, p->fw, kl))) {
     return rc;
   }
   p->timer.end(kPhPost, st);

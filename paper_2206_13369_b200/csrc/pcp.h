@@ -48,7 +48,7 @@ struct TrdBuf {
   uint4 *pll, *rowll, *sll;      // flag-carrying publication buffers (2 x n, 2 x n, 2 x 256 records)
   uint4* sent;                   // per-CTA and row sentinels, one 128-byte line each
   double* scale;                 // power-of-two scale of T used by the bisection / vectors
-  int* info;                     // [0] = k (eigenvalues above tau^2), [1] = failure
+  int* info;                     // [0] = k (eigenvalues above tau^2), [1] = failure, [2] = V columns in use
 };
 
 struct PcpPlan {

@@ -796,6 +796,7 @@ __global__ void trd_commit_kernel(PcpDev* st, TrdBuf b, int n, int np, double* _
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
       Bm[(int64_t)i * (np + 1)] = i < k ? b.lam[i] : 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    b.info[2] = ok ? k : np;  // columns of V the SVT products need (the Jacobi fallback fills all)
     st->trd_ok = ok;
     st->eig_skip = ok;
     if (ok && k == 0) st->jac_skip = 1;  // rank 0: no W~ / Z products, Z cleared
