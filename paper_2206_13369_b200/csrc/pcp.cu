@@ -1828,10 +1828,11 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   // slices summed in a fixed order
   const int ksplit = p->coarse_ksplit;
   auto mm = [&](const double* A, bool ta, const double* Bp, bool tb, double* C, const double* ks,
-                const int* klim = nullptr, const int* nlim = nullptr) {
+                const int* klim = nullptr, const int* nlim = nullptr, bool sym = false) {
     GemmSpec g{};
     g.klim = klim;
     g.nlim = nlim;
+    g.sym = sym;
     g.M = np; g.N = np; g.K = np;
     g.A = A; g.lda = np; g.a_f32 = false; g.trans_a = ta;
     g.B = Bp; g.ldb = np; g.b_f32 = false; g.trans_b = tb;
@@ -1846,7 +1847,9 @@ int pcp_svt(PcpPlan* p, const double* red, cudaStream_t st) {
   const bool use_trd = p->trd_on && p->trunc_sv0 == 0;
   if (use_trd) {
     if ((rc = mm(red, false, p->ch.gi, false, p->Xm, nullptr))) return rc;    // X = K G^-1
-    if ((rc = mm(p->ch.gi, false, p->Xm, false, p->Bm, nullptr))) return rc;  // B = G^-1 X
+    // B = G^-1 X, symmetric: upper tiles only, mirrored (large n_p; measured
+    // slower at n_p <= 256, where the halved tile count under-fills the GPU)
+    if ((rc = mm(p->ch.gi, false, p->Xm, false, p->Bm, nullptr, nullptr, nullptr, np >= 512))) return rc;
   } else {
     if ((rc = mm(p->ch.gi, false, p->Vm, false, p->T1, nullptr))) return rc;   // U = G^-1 V
     if ((rc = mm(red, false, p->T1, false, p->Xm, nullptr))) return rc;        // T = K U
