@@ -1547,7 +1547,7 @@ __global__ void eig_permute_kernel(const PcpDev* __restrict__ st, const double* 
   }
 }
 
-__global__ void pcp_jac_skip_done(PcpDev* st) { st->jac_skip = st->done; }
+__global__ void pcp_jac_skip_done(PcpDev* st, int pow) { st->jac_skip = st->done || (pow && st->r0_state == 2); }
 // Z = 0 on a certified rank-0 iteration (the reconstruction GEMM was skipped)
 __global__ void pcp_zero_if_rank0(const PcpDev* __restrict__ st, uint32_t* __restrict__ z, int64_t n) {
   if (st->done || !st->jac_skip) return;
@@ -1588,7 +1588,8 @@ int64_t rank0_smem_bytes(int nh) {
 // (tile (I, J), I >= J, owned by one thread); per step two barriers: the
 // pivot, then the scaled column l broadcast through shared memory.
 __global__ void __launch_bounds__(R0_THREADS) pcp_rank0_test(PcpDev* st, const double* __restrict__ Bt, int np,
-                                                             int nh) {
+                                                             int nh, int decided_if_set) {
+  if (decided_if_set && st->r0_state != 0) return;  // the power bound (or the diagonal) decided
   __shared__ __align__(16) float l[4 * 96];
   __shared__ float piv;
   const int tid = threadIdx.x;
@@ -1701,7 +1702,8 @@ __global__ void __launch_bounds__(R0_THREADS) pcp_rank0_test(PcpDev* st, const d
 constexpr int R0G_B = 8, R0G_T = 256;
 
 __global__ void __launch_bounds__(R0G_T) pcp_rank0_grid(PcpDev* st, const double* __restrict__ Bt, int np, int nh,
-                                                        float* __restrict__ W) {
+                                                        float* __restrict__ W, int decided_if_set) {
+  if (decided_if_set && st->r0_state != 0) return;  // the power bound (or the diagonal) decided
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) float pan[];  // [R0G_B][nh]
   __shared__ int s_big;
@@ -1769,6 +1771,86 @@ __global__ void __launch_bounds__(R0G_T) pcp_rank0_grid(PcpDev* st, const double
   if (b == 0 && tid == 0) st->jac_skip = ok;
 }
 
+// Power-bound rank-0 certificate (before the Cholesky one).  With
+// P = (B + B^T) / (2 tau^2) (PSD), lambda_max(P)^q <= trace(P^q) for
+// q = 2^s, so trace(P^q) <= (1 - margin)^q certifies lambda_max(B) <
+// tau^2 (1 - margin) -- the Cholesky certificate's condition -- and the
+// bound over-estimates lambda_max by at most n^(1/q) (q = 128: 1.06 at
+// n_H = 1250).  s symmetric FP64 squarings (n_p^3 each, upper tiles) cost
+// far less than the panel Cholesky's n_H / 8 grid barriers; when the bound
+// fails, the Cholesky certificate decides as before.
+constexpr int R0_POW_SQUARINGS = 7;
+__global__ void r0_pow_init(PcpDev* st, const double* __restrict__ Bt, int np, int nh, double* __restrict__ P) {
+  __shared__ int s_big;
+  if (st->done) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->r0_state = 3;
+      st->jac_skip = 1;
+    }
+    return;
+  }
+  const double tau = st->tau, t2 = tau * tau;
+  if (threadIdx.x == 0) s_big = 0;
+  __syncthreads();
+  int big = 0;
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) big |= Bt[(int64_t)i * np + i] > t2;
+  if (big) s_big = 1;
+  __syncthreads();
+  if (s_big) {  // a diagonal entry above tau^2: rank > 0 (same verdict in every CTA)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->r0_state = 1;
+      st->jac_skip = 0;
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->r0_state = 0;
+  const double inv = 0.5 / t2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)np * np;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / np), j = (int)(e % np);
+    P[e] = (i < nh && j < nh) ? (Bt[(int64_t)i * np + j] + Bt[(int64_t)j * np + i]) * inv : 0.0;
+  }
+}
+__global__ void __launch_bounds__(1024) r0_pow_decide(PcpDev* st, const double* __restrict__ P, int np, int nh,
+                                                      double thr) {
+  __shared__ double scratch[32];
+  if (st->r0_state != 0) return;
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) v[0] += P[(int64_t)i * np + i];
+  block_sum<1>(v, scratch);
+  if (threadIdx.x == 0 && v[0] <= thr) {  // NaN / inf (lambda > 1 overflowed): not certified
+    st->r0_state = 2;
+    st->jac_skip = 1;
+  }
+}
+static int r0_power_bound(PcpPlan* p, cudaStream_t st) {
+  const int nh = p->ch.nh, np = p->ch.np;
+  double* Pa = p->T1;  // both free between the pre products and the SVT products
+  double* Pb = p->Xm;
+  r0_pow_init<<<148, 256, 0, st>>>(p->dev, p->Bm, np, nh, Pa);
+  MLR_LAUNCH_CHECK("r0_pow_init");
+  const int* skip = &p->dev->r0_state;
+  const int ksplit = p->coarse_ksplit;
+  for (int s = 0; s < R0_POW_SQUARINGS; ++s) {
+    GemmSpec g{};
+    g.M = np; g.N = np; g.K = np;
+    g.A = Pa; g.lda = np; g.a_f32 = false; g.trans_a = false;
+    g.B = Pa; g.ldb = np; g.b_f32 = false; g.trans_b = false;
+    g.C = ksplit > 1 ? p->gram_part : Pb; g.ldc = np; g.c_f32 = false;
+    g.c_slice = ksplit > 1 ? (int64_t)np * np : 0; g.splits = ksplit; g.alpha = 1.0;
+    g.kscale = nullptr; g.skip = skip; g.sym = true;
+    int rc = gemm_f64(g, st);
+    if (rc) return rc;
+    if (ksplit > 1 && (rc = sum_slices(p->gram_part, (int64_t)np * np, (int64_t)np * np, ksplit, Pb, st, skip)))
+      return rc;
+    std::swap(Pa, Pb);
+  }
+  const double thr = std::pow(1.0 - rank0_margin(nh), (double)(1 << R0_POW_SQUARINGS));
+  r0_pow_decide<<<1, 1024, 0, st>>>(p->dev, Pa, np, nh, thr);
+  MLR_LAUNCH_CHECK("r0_pow_decide");
+  return kOk;
+}
+
 int pcp_rank0(PcpPlan* p, cudaStream_t st) {
   const int nh = p->ch.nh, np = p->ch.np;
   const int64_t smem = rank0_smem_bytes(nh);
@@ -1779,6 +1861,15 @@ int pcp_rank0(PcpPlan* p, cudaStream_t st) {
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   const char* env = getenv("MLR_RANK0_TEST");
+  const char* pwe = getenv("MLR_RANK0_POW");
+  // measured: the power bound pays where the Cholesky certificate needs the
+  // grid version (n_H > 268: C5 eigensolve phase 134.4 -> 124.9 ms); below,
+  // the one-CTA register Cholesky is cheaper (C1 17.0 vs 18.7 ms)
+  const int use_pow = !(env && env[0] == '0') && (pwe ? pwe[0] == '1' : rank0_smem_bytes(nh) > max_optin);
+  if (use_pow) {
+    const int rc = r0_power_bound(p, st);
+    if (rc) return rc;
+  }
   const size_t gscratch = (size_t)nh * nh * sizeof(float);
   const size_t gfree = (size_t)p->gram_splits * np * np * sizeof(double);  // Gram slices: free until post
   const char* genv = getenv("MLR_RANK0_GRID");  // 1: grid version for every n_H, 0: never
@@ -1798,18 +1889,19 @@ int pcp_rank0(PcpPlan* p, cudaStream_t st) {
       const double* bm = p->Bm;
       int npv = np, nhv = nh;
       float* w = reinterpret_cast<float*>(p->gram_part);
-      void* args[] = {&dev, &bm, &npv, &nhv, &w};
+      int up = use_pow;
+      void* args[] = {&dev, &bm, &npv, &nhv, &w, &up};
       MLR_CUDA(cudaLaunchCooperativeKernel((void*)pcp_rank0_grid, dim3(sms), dim3(R0G_T), args, psm, st));
       return kOk;
     }
   }
   if (smem > max_optin || (env && env[0] == '0')) {
-    pcp_jac_skip_done<<<1, 1, 0, st>>>(p->dev);
+    pcp_jac_skip_done<<<1, 1, 0, st>>>(p->dev, use_pow);
     MLR_LAUNCH_CHECK("pcp_jac_skip_done");
     return kOk;
   }
   MLR_CUDA(cudaFuncSetAttribute(pcp_rank0_test, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  pcp_rank0_test<<<1, R0_THREADS, smem, st>>>(p->dev, p->Bm, np, nh);
+  pcp_rank0_test<<<1, R0_THREADS, smem, st>>>(p->dev, p->Bm, np, nh, use_pow);
   MLR_LAUNCH_CHECK("pcp_rank0_test");
   return kOk;
 }

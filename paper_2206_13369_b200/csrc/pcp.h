@@ -29,6 +29,7 @@ struct PcpDev {
   int jac_sweeps;
   int trunc, sv, sv_cap;  // ialm_solve: keep only the top-sv triplets, adapt sv (pcp.py:157-165)
   int jac_skip;     // Jacobi not needed this iteration: done, or rank 0 certified (pcp_rank0_test)
+  int r0_state;     // rank-0 test: 0 undecided, 1 rank > 0 (diagonal), 2 certified (power bound), 3 done
   int eig_skip;     // trd path: the Jacobi fallback is not needed (trd solved it, or jac_skip)
   int trd_ok;       // trd path: this iteration's eigenpairs came from the tridiagonal solver
 };
