@@ -589,6 +589,9 @@ __global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int 
   double* __restrict__ zz = rms + n;
   const double sc = b.scale[0];
   const double lam = b.lam[c] * sc;
+  // (nearly) repeated eigenvalues: the twisted vectors of a cluster this
+  // tight are not mutually orthogonal, so the Jacobi takes the iteration
+  if (lane == 0 && c + 1 < k && !(b.lam[c] - b.lam[c + 1] > 1e-10 * fabs(b.lam[c]))) atomicExch(b.info + 1, 1);
   const double* __restrict__ d = b.dd;
   const double* __restrict__ e = b.ee;
   const double piv = 0x1p-900, big = 0x1p+900;
@@ -775,7 +778,7 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
 // Eigenvalues onto diag(B~) (svt_weights), V zero outside the k computed
 // columns; a failed solve hands V = I to the Jacobi fallback.
 __global__ void trd_commit_kernel(PcpDev* st, TrdBuf b, int n, int np, double* __restrict__ Bm,
-                                  double* __restrict__ V) {
+                                  double* __restrict__ V, int force_fail) {
   if (st->done || st->jac_skip) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       st->eig_skip = 1;
@@ -784,7 +787,7 @@ __global__ void trd_commit_kernel(PcpDev* st, TrdBuf b, int n, int np, double* _
     return;
   }
   const int k = b.info[0];
-  bool ok = b.info[1] == 0;
+  bool ok = b.info[1] == 0 && !force_fail;
   for (int c = 0; c < k && ok; ++c) ok = isfinite(b.lam[c]);
   const int64_t tot = (int64_t)np * np;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
@@ -931,7 +934,9 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     return kErrArg;
   }
 #undef TRD_BACK
-  trd_commit_kernel<<<std::min<int>(ceil_div((int64_t)np * np, 256), 592), 256, 0, s>>>(st, *b, n, np, Bm, V);
+  static const int force_fail = getenv("MLR_TRD_FORCE_FALLBACK") ? atoi(getenv("MLR_TRD_FORCE_FALLBACK")) : 0;
+  trd_commit_kernel<<<std::min<int>(ceil_div((int64_t)np * np, 256), 592), 256, 0, s>>>(st, *b, n, np, Bm, V,
+                                                                                       force_fail);
   MLR_LAUNCH_CHECK("trd_commit_kernel");
   return kOk;
 }

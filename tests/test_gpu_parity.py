@@ -22,6 +22,8 @@ import paper_2206_13369_b200 as pkg  # noqa: E402
 from oracle import mlrpca_oracle as O  # noqa: E402
 from paper_2206_13369_b200.datasets import CONFIGS, make_config  # noqa: E402
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 def relf(a, b):
     a = np.asarray(a, dtype=np.float64)
@@ -453,3 +455,46 @@ def test_coarse_eigensolvers_match_oracle(eig, m, n, rank, levels, dtype, monkey
     n_cmp = min(st.iter, ref.iter)
     assert [h.rank_l for h in st.history][:n_cmp] == [h.rank_l for h in ref.history][:n_cmp]
     assert relf(st.l, ref.l) <= tol and relf(st.s, ref.s) <= tol
+
+
+def test_block_diagonal_input_matches_oracle(monkeypatch):
+    """D = blockdiag(X, X): nearly repeated coarse eigenvalues (the stencil
+    couples the two halves only at the group boundary), and the vectors of a
+    cluster closer than 1e-10 relative would go to the Jacobi instead.  The
+    tridiagonal solve must match the oracle (pcp.py:257-262)."""
+    monkeypatch.setenv("MLR_EIG", "trd")
+    x, _ = O.gaussian_rpca(150, 128, 6, 0.10, 4)
+    d = np.zeros((300, 256))
+    d[:150, :128] = x
+    d[150:, 128:] = x
+    ref = O.ml_ialm(d, levels=32, tol=1e-7)
+    st = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=32, tol_feasibility=1e-7))
+    assert st.iter == ref.iter
+    assert [h.rank_l for h in st.history] == [h.rank_l for h in ref.history]
+    assert relf(st.l, ref.l) <= 1e-10 and relf(st.s, ref.s) <= 1e-10
+
+
+def test_tridiagonal_failure_falls_back_to_jacobi():
+    """A tridiagonal solve that reports failure (forced here through
+    MLR_TRD_FORCE_FALLBACK, read at first use, so in a subprocess) hands the
+    iteration to the Jacobi with V = I: same iterates as the oracle, and the
+    history's sweep column shows the Jacobi ran."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2206_13369_b200 as pkg; from paper_2206_13369_b200 import pcp as P\n"
+        "from oracle import mlrpca_oracle as O\n"
+        "d, _ = O.gaussian_rpca(400, 320, 8, 0.1, 6)\n"
+        "ref = O.ml_ialm(d, levels=80, tol=1e-7)\n"
+        "sink = []; P.TIMING_SINK = sink\n"
+        "st = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=80, tol_feasibility=1e-7))\n"
+        "sw = sink[0]['jac_sweeps'][:st.iter]\n"
+        "rl = np.linalg.norm(st.l - ref.l) / np.linalg.norm(ref.l)\n"
+        "assert st.iter == ref.iter and rl <= 1e-10, (st.iter, ref.iter, rl)\n"
+        "assert all(s > 0 for s, h in zip(sw, st.history) if h.rank_l > 0), sw\n"
+        "assert -1 not in sw, sw\n"
+        "print('ok')\n") % (ROOT, ROOT)
+    env = dict(os.environ, MLR_EIG="trd", MLR_TRD_FORCE_FALLBACK="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
