@@ -74,7 +74,7 @@ def _peaks():
     p = _json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {"hbm_gbs": 6650.0, "_fallback": True}
     own = _json(os.path.join(ROOT, "profiles", "peaks_b200.json")) or {}
     p = dict(p)
-    for k in ("fp64_mma_tflops", "fp64_dfma_tflops", "fp32_ffma_tflops", "tf32_tc_tflops"):
+    for k in ("fp64_mma_tflops", "fp64_dfma_tflops", "fp32_ffma_tflops", "tf32_tc_tflops", "ll_record_roundtrip_cycles"):
         if k in own:
             p[k] = own[k]
     return p
@@ -363,7 +363,15 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic, 
             peak_source="profiles/peaks_b200.json (measured FP64 DFMA; the reduction runs on the FP64 pipe, "
                         "not the tensor cores)")
         if "jacobi" in out:
-            out["jacobi"]["us_per_column_step"] = out["jacobi"]["avg_us"] / max(1, nh - 2)
+            # latency view: every column step needs one grid-wide exchange, whose measured round trip
+            # (profiles/peaks_b200.json, tools/ubench_ll.cu) bounds the step from below
+            step = out["jacobi"]["avg_us"] / max(1, nh - 2)
+            rt = (peaks.get("ll_record_roundtrip_cycles") or {}).get("32_pollers")
+            out["jacobi"]["us_per_column_step"] = step
+            if rt:
+                floor = rt / 1965.0  # us at the max SM clock
+                out["jacobi"]["latency_floor_us_per_step"] = floor
+                out["jacobi"]["latency_frac"] = floor / step
     if sweeps:
         # per sweep: B~ <- J^T B~ J on the symmetric half (n_p/32 (n_p/32 - 1)/2 block pairs per step,
         # 2 x 2 x 32^3 flops each, n_p/16 steps: 4 n_p^3) + V <- V J (4 n_p^3)
