@@ -123,7 +123,22 @@ __device__ __forceinline__ void trd_reflector(double alpha, double s, double& be
 // NQ > 0: each warp keeps its row in registers (element k = lane + 32 q),
 // which halves the shared-memory traffic of the matvec and the update;
 // NQ = 0: rows in shared memory (any n up to the limits).
-template <int NQ>
+__device__ __forceinline__ void trd_dsm_st(const double* local_addr, uint32_t cta, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(remote)
+               : "r"((uint32_t)__cvta_generic_to_shared(local_addr)), "r"(cta));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+}
+__device__ __forceinline__ void trd_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// CL: the whole grid is one thread-block cluster (n_H <= 256): p and the
+// replica row are written straight into every CTA's shared memory
+// (st.shared::cluster) and one cluster barrier per step replaces the
+// flag-carrying records and sentinels in L2.
+template <int NQ, bool CL>
 __global__ void __launch_bounds__(TRD_T, 1)
 trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const int* __restrict__ skip, int trace, int slp) {
   if (skip && *skip) return;
@@ -142,6 +157,8 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
   double* wpv = vsb + 2 * (size_t)n;   // w of the pending update
   double* ps = wpv + n;
   double* cur = ps + n;                // the replica of row j + 1
+  double* psb = cur + n;               // CL: 2 x n, p by step parity (written by every CTA)
+  double* nxt = psb + 2 * (size_t)n;   // CL: 2 x n, the next replica row by row parity
   __shared__ double kpart[TRD_W], sqpart[TRD_W], s1part[TRD_W], s2part[TRD_W], s_bs[2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (NQ == 0)
@@ -179,6 +196,10 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     }
   }
   __syncthreads();
+  if constexpr (CL) {
+    for (int k = tid; k < n; k += TRD_T) nxt[n + k] = B[ldb + k];  // row 1 for step 0
+    trd_cluster_sync();  // every CTA is running before the first remote store
+  }
   const int my_i = g + wid * G;  // the row this warp owns (if < n and wid < R)
   const bool has_row = wid < R && my_i < n;
   double* my_row = rows + (size_t)wid * n;
@@ -195,6 +216,10 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     const uint32_t tag = (uint32_t)j + 1u;
     const double* vc = vsb + (size_t)(j & 1) * n;         // v_j
     const double* vp = vsb + (size_t)((j + 1) & 1) * n;   // v_{j-1} (pending)
+    if constexpr (CL) {
+      ps = psb + (size_t)(j & 1) * n;
+      cur = nxt + (size_t)(m1 & 1) * n;
+    }
 #ifdef TRD_TRACE
     const bool trs = tron && j == n / 2;
     if (trs) {
@@ -240,12 +265,18 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
-      if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
+      if constexpr (CL) {
+        if (lane < G) trd_dsm_st(ps + my_i, (uint32_t)lane, bet * raw);
+      } else {
+        if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
+      }
     }
-    // this CTA's sentinel (one 128-byte line per CTA): readers poll it
-    // instead of every p record, so each line has G pollers, not G x 8
-    __syncthreads();
-    if (tid == 0) ll_store(b.sent + ((size_t)(j & 1) * TRD_MAXG + g) * 8, 0.0, tag);
+    if constexpr (!CL) {
+      // this CTA's sentinel (one 128-byte line per CTA): readers poll it
+      // instead of every p record, so each line has G pollers, not G x 8
+      __syncthreads();
+      if (tid == 0) ll_store(b.sent + ((size_t)(j & 1) * TRD_MAXG + g) * 8, 0.0, tag);
+    }
 #ifdef TRD_TRACE
     if (trs) tr[1] = clock64();
 #endif
@@ -260,7 +291,12 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
           const int k = lane + 32 * q;
           if (k >= m1 && k < n) {
             rr[q] = fma(-vi, wpv[k], fma(-wi, vp[k], rr[q]));
-            if (pub) ll_store(pub + k, rr[q], tag);
+            if constexpr (CL) {
+              if (my_i == m1)
+                for (int c = 0; c < G; ++c) trd_dsm_st(cur + k, (uint32_t)c, rr[q]);
+            } else {
+              if (pub) ll_store(pub + k, rr[q], tag);
+            }
           }
         }
       }
@@ -280,7 +316,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         my_row[k] = x0;
         if (pub) ll_store(pub + k, x0, tag);
       }
-      if (pub) {
+      if (pub && !CL) {
         __syncwarp();
         if (lane == 0) ll_store(b.sent + ((size_t)2 * TRD_MAXG + (m1 & 1)) * 8, 0.0, tag);
       }
@@ -293,6 +329,10 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     //     The sentinels first (one poller per source line), then every record
     //     is read and its tag checked (a relaxed store may still be in
     //     flight: those are polled again)
+    if constexpr (CL) {
+      trd_cluster_sync();  // every CTA's p and the replica row are in place
+    }
+    if constexpr (!CL) {
     if (tid < G) {
       const uint4* sp = b.sent + ((size_t)(j & 1) * TRD_MAXG + tid) * 8;
       while (ll_ld(sp).y != tag) {
@@ -349,6 +389,12 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
       } else {
         for (int k = m1 + tid; k < n; k += TRD_T) cur[k] = B[ldb + k];
       }
+      q = warp_sum(q);
+      if (lane == 0) kpart[wid] = q;
+    }
+    } else {
+      double q = 0.0;
+      for (int k = m1 + tid; k < n; k += TRD_T) q = fma(ps[k], vc[k], q);
       q = warp_sum(q);
       if (lane == 0) kpart[wid] = q;
     }
@@ -459,6 +505,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
       b.dd[n - 1] = fma(-vi, wi, fma(-wi, vi, a));
     }
   }
+  if constexpr (CL) trd_cluster_sync();  // no CTA leaves while remote stores into it may be in flight
 }
 
 // Number of eigenvalues of T greater than x: sign changes of the Sturm
@@ -877,18 +924,20 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
   const int nq = (n + 31) / 32;
   const char* re = getenv("MLR_TRD_REGROWS");
   const bool regs = !(re && re[0] == '0') && nq <= 16;  // measured: spills above 16 (C5 at 40: 148 -> 198 ms)
-  const size_t smem = 8 * ((regs ? 0 : (size_t)R * n) + 5 * (size_t)n);
-  // the publication records carry step tags >= 1: clear them (and info)
-  MLR_CUDA(cudaMemsetAsync(b->pll, 0, 16 * 2 * (size_t)n, s));
-  MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
-  MLR_CUDA(cudaMemsetAsync(b->sll, 0, 16 * 2 * (size_t)TRD_MAXG, s));
-  MLR_CUDA(cudaMemsetAsync(b->sent, 0, 16 * 8 * (2 * (size_t)TRD_MAXG + 2), s));
+  // one thread-block cluster for small n (register rows, G <= 16 CTAs)
+  const char* ce = getenv("MLR_TRD_CLUSTER");
+  const bool cl = regs && nq <= 8 && G <= 16 && !(ce && ce[0] == '0');
+  const size_t smem = 8 * ((regs ? 0 : (size_t)R * n) + (cl ? 9 : 5) * (size_t)n);
   MLR_CUDA(cudaMemsetAsync(b->info, 0, 4 * 16, s));
-  void* kfn = (void*)trd_reduce_kernel<0>;
-  if (regs) {
-    if (nq <= 8) kfn = (void*)trd_reduce_kernel<8>;
-    else kfn = (void*)trd_reduce_kernel<16>;
+  if (!cl) {  // the publication records carry step tags >= 1: clear them
+    MLR_CUDA(cudaMemsetAsync(b->pll, 0, 16 * 2 * (size_t)n, s));
+    MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
+    MLR_CUDA(cudaMemsetAsync(b->sll, 0, 16 * 2 * (size_t)TRD_MAXG, s));
+    MLR_CUDA(cudaMemsetAsync(b->sent, 0, 16 * 8 * (2 * (size_t)TRD_MAXG + 2), s));
   }
+  void* kfn = (void*)trd_reduce_kernel<0, false>;
+  if (cl) kfn = (void*)trd_reduce_kernel<8, true>;
+  else if (regs) kfn = nq <= 8 ? (void*)trd_reduce_kernel<8, false> : (void*)trd_reduce_kernel<16, false>;
   MLR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
     const double* bp = Bm;
@@ -899,7 +948,24 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     static const int slp0 = getenv("MLR_TRD_SLEEP") ? atoi(getenv("MLR_TRD_SLEEP")) : 0;
     int slp = slp0;
     void* args[] = {(void*)&bp, &ld, &nn, &bb, (void*)&skip, &tr, &slp};
-    MLR_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(TRD_T), args, smem, s));
+    if (cl) {
+      if (G > 8) MLR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(TRD_T);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = G;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      MLR_CUDA(cudaLaunchKernelExC(&cfg, kfn, args));
+    } else {
+      MLR_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(TRD_T), args, smem, s));
+    }
   }
   const int wpb = 8;  // warps per bisection CTA
   MLR_CUDA(cudaFuncSetAttribute(trd_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 * n)));
