@@ -626,14 +626,19 @@ constexpr int TRD_VW = 6;
 
 __global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int n, const int* __restrict__ skip) {
   if (skip && *skip) return;
-  extern __shared__ double vsm[];  // TRD_VW x 3 n
+  extern __shared__ double vsm[];  // (blockDim / 32) x 4 n
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int k = b.info[0];
   const int c = blockIdx.x * (blockDim.x >> 5) + wid;
   if (c >= k) return;
-  double* __restrict__ dps = vsm + (size_t)wid * 3 * n;  // D+_i
-  double* __restrict__ rms = dps + n;                     // R-_i
-  double* __restrict__ zz = rms + n;
+  // lane 0 runs only the two Sturm recurrences (one FMA each on the chain,
+  // forward and backward interleaved) and stores the numerator and
+  // denominator of every pivot; the divisions, the twist search and the
+  // multipliers of the z products are then spread over the 32 lanes
+  double* __restrict__ nf = vsm + (size_t)wid * 4 * n;  // forward p_i, then D+_i
+  double* __restrict__ df = nf + n;                     // forward p_{i-1}, then the upward multipliers, then z
+  double* __restrict__ nb = df + n;                     // backward r_i, then R-_i
+  double* __restrict__ db = nb + n;                     // backward r_{i+1}, then the downward multipliers
   const double sc = b.scale[0];
   const double lam = b.lam[c] * sc;
   // (nearly) repeated eigenvalues: the twisted vectors of a cluster this
@@ -642,65 +647,99 @@ __global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int 
   const double* __restrict__ d = b.dd;
   const double* __restrict__ e = b.ee;
   const double piv = 0x1p-900, big = 0x1p+900;
+  auto clampd = [&](double x) { return fabs(x) < piv ? -piv : fmin(fmax(x, -big), big); };
   if (lane == 0) {
-    // forward: p_i = (d_i - lam) p_{i-1} - e_{i-1}^2 p_{i-2}
+    // p_i = (d_i - lam) p_{i-1} - e_{i-1}^2 p_{i-2} (D+_i = p_i / p_{i-1}) and
+    // r_i = (d_i - lam) r_{i+1} - e_i^2 r_{i+2}   (R-_i = r_i / r_{i+1})
     double pm = 1.0, pc = fma(__ldg(d), sc, -lam);
-    dps[0] = pc;
+    double rn = 1.0, rc = fma(__ldg(d + n - 1), sc, -lam);
+    nf[0] = pc;
+    df[0] = 1.0;
+    nb[n - 1] = rc;
+    db[n - 1] = 1.0;
 #pragma unroll 4
-    for (int i = 1; i < n; ++i) {
-      const double ei = __ldg(e + i - 1) * sc;
-      const double pn = fma(fma(__ldg(d + i), sc, -lam), pc, -(ei * ei) * pm);
-      dps[i] = trd_div(pn, pc);
+    for (int t = 1; t < n; ++t) {
+      const int i = t, ib = n - 1 - t;
+      const double ef = __ldg(e + i - 1) * sc, eb = __ldg(e + ib) * sc;
+      const double pn = fma(fma(__ldg(d + i), sc, -lam), pc, -(ef * ef) * pm);
+      const double rp = fma(fma(__ldg(d + ib), sc, -lam), rc, -(eb * eb) * rn);
+      nf[i] = pn;
+      df[i] = pc;
+      nb[ib] = rp;
+      db[ib] = rc;
       pm = pc;
       pc = pn;
-      if ((i & 7) == 0) trd_rescale_pair(pc, pm);
-    }
-    // backward: r_i = (d_i - lam) r_{i+1} - e_i^2 r_{i+2}; gamma on the fly
-    double rn = 1.0, rc = fma(__ldg(d + n - 1), sc, -lam);
-    rms[n - 1] = rc;
-    auto clampd = [&](double x) { return fabs(x) < piv ? -piv : fmin(fmax(x, -big), big); };
-    int r = n - 1;
-    double best = fabs(clampd(dps[n - 1]));
-#pragma unroll 4
-    for (int i = n - 2; i >= 0; --i) {
-      const double ei = __ldg(e + i) * sc;
-      const double di = fma(__ldg(d + i), sc, -lam);
-      const double rp = fma(di, rc, -(ei * ei) * rn);
-      const double rmi = trd_div(rp, rc);
-      rms[i] = rmi;
       rn = rc;
       rc = rp;
-      if ((i & 7) == 0) trd_rescale_pair(rc, rn);
-      const double gam = clampd(dps[i]) + clampd(rmi) - di;
-      if (fabs(gam) < best) {
-        best = fabs(gam);
-        r = i;
+      if ((t & 7) == 0) {
+        trd_rescale_pair(pc, pm);
+        trd_rescale_pair(rc, rn);
       }
     }
-    // z
-    double ss = 1.0, zi = 1.0;
-    zz[r] = 1.0;
-#pragma unroll 4
-    for (int i = r - 1; i >= 0; --i) {
-      zi = -trd_div(__ldg(e + i) * sc, clampd(dps[i])) * zi;
-      zz[i] = zi;
-      ss = fma(zi, zi, ss);
-    }
-    zi = 1.0;
-#pragma unroll 4
-    for (int i = r; i < n - 1; ++i) {
-      zi = -trd_div(__ldg(e + i) * sc, clampd(rms[i + 1])) * zi;
-      zz[i + 1] = zi;
-      ss = fma(zi, zi, ss);
-    }
-    const double inv = 1.0 / sqrt(ss);
-    if (!(isfinite(inv) && inv > 0.0)) atomicExch(b.info + 1, 1);
-    rms[0] = inv;  // hand the norm to the warp
   }
   __syncwarp();
-  const double inv = rms[0];
+  // pivots and the twist index r = argmin |gamma_i|, gamma_i = D+_i + R-_i - (d_i - lam)
+  double best = 1e300;
+  int r = -1;
+  for (int i = lane; i < n; i += 32) {
+    const double dp = clampd(nf[i] / df[i]), rm = clampd(nb[i] / db[i]);
+    nf[i] = dp;
+    nb[i] = rm;
+    const double gam = fabs(dp + rm - fma(__ldg(d + i), sc, -lam));
+    if (gam < best || (gam == best && i > r)) {  // ties: the largest i (the serial scan's choice)
+      best = gam;
+      r = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int orr = __shfl_xor_sync(0xffffffffu, r, o);
+    if (ob < best || (ob == best && orr > r)) {
+      best = ob;
+      r = orr;
+    }
+  }
+  __syncwarp();
+  // multipliers: upward z_i = -(e_i / D+_i) z_{i+1} (i < r), downward
+  // z_{i+1} = -(e_i / R-_{i+1}) z_i (i >= r)
+  for (int i = lane; i < n - 1; i += 32) {
+    const double ei = __ldg(e + i) * sc;
+    if (i < r) df[i] = -ei / nf[i];
+    else db[i] = -ei / nb[i + 1];
+  }
+  __syncwarp();
+  double* __restrict__ zz = nb;  // R- no longer needed
+  if (lane == 0) {
+    // both products in one loop (two independent multiply chains)
+    double zu = 1.0, zd = 1.0, ss = 1.0;
+    const int nu = r, nd = n - 1 - r, nt = max(nu, nd);
+    double zr = 1.0;
+#pragma unroll 4
+    for (int t = 0; t < nt; ++t) {
+      if (t < nu) {
+        const int i = r - 1 - t;
+        zu *= df[i];
+        df[i] = zu;  // z_i (upward part stored in place)
+        ss = fma(zu, zu, ss);
+      }
+      if (t < nd) {
+        const int i = r + t;
+        zd *= db[i];
+        zz[i + 1] = zd;  // z_{i+1} (into the R- buffer)
+        ss = fma(zd, zd, ss);
+      }
+    }
+    df[r] = zr;
+    const double inv = 1.0 / sqrt(ss);
+    if (!(isfinite(inv) && inv > 0.0)) atomicExch(b.info + 1, 1);
+    nf[0] = inv;  // hand the norm to the warp (D+ is no longer read)
+  }
+  __syncwarp();
+  const double inv = nf[0];
   double* __restrict__ out = b.z + (size_t)c * n;
-  for (int i = lane; i < n; i += 32) out[i] = zz[i] * inv;
+  // z_i: i <= r from df (upward part and z_r = 1), i > r from the R- buffer
+  for (int i = lane; i < n; i += 32) out[i] = (i <= r ? df[i] : zz[i]) * inv;
 }
 
 // V = Q Z = H_0 H_1 ... H_{n-3} Z, one warp per column c < k with the column
@@ -911,7 +950,7 @@ bool trd_supported(int n) {
   if (G > TRD_MAXG) return false;
   const int R = (n + G - 1) / G;
   const size_t smem = 8 * ((size_t)R * n + 5 * (size_t)n);
-  return smem <= 224 * 1024 && 8 * 12 * (size_t)(n + 1) <= 200 * 1024 && 24 * (size_t)n <= 200 * 1024;
+  return smem <= 224 * 1024 && 8 * 12 * (size_t)(n + 1) <= 200 * 1024 && 32 * (size_t)n <= 200 * 1024;
 }
 
 // Eigenpairs of B (n x n in the leading block of an np x np buffer) above
@@ -972,8 +1011,8 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
   trd_bisect_kernel<<<(n + wpb - 1) / wpb, 32 * wpb, 16 * (size_t)n, s>>>(*b, n, tau, skip);
   MLR_LAUNCH_CHECK("trd_bisect_kernel");
   {
-    const int vw = (int)std::max<size_t>(1, std::min<size_t>(TRD_VW, (200 * 1024) / (24 * (size_t)n)));
-    const size_t vsm = 24 * (size_t)n * vw;
+    const int vw = (int)std::max<size_t>(1, std::min<size_t>(TRD_VW, (200 * 1024) / (32 * (size_t)n)));
+    const size_t vsm = 32 * (size_t)n * vw;
     MLR_CUDA(cudaFuncSetAttribute(trd_vectors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm));
     trd_vectors_kernel<<<(n + vw - 1) / vw, 32 * vw, vsm, s>>>(*b, n, skip);
   }
