@@ -822,14 +822,13 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
       double acc[CPW];
 #pragma unroll
       for (int u = 0; u < CPW; ++u) acc[u] = 0.0;
+      double hr[NQ];  // the reflector's entries, read from shared memory once for both passes
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int i = lane + 32 * q;
-        if (q >= q0 && i > j && i < n) {
-          const double hv = h[i];
+        hr[q] = (q >= q0 && i > j && i < n) ? h[i] : 0.0;
 #pragma unroll
-          for (int u = 0; u < CPW; ++u) acc[u] = fma(hv, z[u][q], acc[u]);
-        }
+        for (int u = 0; u < CPW; ++u) acc[u] = fma(hr[q], z[u][q], acc[u]);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
@@ -838,14 +837,9 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
 #pragma unroll
       for (int u = 0; u < CPW; ++u) acc[u] *= bet;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int i = lane + 32 * q;
-        if (q >= q0 && i > j && i < n) {
-          const double hv = h[i];
+      for (int q = 0; q < NQ; ++q)
 #pragma unroll
-          for (int u = 0; u < CPW; ++u) z[u][q] = fma(-acc[u], hv, z[u][q]);
-        }
-      }
+        for (int u = 0; u < CPW; ++u) z[u][q] = fma(-acc[u], hr[q], z[u][q]);
     }
     __syncthreads();  // stage st consumed by every warp
     if (threadIdx.x == 0 && ch + TRD_BST < nch) issue(ch + TRD_BST);
