@@ -42,6 +42,6 @@ def block_lanczos(b, tol=1e-9, maxp=200, seed=0):
         Qprev, Bprev, Q = Q, Bj, Qn
         Qs.append(Q)
     return maxp, np.sqrt(th)
-for b in [1, 2, 4, 8, 16]:
+for b in ([int(x) for x in sys.argv[2:]] or [1, 2, 4, 8, 16]):
     p, s = block_lanczos(b)
     print(name, 'block', b, 'passes', p, 'sigma1', s, 'err', (abs(s - s_true) / s_true) if s_true else None, flush=True)
