@@ -367,7 +367,9 @@ def roofline_entries(name, cfg, phases, sweeps, m_local, world, peaks, traffic, 
             # (profiles/peaks_b200.json, tools/ubench_ll.cu) bounds the step from below
             step = out["jacobi"]["avg_us"] / max(1, nh - 2)
             rt = (peaks.get("ll_record_roundtrip_cycles") or {}).get("32_pollers")
-            out["jacobi"]["us_per_column_step"] = step
+            # the phase also holds the rank-0 certificates, bisection, vectors and back-transform:
+            # an upper bound on the reduction's own step (ncu: 5.6 ms / 1248 steps = 4.5 us at C5)
+            out["jacobi"]["phase_us_per_column_step"] = step
             if rt:
                 floor = rt / 1965.0  # us at the max SM clock
                 out["jacobi"]["latency_floor_us_per_step"] = floor
