@@ -27,7 +27,11 @@
  *   mlr_eigh_psd          the SVD inside svd_full (linalg.py:86-99) as used by
  *                         the SVT step (pcp.py:257-267), via Jacobi on M^T M
  *   mlr_pcp_*             pcp.ml_ialm_solve loop (pcp.py:213-309) incl. the
- *                         sigma_1 / dual init (pcp.py:95-115)
+ *                         sigma_1 / dual init (pcp.py:95-115); the coarse SVT
+ *                         (pcp.py:257-267) inside mlr_pcp_svt runs a
+ *                         tridiagonal eigensolver on M^T M (Householder
+ *                         reduction, Sturm bisection, twisted-factorisation
+ *                         vectors) with the block Jacobi as fallback
  *   mlr_cpcp_*            cpcp.ml_fwt_solve / _run_fwt (cpcp.py:326-515)
  */
 #ifndef MLR_B200_H
@@ -142,7 +146,8 @@ int mlr_pcp_svt(void* plan, const double* red, void* stream);
 int mlr_pcp_update(void* plan, const void* D, int64_t ldd, const void* Y_in, void* Y_out, int64_t ldy, void* stream);
 int mlr_pcp_outputs(void* plan, const void* D, int64_t ldd, const void* Y_prev, int64_t ldy, void* L, void* S,
                     int64_t ldo, void* stream);
-/* out16: k, done, status, rank, mu, mu_final, mu_last, nuclear, sigma1, d_norm, jac_sweeps, tau, scale, lam, 0, 0 */
+/* out16: k, done, status, rank, mu, mu_final, mu_last, nuclear, sigma1, d_norm, jac_sweeps, tau, scale, lam, 0, 0
+ * (jac_sweeps: Jacobi sweeps of the latest eigensolve, 0 when none ran, -1 when the tridiagonal solver ran) */
 int mlr_pcp_state(void* plan, double* out16, void* stream);
 /* Pipelined polling: mlr_pcp_snapshot enqueues an asynchronous copy of the
  * plan's device state (solver + Lanczos) into `host` (pinned, at least
@@ -159,7 +164,7 @@ int mlr_pcp_history(void* plan, int count, double* out, void* stream); /* count 
  * of each iteration take part and sv adapts (pcp.py:160-165), capped at cap.
  * Call before mlr_pcp_start; sv0 = 0 restores the full SVT. */
 int mlr_pcp_set_truncation(void* plan, int sv0, int cap);
-/* Per-phase CUDA-event timing: phases gram, pre (B, X=BV), jacobi, post
+/* Per-phase CUDA-event timing: phases gram, pre (B, X=BV), jacobi (the coarse eigensolve: tridiagonal or Jacobi, incl. the rank-0 certificate), post
  * (weights, P, W~), recon (Z = A W~), update (fused fine pass), finalize,
  * lanczos (sigma_1 estimate).  mlr_pcp_timing synchronises, returns total ms
  * and launch counts per phase (8 entries each) and resets the accumulators. */
