@@ -46,7 +46,7 @@ struct TrdBuf {
   double* hv;     // n x ldh (ldh = n rounded up to even): row j = Householder vector v_j (entries j+1..n-1)
   double* z;      // n x n: eigenvectors of T, vector c at z[c * n + i]
   double *beta, *dd, *ee, *lam;  // n each: reflector scalars, diag / off-diag of T, eigenvalues (descending)
-  uint4 *pll, *rowll, *sll;      // flag-carrying publication buffers (2 x n, 2 x n, 2 x 256 records)
+  uint4 *pll, *rowll;            // flag-carrying publication buffers (2 x n each): p by step parity, rows by row parity
   uint4* sent;                   // per-CTA and row sentinels, one 128-byte line each
   double* scale;                 // power-of-two scale of T used by the bisection / vectors
   int* info;                     // [0] = k (eigenvalues above tau^2), [1] = failure, [2] = V columns in use

@@ -74,16 +74,6 @@ __device__ __forceinline__ uint4 ll_ld(const uint4* p) {
 __device__ __forceinline__ double ll_val(uint4 v) {
   return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
 }
-__device__ __forceinline__ double ll_load(const uint4* p, uint32_t tag) {
-  uint32_t a, f1, c, f2;
-  do {
-    asm volatile("ld.relaxed.gpu.global.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(a), "=r"(f1), "=r"(c), "=r"(f2)
-                 : "l"(p)
-                 : "memory");
-  } while (f1 != tag || f2 != tag);
-  return __longlong_as_double((long long)(((unsigned long long)c << 32) | a));
-}
 
 // a / b to ~1 ulp: approximate reciprocal and two Newton steps (normal
 // inputs of moderate exponent: T is pre-scaled to |T| ~ 1)
@@ -140,7 +130,7 @@ __device__ __forceinline__ void trd_cluster_sync() {
 // flag-carrying records and sentinels in L2.
 template <int NQ, bool CL>
 __global__ void __launch_bounds__(TRD_T, 1)
-trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const int* __restrict__ skip, int trace, int slp) {
+trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const int* __restrict__ skip, int trace) {
   if (skip && *skip) return;
 #ifdef TRD_TRACE
   long long tr[8];
@@ -358,10 +348,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         for (int u = 0; u < TRD_LL; ++u) {
           const int k = m1 + tid + u * TRD_T;
           if (k < n) {
-            while (pr[u].y != tag || pr[u].w != tag) {
-              if (slp) __nanosleep(slp);
-              pr[u] = ll_ld(pl + k);
-            }
+            while (pr[u].y != tag || pr[u].w != tag) pr[u] = ll_ld(pl + k);
             const double p = ll_val(pr[u]);
             ps[k] = p;
             q = fma(p, vc[k], q);
@@ -379,10 +366,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         for (int u = 0; u < TRD_LL; ++u) {
           const int k = m1 + tid + u * TRD_T;
           if (k < n) {
-            while (cr[u].y != tag || cr[u].w != tag) {
-              if (slp) __nanosleep(slp);
-              cr[u] = ll_ld(rl + k);
-            }
+            while (cr[u].y != tag || cr[u].w != tag) cr[u] = ll_ld(rl + k);
             cur[k] = ll_val(cr[u]);
           }
         }
@@ -892,7 +876,7 @@ int trd_max_n() { return TRD_LL * TRD_T; }
 
 size_t trd_bytes(int n) {
   const size_t nn = (size_t)n * n;
-  // hv (n x ldh), z: 2 n^2 + n; beta, dd, ee, lam: 4 n; pll, rowll: 4 n records; sll; scale, info
+  // hv (n x ldh), z: 2 n^2 + n; beta, dd, ee, lam: 4 n; pll, rowll: 4 n records; sentinels; scale, info
   return 8 * (2 * nn + 5 * (size_t)n) + 16 * (4 * (size_t)n + 2 * TRD_MAXG) + 128 * (2 * TRD_MAXG + 2) + 8 * 4 +
          4 * 16 + 14 * 256;
 }
@@ -914,7 +898,6 @@ void trd_carve(TrdBuf* b, char* base, int n) {
   b->lam = (double*)take(8 * (size_t)n);
   b->pll = (uint4*)take(16 * 2 * (size_t)n);
   b->rowll = (uint4*)take(16 * 2 * (size_t)n);
-  b->sll = (uint4*)take(16 * 2 * (size_t)TRD_MAXG);
   b->sent = (uint4*)take(16 * 8 * (2 * (size_t)TRD_MAXG + 2));
   b->scale = (double*)take(8 * 4);
   b->info = (int*)take(4 * 16);
@@ -965,7 +948,6 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
   if (!cl) {  // the publication records carry step tags >= 1: clear them
     MLR_CUDA(cudaMemsetAsync(b->pll, 0, 16 * 2 * (size_t)n, s));
     MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
-    MLR_CUDA(cudaMemsetAsync(b->sll, 0, 16 * 2 * (size_t)TRD_MAXG, s));
     MLR_CUDA(cudaMemsetAsync(b->sent, 0, 16 * 8 * (2 * (size_t)TRD_MAXG + 2), s));
   }
   void* kfn = (void*)trd_reduce_kernel<0, false>;
@@ -978,9 +960,7 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     TrdBuf bb = *b;
     static const int trace = getenv("MLR_TRD_TRACE") ? 1 : 0;
     int tr = trace;
-    static const int slp0 = getenv("MLR_TRD_SLEEP") ? atoi(getenv("MLR_TRD_SLEEP")) : 0;
-    int slp = slp0;
-    void* args[] = {(void*)&bp, &ld, &nn, &bb, (void*)&skip, &tr, &slp};
+    void* args[] = {(void*)&bp, &ld, &nn, &bb, (void*)&skip, &tr};
     if (cl) {
       if (G > 8) MLR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       cudaLaunchConfig_t cfg = {};
