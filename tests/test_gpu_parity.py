@@ -498,3 +498,17 @@ def test_tridiagonal_failure_falls_back_to_jacobi():
     env = dict(os.environ, MLR_EIG="trd", MLR_TRD_FORCE_FALLBACK="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("n,levels", [(140, 3), (140, 5), (140, 9), (140, 35), (140, 70), (130, 65), (264, 33)])
+def test_tridiagonal_eigensolver_small_and_odd_coarse_widths(n, levels, monkeypatch):
+    """The tridiagonal coarse eigensolver at tiny and odd n_H (one-CTA cluster,
+    partial warps, n_H not a multiple of 32 or of the 64 padding) against the
+    oracle's SVD-based SVT (pcp.py:257-262)."""
+    monkeypatch.setenv("MLR_EIG", "trd")
+    d, _ = O.gaussian_rpca(160, n, 3, 0.10, 9)
+    ref = O.ml_ialm(d, levels=levels, tol=1e-7)
+    st = pkg.ml_ialm_solve(d, pkg.PcpOptions(levels=levels, tol_feasibility=1e-7))
+    assert st.iter == ref.iter
+    assert [h.rank_l for h in st.history] == [h.rank_l for h in ref.history]
+    assert relf(st.l, ref.l) <= 1e-10 and relf(st.s, ref.s) <= 1e-10
