@@ -368,6 +368,29 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// FP32 -> FP64 on the integer pipe: sign | (e8 + 896) << 20 | m23 >> 3 in the
+// high word, m23 << 29 in the low word (exact for every normal float).  The
+// F2F.F64.F32 conversion runs on the XU pipe at 16 lanes/clk/SM and is the
+// busiest pipe of this kernel (ncu: XU 44% of peak, the top pipe, with the
+// warps stalled on its results); 4 integer operations convert at the same
+// rate on the ALU pipe, so alternating the two doubles the conversion rate.
+// Zeros and denormals map to +-2^-127 (1 + m / 2^23) (absolute error below
+// 1.2e-38: no effect on an FP64 sum of |x q| terms); the input was checked
+// to be finite (input_stats_kernel) before the Lanczos runs.
+__device__ __forceinline__ double lz_f2d_int(float x) {
+  const uint32_t f = __float_as_uint(x);
+  const uint32_t hi = (((uint32_t)((int32_t)f >> 3)) & 0x8FFFFFFFu) + 0x38000000u;
+  return __hiloint2double((int)hi, (int)(f << 29));
+}
+template <int CV>
+__device__ __forceinline__ void lz_cvt4(const float4 x, double (&d)[4]) {
+  d[0] = CV == 2 ? lz_f2d_int(x.x) : (double)x.x;
+  d[1] = CV >= 1 ? lz_f2d_int(x.y) : (double)x.y;
+  d[2] = CV == 2 ? lz_f2d_int(x.z) : (double)x.z;
+  d[3] = CV >= 1 ? lz_f2d_int(x.w) : (double)x.w;
+}
+
+template <int CV>
 __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev* __restrict__ lz,
                                                                 const float* __restrict__ D, int64_t ldd,
                                                                 int64_t m, int n, int seg, int stages,
@@ -433,11 +456,12 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
           for (int g = 0; g < LZL_NG; ++g) {
             const int k = tid + g * LZL_T;
             if (k < ng4) {
-              const float4 x = row[k];
-              a0 = fma((double)x.x, qv[g][0], a0);
-              a1 = fma((double)x.y, qv[g][1], a1);
-              a0 = fma((double)x.z, qv[g][2], a0);
-              a1 = fma((double)x.w, qv[g][3], a1);
+              double xd[4];
+              lz_cvt4<CV>(row[k], xd);
+              a0 = fma(xd[0], qv[g][0], a0);
+              a1 = fma(xd[1], qv[g][1], a1);
+              a0 = fma(xd[2], qv[g][2], a0);
+              a1 = fma(xd[3], qv[g][3], a1);
             }
           }
           pr = warp_sum(a0 + a1);
@@ -491,11 +515,10 @@ __global__ void __launch_bounds__(LZL_T, 1) lz_dtdq_long_kernel(const LanczosDev
           for (int g = 0; g < LZL_NG; ++g) {
             const int k = tid + g * LZL_T;
             if (k < ng4) {
-              const float4 x = row[k];
-              acc[g][0] = fma((double)x.x, t[r], acc[g][0]);
-              acc[g][1] = fma((double)x.y, t[r], acc[g][1]);
-              acc[g][2] = fma((double)x.z, t[r], acc[g][2]);
-              acc[g][3] = fma((double)x.w, t[r], acc[g][3]);
+              double xd[4];
+              lz_cvt4<CV>(row[k], xd);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[g][e] = fma(xd[e], t[r], acc[g][e]);
             }
           }
         }
@@ -1313,9 +1336,14 @@ int pcp_lanczos_matvec(PcpPlan* p, const void* D, int64_t ldd, double* wpart_out
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MLR_CUDA(cudaFuncSetAttribute(lz_dtdq_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MLR_CUDA(cudaLaunchKernelEx(&cfg, lz_dtdq_long_kernel, (const LanczosDev*)p->lz, (const float*)D, ldd, m, n, seg,
-                                stages, (const double*)p->lzQ, p->lzW));
+    static const int cv = [] {
+      const char* e = getenv("MLR_LZ_CVT");  // 0: F2F only, 1: F2F / integer alternating (default), 2: integer only
+      return e ? atoi(e) : 1;
+    }();
+    auto kern = cv == 0 ? lz_dtdq_long_kernel<0> : cv == 2 ? lz_dtdq_long_kernel<2> : lz_dtdq_long_kernel<1>;
+    MLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLR_CUDA(cudaLaunchKernelEx(&cfg, kern, (const LanczosDev*)p->lz, (const float*)D, ldd, m, n, seg, stages,
+                                (const double*)p->lzQ, p->lzW));
     MLR_LAUNCH_CHECK("lz_dtdq_long_kernel");
     const int rc = sum_slices(p->lzW, n, n, ncl, wpart_out, st);
     p->timer.end(kPhLanczos, st);
