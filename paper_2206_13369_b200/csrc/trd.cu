@@ -128,7 +128,7 @@ __device__ __forceinline__ void trd_cluster_sync() {
 // replica row are written straight into every CTA's shared memory
 // (st.shared::cluster) and one cluster barrier per step replaces the
 // flag-carrying records and sentinels in L2.
-template <int NQ, bool CL>
+template <int NQ, bool CL, bool COLX>
 __global__ void __launch_bounds__(TRD_T, 1)
 trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const int* __restrict__ skip, int trace) {
   if (skip && *skip) return;
@@ -255,10 +255,33 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
+      // B is symmetric: the replica of row j + 1 that every CTA needs for the
+      // next reflector is column j + 1, and this warp holds its entry
+      // A[i][j + 1].  It travels with p_i (after the pending update of step
+      // j - 1 on that one entry), so no owner has to finish its row update
+      // and publish 1 row before the exchange can complete.
+      double cm = 0.0;
+      if (COLX && j > 0) {
+        const double vi = vp[my_i], wi = wpv[my_i];
+        if constexpr (NQ > 0) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            if (lane + 32 * q == m1) cm = fma(-vi, wpv[m1], fma(-wi, vp[m1], rr[q]));
+          cm = __shfl_sync(0xffffffffu, cm, m1 & 31);
+        } else {
+          cm = fma(-vi, wpv[m1], fma(-wi, vp[m1], my_row[m1]));
+        }
+      }
       if constexpr (CL) {
-        if (lane < G) trd_dsm_st(ps + my_i, (uint32_t)lane, bet * raw);
+        if (lane < G) {
+          trd_dsm_st(ps + my_i, (uint32_t)lane, bet * raw);
+          if (COLX && j > 0) trd_dsm_st(cur + my_i, (uint32_t)lane, cm);
+        }
       } else {
-        if (lane == 0) ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
+        if (lane == 0) {
+          ll_store(b.pll + (size_t)(j & 1) * n + my_i, bet * raw, tag);
+          if (COLX && j > 0) ll_store(b.rowll + (size_t)(m1 & 1) * n + my_i, cm, tag);
+        }
       }
     }
     if constexpr (!CL) {
@@ -274,7 +297,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     //     the owner of row j + 1 publishes it (through step j - 1)
     if (j > 0 && has_row && my_i >= m1) {
       const double vi = vp[my_i], wi = wpv[my_i];
-      uint4* pub = my_i == m1 ? b.rowll + (size_t)(m1 & 1) * n : nullptr;
+      uint4* pub = (!COLX && my_i == m1) ? b.rowll + (size_t)(m1 & 1) * n : nullptr;
       if constexpr (NQ > 0) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
@@ -282,7 +305,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
           if (k >= m1 && k < n) {
             rr[q] = fma(-vi, wpv[k], fma(-wi, vp[k], rr[q]));
             if constexpr (CL) {
-              if (my_i == m1)
+              if (!COLX && my_i == m1)
                 for (int c = 0; c < G; ++c) trd_dsm_st(cur + k, (uint32_t)c, rr[q]);
             } else {
               if (pub) ll_store(pub + k, rr[q], tag);
@@ -327,7 +350,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
       const uint4* sp = b.sent + ((size_t)(j & 1) * TRD_MAXG + tid) * 8;
       while (ll_ld(sp).y != tag) {
       }
-    } else if (tid == TRD_T - 1 && j > 0) {
+    } else if (!COLX && tid == TRD_T - 1 && j > 0) {
       const uint4* sp = b.sent + ((size_t)2 * TRD_MAXG + (m1 & 1)) * 8;
       while (ll_ld(sp).y != tag) {
       }
@@ -950,9 +973,13 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
     MLR_CUDA(cudaMemsetAsync(b->rowll, 0, 16 * 2 * (size_t)n, s));
     MLR_CUDA(cudaMemsetAsync(b->sent, 0, 16 * 8 * (2 * (size_t)TRD_MAXG + 2), s));
   }
-  void* kfn = (void*)trd_reduce_kernel<0, false>;
-  if (cl) kfn = (void*)trd_reduce_kernel<8, true>;
-  else if (regs) kfn = nq <= 8 ? (void*)trd_reduce_kernel<8, false> : (void*)trd_reduce_kernel<16, false>;
+  // MLR_TRD_COLX=0: the owner of row j + 1 publishes it after its row update (the round-4 exchange)
+  static const bool colx = !(getenv("MLR_TRD_COLX") && getenv("MLR_TRD_COLX")[0] == '0');
+  void* kfn = colx ? (void*)trd_reduce_kernel<0, false, true> : (void*)trd_reduce_kernel<0, false, false>;
+  if (cl) kfn = colx ? (void*)trd_reduce_kernel<8, true, true> : (void*)trd_reduce_kernel<8, true, false>;
+  else if (regs)
+    kfn = nq <= 8 ? (colx ? (void*)trd_reduce_kernel<8, false, true> : (void*)trd_reduce_kernel<8, false, false>)
+                  : (colx ? (void*)trd_reduce_kernel<16, false, true> : (void*)trd_reduce_kernel<16, false, false>);
   MLR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
     const double* bp = Bm;
