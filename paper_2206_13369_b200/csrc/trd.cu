@@ -238,12 +238,24 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         a0 += a2;
         a1 += a3;
       } else {
+        // four independent load / FMA chains in flight per lane
+        double a2 = 0.0, a3 = 0.0;
         int k = m1 + lane;
-        for (; k + 32 < n; k += 64) {
+        for (; k + 96 < n; k += 128) {
           a0 = fma(my_row[k], vc[k], a0);
           a1 = fma(my_row[k + 32], vc[k + 32], a1);
+          a2 = fma(my_row[k + 64], vc[k + 64], a2);
+          a3 = fma(my_row[k + 96], vc[k + 96], a3);
         }
-        if (k < n) a0 = fma(my_row[k], vc[k], a0);
+        if (k + 32 < n) {
+          a0 = fma(my_row[k], vc[k], a0);
+          a1 = fma(my_row[k + 32], vc[k + 32], a1);
+          k += 64;
+        }
+        if (k < n) a2 = fma(my_row[k], vc[k], a2);
+        if (k + 32 < n) a3 = fma(my_row[k + 32], vc[k + 32], a3);
+        a0 += a2;
+        a1 += a3;
       }
       // the row dot and the two correction dots reduced together (three
       // independent shuffle chains in flight)
@@ -361,14 +373,20 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
       const uint4* rl = b.rowll + (size_t)(m1 & 1) * n;
       double q = 0.0;
       {
-        uint4 pr[TRD_LL];
+        // the p and the replica records are fetched together: one L2 round
+        // trip on the step's critical path instead of two
+        constexpr int LLU = NQ > 0 ? 1 : TRD_LL;  // register rows: n <= TRD_T
+        uint4 pr[LLU], cr[LLU];
 #pragma unroll
-        for (int u = 0; u < TRD_LL; ++u) {
+        for (int u = 0; u < LLU; ++u) {
           const int k = m1 + tid + u * TRD_T;
-          if (k < n) pr[u] = ll_ld(pl + k);
+          if (k < n) {
+            pr[u] = ll_ld(pl + k);
+            if (j > 0) cr[u] = ll_ld(rl + k);
+          }
         }
 #pragma unroll
-        for (int u = 0; u < TRD_LL; ++u) {
+        for (int u = 0; u < LLU; ++u) {
           const int k = m1 + tid + u * TRD_T;
           if (k < n) {
             while (pr[u].y != tag || pr[u].w != tag) pr[u] = ll_ld(pl + k);
@@ -377,24 +395,18 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
             q = fma(p, vc[k], q);
           }
         }
-      }
-      if (j > 0) {
-        uint4 cr[TRD_LL];
+        if (j > 0) {
 #pragma unroll
-        for (int u = 0; u < TRD_LL; ++u) {
-          const int k = m1 + tid + u * TRD_T;
-          if (k < n) cr[u] = ll_ld(rl + k);
-        }
-#pragma unroll
-        for (int u = 0; u < TRD_LL; ++u) {
-          const int k = m1 + tid + u * TRD_T;
-          if (k < n) {
-            while (cr[u].y != tag || cr[u].w != tag) cr[u] = ll_ld(rl + k);
-            cur[k] = ll_val(cr[u]);
+          for (int u = 0; u < LLU; ++u) {
+            const int k = m1 + tid + u * TRD_T;
+            if (k < n) {
+              while (cr[u].y != tag || cr[u].w != tag) cr[u] = ll_ld(rl + k);
+              cur[k] = ll_val(cr[u]);
+            }
           }
+        } else {
+          for (int k = m1 + tid; k < n; k += TRD_T) cur[k] = B[ldb + k];
         }
-      } else {
-        for (int k = m1 + tid; k < n; k += TRD_T) cur[k] = B[ldb + k];
       }
       q = warp_sum(q);
       if (lane == 0) kpart[wid] = q;
