@@ -212,6 +212,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     }
 #ifdef TRD_TRACE
     const bool trs = tron && j == n / 2;
+    const long long tr0s = clock64();
     if (trs) {
       tr[0] = clock64();
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[7]));
@@ -219,6 +220,11 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
 #endif
     // (1) p_i = beta (A_i . v - v'_i s1 - w'_i s2) for the local rows i >= j + 1
     if (has_row && my_i >= m1) {
+#ifdef TRD_TRACE
+      long long w0 = 0, w1 = 0, w2 = 0;
+      const bool wtr = trace && j == n / 2 && lane == 0 && wid == R - 1 && g < 4;
+      if (wtr) w0 = clock64();
+#endif
       double s1 = (j > 0 && lane < TRD_W) ? s1part[lane] : 0.0;
       double s2 = (j > 0 && lane < TRD_W) ? s2part[lane] : 0.0;
       double a0 = 0.0, a1 = 0.0;
@@ -260,6 +266,9 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
       // the row dot and the two correction dots reduced together (three
       // independent shuffle chains in flight)
       double raw = a0 + a1;
+#ifdef TRD_TRACE
+      if (wtr) w1 = clock64();
+#endif
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         raw += __shfl_xor_sync(0xffffffffu, raw, o);
@@ -267,6 +276,9 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if (j > 0) raw = fma(-vp[my_i], s1, fma(-wpv[my_i], s2, raw));
+#ifdef TRD_TRACE
+      if (wtr) w2 = clock64();
+#endif
       // B is symmetric: the replica of row j + 1 that every CTA needs for the
       // next reflector is column j + 1, and this warp holds its entry
       // A[i][j + 1].  It travels with p_i (after the pending update of step
@@ -295,6 +307,9 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
           if (COLX && j > 0) ll_store(b.rowll + (size_t)(m1 & 1) * n + my_i, cm, tag);
         }
       }
+#ifdef TRD_TRACE
+      if (wtr) printf("trdw g=%d: since step start %lld loop %lld shfl %lld publish %lld\n", g, w0 - tr0s, w1 - w0, w2 - w1, clock64() - w2);
+#endif
     }
     if constexpr (!CL) {
       // this CTA's sentinel (one 128-byte line per CTA): readers poll it
