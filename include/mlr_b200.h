@@ -261,6 +261,14 @@ int mlr_frames_to_matrix(const uint8_t* frames, int count, int height, int width
 int mlr_matrix_to_frames(const void* x, int64_t ldx, int f32, int count, int height, int width, uint8_t* frames,
                          void* stream);
 
+/* ------------------------------------------------------------ observation mask
+ * The reference's ObservationMask (cpcp.py:23-53) holds a boolean m x n array; the
+ * ML-CPCP passes read it bit-packed (see mlr_cpcp_start).  observed: m x n bytes in
+ * device memory (non-zero = observed, row stride ld_observed bytes); bits: m x ldm
+ * uint32 words, bit j & 31 of word j >> 5, words past ceil(n / 32) zeroed. */
+int mlr_mask_pack(const uint8_t* observed, int64_t ld_observed, int64_t m, int64_t n, uint32_t* bits, int64_t ldm,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,7 @@ _SIGS = {
     "mlr_pcp_delta": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "mlr_frames_to_matrix": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int64, c_void_p]),
     "mlr_matrix_to_frames": (c_int, [c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
+    "mlr_mask_pack": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p]),
     "mlr_cpcp_rank_shadow": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "mlr_cpcp_atom_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "mlr_cpcp_atom_dense": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),

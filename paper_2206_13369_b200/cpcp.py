@@ -15,6 +15,7 @@ import os
 import numpy as np
 import torch
 
+from . import _lib
 from .api_types import CpcpOptions, CpcpState, IterationRecord, ObservationMask
 from .backend import CudaCpcp, CudaSpectrum, chain_cholesky
 from .chain import build_chain, resolve_coarse_width
@@ -150,15 +151,37 @@ def _state_from(L, S, st, hist, objs, kind, atoms=None):
 
 
 def _mask_bits(mask, shape, device, rows=None):
+    """The observation pattern as bit-packed rows on ``device`` (uint32 words,
+    bit j & 31 of word j >> 5).  ``mask``: an ObservationMask, a boolean array,
+    or a boolean / uint8 CUDA tensor (a mask already resident in HBM).  The
+    bytes are packed on the device (``mlr_mask_pack``); a host mask crosses
+    PCIe as one byte per entry."""
     if mask is None:
         return None
-    obs = mask.observed if isinstance(mask, ObservationMask) else np.asarray(mask).astype(bool)
-    if rows is not None:
-        obs = obs[rows]
-    if obs.shape != tuple(shape):
-        raise ValueError("mask shape does not match data")
-    bits = ObservationMask(obs).packed_bits()
-    return torch.from_numpy(bits.view(np.int32)).to(device)
+    if isinstance(mask, torch.Tensor):
+        obs = mask if rows is None else mask[rows]
+        if obs.dtype not in (torch.bool, torch.uint8):
+            obs = obs != 0
+        if tuple(obs.shape) != tuple(shape):
+            raise ValueError("mask shape does not match data")
+        obs = obs.to(device).contiguous()
+    else:
+        obs = mask.observed if isinstance(mask, ObservationMask) else np.asarray(mask)
+        if obs.dtype != np.bool_:
+            obs = obs.astype(bool)
+        if rows is not None:
+            obs = obs[rows]
+        if obs.shape != tuple(shape):
+            raise ValueError("mask shape does not match data")
+        obs = torch.from_numpy(np.ascontiguousarray(obs).view(np.uint8)).to(device)
+    m, n = shape
+    words = (n + 31) // 32
+    bits = torch.empty((m, words), dtype=torch.int32, device=device)
+    if m:
+        with torch.cuda.device(device):
+            _lib.check(_lib.load().mlr_mask_pack(obs.data_ptr(), n, m, n, bits.data_ptr(), words,
+                                                 torch.cuda.current_stream().cuda_stream))
+    return bits
 
 
 def ml_fwt_solve(d, mask=None, opts=None):

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/mlr_b200.h): chain upload, plan creation over
 // caller workspace, and thin wrappers over the pcp.cu / cpcp.cu drivers.
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -814,6 +815,14 @@ int mlr_matrix_to_frames(const void* x, int64_t ldx, int f32, int count, int hei
     return kErrArg;
   }
   return matrix_to_frames(x, ldx, f32 != 0, count, height, width, frames, (cudaStream_t)stream);
+}
+int mlr_mask_pack(const uint8_t* observed, int64_t ld_observed, int64_t m, int64_t n, uint32_t* bits, int64_t ldm,
+                  void* stream) {
+  if (!observed || !bits || m < 0 || n < 1 || n > INT_MAX - 32 || ld_observed < n || ldm < (n + 31) / 32) {
+    set_error("mlr_mask_pack: invalid arguments");
+    return kErrArg;
+  }
+  return mask_pack(observed, ld_observed, m, (int)n, bits, ldm, (cudaStream_t)stream);
 }
 int mlr_chain_cholesky(void* chain, double* C, int64_t ldc, void* stream) {
   if (!chain || !C || ldc < ((Chain*)chain)->d.nh) {

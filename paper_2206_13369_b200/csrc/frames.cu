@@ -8,6 +8,8 @@
 // row a 2-D transpose between frames and columns, done in 32 x 32 tiles
 // through shared memory so both sides are coalesced.  Pure byte/streaming
 // work (HBM-bound): 1 byte read + sizeof(T) written per pixel on ingest.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace mlr {
@@ -77,6 +79,35 @@ int matrix_to_frames(const void* x, int64_t ldx, bool f32, int count, int H, int
   else
     matrix_to_frames_kernel<double><<<grid, block, 0, st>>>((const double*)x, ldx, count, H, W, frames);
   MLR_LAUNCH_CHECK("matrix_to_frames_kernel");
+  return kOk;
+}
+
+// Observation mask (reference cpcp.py:23-53: a boolean m x n array) -> the
+// bit-packed rows the ML-CPCP passes read: uint32 words, bit j & 31 of word
+// j >> 5, ldm words per row.  One warp per word: 32 coalesced byte loads, one
+// ballot, one store.  The host path it replaces (numpy packbits of the whole
+// mask on every solve) cost 31 ms of a 154 ms C4 solve.
+__global__ void __launch_bounds__(256) mask_pack_kernel(const uint8_t* __restrict__ obs, int64_t ldo, int64_t m,
+                                                        int n, uint32_t* __restrict__ bits, int64_t ldm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int words = (n + 31) >> 5;
+  const int64_t items = m * (int64_t)ldm;
+  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += warps) {
+    const int64_t row = it / ldm;
+    const int w = (int)(it - row * ldm);
+    const int j = w * 32 + lane;
+    const bool on = w < words && j < n && obs[row * ldo + j] != 0;
+    const uint32_t word = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) bits[it] = word;
+  }
+}
+
+int mask_pack(const uint8_t* obs, int64_t ldo, int64_t m, int n, uint32_t* bits, int64_t ldm, cudaStream_t st) {
+  const int64_t items = m * ldm;
+  const int grid = (int)std::min<int64_t>((items + 7) / 8, 148 * 16);
+  if (grid > 0) mask_pack_kernel<<<grid, 256, 0, st>>>(obs, ldo, m, n, bits, ldm);
+  MLR_LAUNCH_CHECK("mask_pack_kernel");
   return kOk;
 }
 

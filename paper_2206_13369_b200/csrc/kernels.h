@@ -34,6 +34,7 @@ bool gram128_ok(int n);  // the blocked Gram kernel handles width n (gemm_f64.cu
 
 // frame-stack layout (frames.cu)
 int frames_to_matrix(const uint8_t* frames, int count, int H, int W, bool f32, void* x, int64_t ldx, cudaStream_t st);
+int mask_pack(const uint8_t* obs, int64_t ldo, int64_t m, int n, uint32_t* bits, int64_t ldm, cudaStream_t st);
 int matrix_to_frames(const void* x, int64_t ldx, bool f32, int count, int H, int W, uint8_t* frames,
                      cudaStream_t st);
 int sum_slices(const double* P, int64_t count, int64_t slice, int slices, double* out, cudaStream_t st,

@@ -378,6 +378,39 @@ def test_ml_fwt_mask_shape_mismatch():
                          pkg.CpcpOptions(lambda_l=0.1, lambda_s=0.1, levels=4, collect_rank=False))
 
 
+@pytest.mark.parametrize("m,n", [(7, 1), (5, 31), (9, 32), (13, 33), (64, 1000), (3, 4100)])
+def test_mask_pack_bitwise(m, n):
+    """mlr_mask_pack (device) against ObservationMask.packed_bits (numpy
+    packbits, the layout the ML-CPCP passes read): bit-exact, from a host
+    boolean mask, an ObservationMask and a CUDA tensor."""
+    import torch
+    from paper_2206_13369_b200.cpcp import _mask_bits
+    rng = np.random.default_rng(m * 1000 + n)
+    obs = rng.random((m, n)) < 0.7
+    want = pkg.ObservationMask(obs).packed_bits().view(np.int32)
+    dev = torch.device("cuda", 0)
+    for src in (obs, pkg.ObservationMask(obs), torch.from_numpy(obs).to(dev), torch.from_numpy(obs.view(np.uint8)).to(dev)):
+        got = _mask_bits(src, (m, n), dev).cpu().numpy()
+        assert got.dtype == np.int32 and got.shape == want.shape
+        assert np.array_equal(got, want)
+    rows = slice(2, m - 1)
+    got = _mask_bits(obs, (m - 3, n), dev, rows).cpu().numpy()
+    assert np.array_equal(got, pkg.ObservationMask(obs[rows]).packed_bits().view(np.int32))
+
+
+def test_ml_fwt_device_mask_equals_host_mask():
+    """A mask resident on the device gives the same solve as the host mask."""
+    import torch
+    rng = np.random.default_rng(5)
+    d = (rng.standard_normal((96, 5)) @ rng.standard_normal((5, 80))).astype(np.float32)
+    obs = rng.random(d.shape) < 0.8
+    opts = pkg.CpcpOptions(lambda_l=0.3, lambda_s=0.05, levels=20, max_iters=40, collect_rank=False)
+    a = pkg.ml_fwt_solve(d, pkg.ObservationMask(obs), opts)
+    b = pkg.ml_fwt_solve(d, torch.from_numpy(obs).cuda(), opts)
+    assert a.iter == b.iter and a.objective_history == b.objective_history
+    assert np.array_equal(a.l, b.l) and np.array_equal(a.s, b.s)
+
+
 # ------------------------------------------------------------------ single operators
 @pytest.mark.parametrize("n,nh", [(500, 125), (101, 13), (64, 8), (33, 9)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
