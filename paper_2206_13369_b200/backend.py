@@ -79,6 +79,7 @@ class CudaPcp:
     """Device plan for ML-PCP over one row block of the iterate."""
 
     def __init__(self, chain, m_local, m_global, f32, max_iters, device):
+        self.h = None  # close() is safe even if the constructor fails below
         self.lib = _lib.load()
         self.device = torch.device(device)
         self.f32 = bool(f32)
@@ -229,6 +230,7 @@ class CudaCpcp:
     """Device plan for ML-CPCP over one row block."""
 
     def __init__(self, chain, m_local, m_global, row0, f32, max_iters, world, device):
+        self.h = None  # close() is safe even if the constructor fails below
         self.lib = _lib.load()
         self.device = torch.device(device)
         self.f32 = bool(f32)
@@ -366,6 +368,7 @@ class CudaSpectrum:
     reference's numerical-rank telemetry (spectrum plan of the C ABI)."""
 
     def __init__(self, m_local, n, f32, device, C=None, skip_ptr=None):
+        self.h = None  # close() is safe even if the constructor fails below
         self.lib = _lib.load()
         self.device = torch.device(device)
         lib = self.lib

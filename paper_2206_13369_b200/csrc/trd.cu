@@ -87,6 +87,20 @@ __device__ __forceinline__ double trd_div(double a, double bb) {
   return a * r;
 }
 
+// Sum of the TRD_W per-warp partials in shared memory: every thread loads
+// them (broadcast reads) and adds them in a fixed tree, ~80 cycles on the
+// step's dependency chain against ~250 for a 5-level shuffle butterfly.
+__device__ __forceinline__ double trd_sum16(const double* part) {
+  static_assert(TRD_W == 16, "trd_sum16 adds 16 partials");
+  const double2* p2 = reinterpret_cast<const double2*>(part);
+  double2 a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = p2[i];
+  const double s0 = (a[0].x + a[0].y) + (a[1].x + a[1].y), s1 = (a[2].x + a[2].y) + (a[3].x + a[3].y);
+  const double s2 = (a[4].x + a[4].y) + (a[5].x + a[5].y), s3 = (a[6].x + a[6].y) + (a[7].x + a[7].y);
+  return (s0 + s1) + (s2 + s3);
+}
+
 // The reflector that zeroes row[j+2..n) of the (replicated) row j + 1
 // (Householder, LAPACK dlarfg convention): beta, the new off-diagonal e and
 // the scale of v = row / (alpha - e).  s = sum of row[k]^2, k >= j + 2.
@@ -149,7 +163,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
   double* cur = ps + n;                // the replica of row j + 1
   double* psb = cur + n;               // CL: 2 x n, p by step parity (written by every CTA)
   double* nxt = psb + 2 * (size_t)n;   // CL: 2 x n, the next replica row by row parity
-  __shared__ double kpart[TRD_W], sqpart[TRD_W], s1part[TRD_W], s2part[TRD_W], s_bs[2];
+  __shared__ __align__(16) double kpart[TRD_W], sqpart[TRD_W], s1part[TRD_W], s2part[TRD_W], s_bs[2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (NQ == 0)
     for (int r = 0; r < R; ++r) {
@@ -447,7 +461,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     // (4) w_j = p - K v_j (the new pending update); the replica row j + 1
     //     through step j and its sum of squares beyond j + 2
     {
-      const double K = 0.5 * bet * warp_sum(lane < TRD_W ? kpart[lane] : 0.0);
+      const double K = 0.5 * bet * trd_sum16(kpart);
       const double vi = vc[m1];
       const double wi = fma(-K, vi, ps[m1]);
       double q = 0.0;
@@ -466,7 +480,7 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
     //     the two correction dots of the next matvec
     if (j + 1 < n - 2) {
       if (wid == 0) {
-        const double s = warp_sum(lane < TRD_W ? sqpart[lane] : 0.0);
+        const double s = trd_sum16(sqpart);
         if (lane == 0) {
           double bt, ej, sc;
           trd_reflector(cur[j + 2], s, bt, ej, sc);
