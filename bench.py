@@ -82,7 +82,7 @@ def _peaks():
 
 def _traffic(name):
     out = {}
-    for r in ("r03", "r04"):  # later captures override earlier ones
+    for r in ("r03", "r04", "r05"):  # later captures override earlier ones
         t = _json(os.path.join(ROOT, "profiles", f"{r}_traffic_{name.lower()}.json"))
         out.update((t or {}).get("kernels", {}))
     return out
