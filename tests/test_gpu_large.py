@@ -357,6 +357,26 @@ def test_lanczos_long_rows_sigma1(m, n):
     assert np.isclose(st.mu_history[0], 1.25 / s1, rtol=1e-8)
 
 
+def test_lanczos_long_rows_zeros_denormals_and_scales():
+    """The one-pass kernel widens every second element FP32 -> FP64 with
+    integer operations (exact for normal floats; zeros and denormals become
+    +-2^-127 (1 + m / 2^23), below 1.2e-38).  A matrix that is mostly exact
+    zeros, with denormal entries, negative zeros and entries spread over 60
+    binades must still give sigma_1 to the FP32 Lanczos tolerance."""
+    rng = np.random.default_rng(23)
+    m, n = 96, 4096
+    d = np.zeros((m, n), dtype=np.float32)
+    pick = rng.random((m, n)) < 0.03
+    d[pick] = (rng.standard_normal(pick.sum()) * np.exp2(rng.integers(-30, 30, pick.sum()))).astype(np.float32)
+    den = rng.random((m, n)) < 0.01
+    d[den] = (rng.integers(1, 1 << 22, den.sum()).astype(np.uint32)).view(np.float32)  # denormals
+    neg0 = rng.random((m, n)) < 0.01
+    d[neg0 & ~pick & ~den] = -0.0
+    st = pkg.ml_ialm_solve(d, pkg.PcpOptions(tol_feasibility=1e-6, max_iters=2))
+    s1 = np.linalg.norm(d.astype(np.float64), 2)
+    assert np.isclose(st.mu_history[0], 1.25 / s1, rtol=1e-8)
+
+
 # ------------------------------------------------------------------ tcgen05 3xTF32 GEMM
 @pytest.mark.parametrize("m,np_", [(300, 256), (1000, 1280), (129, 320), (64, 384)])
 def test_tcgen05_tf32x3_gemm_vs_fp64(m, np_):
