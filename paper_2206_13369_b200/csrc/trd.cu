@@ -798,6 +798,36 @@ __global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int 
 constexpr int TRD_BW = 8, TRD_BCH = 4, TRD_BST = 3;
 __device__ __forceinline__ uint32_t trd_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// z <- (I - beta h h^T) z for this warp's CPW vectors, register blocks
+// q >= Q0 only (Q0 <= q0: the blocks below hold rows <= j, where h is zero).
+template <int NQ, int CPW, int Q0>
+__device__ __forceinline__ void trd_back_apply(const double* __restrict__ h, int j, int n, int q0, int lane,
+                                               double bet, double (&z)[CPW][NQ]) {
+  if constexpr (Q0 < NQ) {
+    double acc[CPW];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) acc[u] = 0.0;
+    double hr[NQ - Q0];  // the reflector's entries, read from shared memory once for both passes
+#pragma unroll
+    for (int q = Q0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      hr[q - Q0] = (q >= q0 && i > j && i < n) ? h[i] : 0.0;
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) acc[u] = fma(hr[q - Q0], z[u][q], acc[u]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) acc[u] *= bet;
+#pragma unroll
+    for (int q = Q0; q < NQ; ++q)
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) z[u][q] = fma(-acc[u], hr[q - Q0], z[u][q]);
+  }
+}
+
 template <int NQ, int CPW>
 __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int n, int K, double* __restrict__ V,
                                                                    int ldv, const int* __restrict__ skip) {
@@ -867,27 +897,19 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
       if (bet == 0.0) continue;
       const double* h = bk_sm + ((size_t)st * TRD_BCH + r) * ldh;
       const int q0 = (j + 1) >> 5;  // lower q hold only rows <= j for every lane
-      double acc[CPW];
-#pragma unroll
-      for (int u = 0; u < CPW; ++u) acc[u] = 0.0;
-      double hr[NQ];  // the reflector's entries, read from shared memory once for both passes
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int i = lane + 32 * q;
-        hr[q] = (q >= q0 && i > j && i < n) ? h[i] : 0.0;
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) acc[u] = fma(hr[q], z[u][q], acc[u]);
+      // reflector j touches rows > j only: the register blocks below q0 are
+      // skipped at compile time in groups of 8 (static register indices;
+      // the group is uniform over the CTA and falls as j does)
+      switch (q0 >> 3) {
+        case 0: trd_back_apply<NQ, CPW, 0>(h, j, n, q0, lane, bet, z); break;
+        case 1: trd_back_apply<NQ, CPW, 8>(h, j, n, q0, lane, bet, z); break;
+        case 2: trd_back_apply<NQ, CPW, 16>(h, j, n, q0, lane, bet, z); break;
+        case 3: trd_back_apply<NQ, CPW, 24>(h, j, n, q0, lane, bet, z); break;
+        case 4: trd_back_apply<NQ, CPW, 32>(h, j, n, q0, lane, bet, z); break;
+        case 5: trd_back_apply<NQ, CPW, 40>(h, j, n, q0, lane, bet, z); break;
+        case 6: trd_back_apply<NQ, CPW, 48>(h, j, n, q0, lane, bet, z); break;
+        default: trd_back_apply<NQ, CPW, 56>(h, j, n, q0, lane, bet, z); break;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
-#pragma unroll
-      for (int u = 0; u < CPW; ++u) acc[u] *= bet;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) z[u][q] = fma(-acc[u], hr[q], z[u][q]);
     }
     __syncthreads();  // stage st consumed by every warp
     if (threadIdx.x == 0 && ch + TRD_BST < nch) issue(ch + TRD_BST);
