@@ -872,6 +872,8 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int ch = 0; ch < TRD_BST && ch < nch; ++ch) issue(ch);
   }
+  double* bk_beta = bk_sm + (size_t)TRD_BST * TRD_BCH * ldh;  // all n reflector scalars
+  for (int i = threadIdx.x; i < n; i += blockDim.x) bk_beta[i] = b.beta[i];
   double z[CPW][NQ];
 #pragma unroll
   for (int u = 0; u < CPW; ++u)
@@ -893,7 +895,7 @@ __global__ void __launch_bounds__(TRD_BW * 32, 1) trd_back_kernel(TrdBuf b, int 
     for (int r = 0; r < TRD_BCH; ++r) {
       const int j = jtop - r;
       if (j < 0) break;
-      const double bet = __ldg(b.beta + j);
+      const double bet = bk_beta[j];  // staged once: a global load here sits on every reflector's chain
       if (bet == 0.0) continue;
       const double* h = bk_sm + ((size_t)st * TRD_BCH + r) * ldh;
       const int q0 = (j + 1) >> 5;  // lower q hold only rows <= j for every lane
@@ -1013,7 +1015,7 @@ bool trd_supported(int n) {
   if (G > TRD_MAXG) return false;
   const int R = (n + G - 1) / G;
   const size_t smem = 8 * ((size_t)R * n + 5 * (size_t)n);
-  return smem <= 224 * 1024 && 8 * 12 * (size_t)(n + 1) <= 200 * 1024 && 32 * (size_t)n <= 200 * 1024;
+  return smem <= 224 * 1024 && 8 * 13 * (size_t)(n + 2) <= 224 * 1024 && 32 * (size_t)n <= 200 * 1024;
 }
 
 // Eigenpairs of B (n x n in the leading block of an np x np buffer) above
@@ -1084,7 +1086,7 @@ int trd_eig(PcpDev* st, TrdBuf* b, double* Bm, double* V, int n, int np, const d
   const char* cpe = getenv("MLR_TRD_BACK_CPW");
   const int cpw = cpe ? std::max(1, std::min(2, atoi(cpe))) : 1;  // 2 measured slower at C5 (spills)
   const int bg = (n + TRD_BW * cpw - 1) / (TRD_BW * cpw);
-  const size_t bsm = 8 * (size_t)TRD_BST * TRD_BCH * ((n + 1) & ~1);
+  const size_t bsm = 8 * ((size_t)TRD_BST * TRD_BCH + 1) * ((n + 1) & ~1);  // reflector ring + the n betas
 #define TRD_BACK(NQ)                                                                                \
   if (nq <= NQ) {                                                                                   \
     if (cpw == 2) {                                                                                 \
