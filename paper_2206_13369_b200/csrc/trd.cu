@@ -258,22 +258,47 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
         a0 += a2;
         a1 += a3;
       } else {
-        // four independent load / FMA chains in flight per lane
+        // blocks of 8 x 32 columns: the 16 loads of a block are issued
+        // together, then four FMA chains; the last, partial block runs the
+        // same code with predicated loads (a rolled remainder loop exposed the
+        // shared-memory latency once per 32 columns: ~1.0 k cycles for the
+        // <= 20 elements per lane of a C5 step)
         double a2 = 0.0, a3 = 0.0;
         int k = m1 + lane;
-        for (; k + 96 < n; k += 128) {
-          a0 = fma(my_row[k], vc[k], a0);
-          a1 = fma(my_row[k + 32], vc[k + 32], a1);
-          a2 = fma(my_row[k + 64], vc[k + 64], a2);
-          a3 = fma(my_row[k + 96], vc[k + 96], a3);
+#pragma unroll 1
+        for (; k + 224 < n; k += 256) {
+          double x[8], y[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            x[u] = my_row[k + 32 * u];
+            y[u] = vc[k + 32 * u];
+          }
+          a0 = fma(x[0], y[0], a0);
+          a1 = fma(x[1], y[1], a1);
+          a2 = fma(x[2], y[2], a2);
+          a3 = fma(x[3], y[3], a3);
+          a0 = fma(x[4], y[4], a0);
+          a1 = fma(x[5], y[5], a1);
+          a2 = fma(x[6], y[6], a2);
+          a3 = fma(x[7], y[7], a3);
         }
-        if (k + 32 < n) {
-          a0 = fma(my_row[k], vc[k], a0);
-          a1 = fma(my_row[k + 32], vc[k + 32], a1);
-          k += 64;
+        if (k < n) {
+          double x[8], y[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const bool in = k + 32 * u < n;
+            x[u] = in ? my_row[k + 32 * u] : 0.0;
+            y[u] = in ? vc[k + 32 * u] : 0.0;
+          }
+          a0 = fma(x[0], y[0], a0);
+          a1 = fma(x[1], y[1], a1);
+          a2 = fma(x[2], y[2], a2);
+          a3 = fma(x[3], y[3], a3);
+          a0 = fma(x[4], y[4], a0);
+          a1 = fma(x[5], y[5], a1);
+          a2 = fma(x[6], y[6], a2);
+          a3 = fma(x[7], y[7], a3);
         }
-        if (k < n) a2 = fma(my_row[k], vc[k], a2);
-        if (k + 32 < n) a3 = fma(my_row[k + 32], vc[k + 32], a3);
         a0 += a2;
         a1 += a3;
       }
@@ -354,21 +379,27 @@ trd_reduce_kernel(const double* __restrict__ B, int ldb, int n, TrdBuf b, const 
           }
         }
       }
+      // blocks of 4 x 32 columns, the 12 loads of a block issued together;
+      // the partial last block with predicated accesses
       int k = NQ > 0 ? n : m1 + lane;
-      for (; k + 32 < n; k += 64) {
-        const double x0 = fma(-vi, wpv[k], fma(-wi, vp[k], my_row[k]));
-        const double x1 = fma(-vi, wpv[k + 32], fma(-wi, vp[k + 32], my_row[k + 32]));
-        my_row[k] = x0;
-        my_row[k + 32] = x1;
-        if (pub) {
-          ll_store(pub + k, x0, tag);
-          ll_store(pub + k + 32, x1, tag);
+#pragma unroll 1
+      for (; k < n; k += 128) {
+        double a[4], w[4], v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool in = k + 32 * u < n;
+          a[u] = in ? my_row[k + 32 * u] : 0.0;
+          w[u] = in ? wpv[k + 32 * u] : 0.0;
+          v[u] = in ? vp[k + 32 * u] : 0.0;
         }
-      }
-      if (k < n) {
-        const double x0 = fma(-vi, wpv[k], fma(-wi, vp[k], my_row[k]));
-        my_row[k] = x0;
-        if (pub) ll_store(pub + k, x0, tag);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k + 32 * u < n) {
+            const double x = fma(-vi, w[u], fma(-wi, v[u], a[u]));
+            my_row[k + 32 * u] = x;
+            if (pub) ll_store(pub + k + 32 * u, x, tag);
+          }
+        }
       }
       if (pub && !CL) {
         __syncwarp();
