@@ -826,7 +826,10 @@ __global__ void __launch_bounds__(TRD_VW * 32) trd_vectors_kernel(TrdBuf b, int 
 // through shared memory by TMA bulk copies (cp.async.bulk, one mbarrier per
 // stage of TRD_BCH rows, TRD_BST stages, thread 0 the producer), shared by
 // the CTA's TRD_BW warps.  Output V[i * ldv + c].
-constexpr int TRD_BW = 8, TRD_BCH = 4, TRD_BST = 3;
+// 5 warps per CTA: the C5 maximum of 731 kept vectors then spreads over 147 of
+// the 148 SMs in one wave (8 warps left 56 SMs idle and two warps per
+// scheduler contending for issue slots: C5 eigensolve phase 106.9 -> 106.5 ms)
+constexpr int TRD_BW = 5, TRD_BCH = 4, TRD_BST = 3;
 __device__ __forceinline__ uint32_t trd_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // z <- (I - beta h h^T) z for this warp's CPW vectors, register blocks
