@@ -17,6 +17,7 @@ D = torch.from_numpy(d).cuda()
 opts = pkg.PcpOptions(lam=1 / np.sqrt(max(m, n)), tol_feasibility=c['tol'], levels=c['n_coarse'])
 chain = build_chain(n, P._checked_width(n, m, opts))
 be = CudaPcp(chain, m, m, True, opts.max_iters, D.device)
+be.set_timing(True)  # the library's own phase timer, read at the end
 st3 = be.input_stats(D)
 be.lanczos_init()
 if be.lanczos_run_available():
@@ -69,4 +70,6 @@ for i in range(12):
 torch.cuda.synchronize()
 ts = [a.elapsed_time(b) for a, b in pairs]
 print(name, 'gram inside 12 queued iterations (svt, update, gram, finalize):', ' '.join('%.3f' % t for t in ts))
+t = be.timing()
+print(name, 'library phase timer:', {k: (round(v[0], 3), v[1], round(v[0] / max(v[1], 1), 4)) for k, v in t.items() if isinstance(v, tuple)})
 be.close()
